@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark of the BoxMG V(2,1) cycle (BASELINE.json metric) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl reference]
+
+A step is one V(2,1) cycle of the whole hot path (all levels, fine-level
+relaxation through the coarsest Cholesky solve and back) on the N=1 workload
+of BASELINE.json configs[3]: 2-D 5-point Poisson on 8193^2 (8191^2 interior
+unknowns), f = h^2, x0 = 0.  Inputs (every level-0 array is 537 MB) are larger
+than the 126 MB L2, so no explicit L2 flush is needed between steps.
+
+Prints ONE JSON line on rank 0.  See DESIGN.md §8 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "V(2,1) cycles/s and Munknowns/s at 8193^2; HBM GB/s vs peak; 1/2/4/8 GPU"
+
+CONFIGS = {
+    # name: (workload, nx, ny, description)
+    "poisson8193": ("poisson", 8191, 8191, "2D 5-point Poisson 8193^2 (8191^2 interior), V(2,1), f=h^2, x0=0"),
+    "checker1025": ("checker", 1023, 1023, "2D 5-point 1e6 checkerboard (8x8 coarse-aligned blocks) 1025^2"),
+    "aniso4097": ("aniso", 4095, 4095, "2D 9-point Q1 anisotropic eps=1e-3 4097^2"),
+    "checker4096": ("checker512", 4095, 4095, "2D 5-point 512-cell 1e6 checkerboard 4096^2 per GPU"),
+}
+
+
+def model_bytes(nx, ny, kind, L, fused_levels):
+    """Algorithmic bytes per V(2,1) cycle.
+
+    model B: (4s+19.5) N_l doubles per non-coarsest level; model A (two fused
+    passes, CI stored): (2s+10.5) N_l.  s = 3 (5-pt level 0) or 5 (9-pt)."""
+    B = A = 0.0
+    for l in range(L - 1):
+        s = 3 if (l == 0 and kind == 5) else 5
+        N = float(nx) * float(ny)
+        B += (4 * s + 19.5) * N * 8
+        A += (2 * s + 10.5) * N * 8
+        nx, ny = nx // 2, ny // 2
+    return B, A
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._th = threading.Thread(target=self._read, daemon=True)
+            self._th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def mark(self, which):
+        setattr(self, which, time.time())
+
+    def stop(self):
+        if self.proc is not None:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [r for t, r in self.rows if self.t0 is not None and self.t0 - 0.06 <= t <= self.t1 + 0.06]
+        if not rows:
+            rows = [r for _, r in self.rows]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        import statistics
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [num(r[1]) for r in rows if num(r[1]) is not None]
+        mx = [num(r[2]) for r in rows if num(r[2]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if len(r) > 4 + k and r[4 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def host_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return model, os.cpu_count()
+
+
+# ------------------------------------------------------------------ oracle (CPU) legs
+ORACLE_SAMPLE_N = 2047
+
+
+def oracle_cycles_per_s(wl, nx, ny, ncycles, warm=1):
+    """Time the oracle V(2,1) on a bounded sample (n=2047, 1/16 of the 8191^2
+    unknowns); returns (cycles/s scaled to the full workload, sample string)."""
+    import numpy as np
+
+    import oracle
+    from paper_2502_05279_b200 import problems as P
+
+    n = ORACLE_SAMPLE_N
+    st = P.workload(wl, n, n)
+    f = P.rhs_const(n, n)
+    h = oracle.Hierarchy(st)
+    u = np.zeros_like(f)
+    for _ in range(warm):
+        u = h.vcycle(f, u, 1)
+    t = time.perf_counter()
+    u = h.vcycle(f, u, ncycles)
+    dt = time.perf_counter() - t
+    scale = (n * n) / (float(nx) * float(ny))
+    per_cycle = dt / ncycles
+    return ncycles / dt * scale, per_cycle, (f"oracle V(2,1) on {wl} {n}x{n} (same recipe, {n*n/(nx*ny):.4f} of the "
+                                             f"{nx}x{ny} unknowns), {ncycles} timed cycles after {warm} warm-up, "
+                                             f"setup untimed; cycles/s scaled by the unknown ratio to {nx}x{ny}")
+
+
+def run_reference(args, cfg):
+    """--impl reference: the oracle (this tier's reference arm), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    wl, nx, ny, desc = CONFIGS[cfg]
+    model, cores = host_info()
+    val, per_cycle, sample = oracle_cycles_per_s(wl, nx, ny, args.steps, warm=args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "cycles/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_cycle * 1e3 * (nx * ny) / ORACLE_SAMPLE_N ** 2,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "nx": nx, "ny": ny, "cycle": "V(2,1)"},
+        "munknowns_per_s": val * nx * ny / 1e6,
+        "cpu_baseline": {"value": val, "unit": "cycles/s", "cores": 1, "kind": "oracle", "sample": sample,
+                         "host_cpu": model, "host_cores": cores},
+        "e2e": {"value": val, "unit": "cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="poisson8193", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--unfused", action="store_true", help="one kernel per method step (debug/comparison)")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args, args.config)
+
+    import numpy as np
+    import torch
+
+    from paper_2502_05279_b200 import bmg, problems as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    wl, nx, ny, desc = CONFIGS[args.config]
+    st = P.workload(wl, nx, ny)
+    prm = bmg.bmg_params_default()
+    prm.fused = 0 if args.unfused else 1
+    solver = bmg.Solver(st, prm)
+    del st
+    f = solver.grid(P.rhs_const(nx, ny))
+    x = solver.grid()
+    L = solver.L
+    kind = bmg.bmg_level_shape(solver.h, 0)[2]
+    stream = torch.cuda.current_stream()
+
+    # warm-up (untimed): builds and caches the CUDA graph
+    solver.vcycle(f, x, args.warmup)
+    torch.cuda.synchronize()
+    kpc = bmg.bmg_cycle_kernel_count(solver.h)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.mark("t0")
+    ev0.record(stream)
+    solver.vcycle(f, x, args.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks.mark("t1")
+    if dist:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clocks.stop()
+    ms_per_step = ms / args.steps
+    cycles_per_s = world * args.steps / (ms / 1e3)
+
+    # roofline: the dominant kernel group = level-0 down leg (smooth+residual+restrict),
+    # launched alone through the ABI step call, CUDA events on its stream.
+    peak, peak_src = measured_peaks()
+    rl = roofline(solver, bmg, torch, f, x, nx, ny, kind, peak, peak_src, ms_per_step, args)
+
+    # convergence sanity of the timed run (residual keeps falling / at rounding floor)
+    rnorm = solver.residual_norm(f, x)
+    fnorm = float(torch.linalg.vector_norm(f))
+
+    # e2e: same metric through the public API with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if args.e2e_steps > 0:
+        fh = f.cpu().pin_memory()
+        xh = torch.zeros_like(fh).pin_memory()
+        bmg.bmg_vcycle_host(solver.h, fh, xh, 1)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            bmg.bmg_vcycle_host(solver.h, fh, xh, 1)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        nbytes = fh.numel() * 8
+        e2e = {"value": world * args.e2e_steps / dt, "unit": "cycles/s", "h2d_bytes_per_step": 2 * nbytes,
+               "d2h_bytes_per_step": nbytes,
+               "note": "bmg_vcycle_host: H2D rhs+x (pinned), 1 V(2,1) cycle, D2H x, per step; host wall clock"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        val, per_cycle, sample = oracle_cycles_per_s(wl, nx, ny, 8, warm=1)
+        model, cores = host_info()
+        cpu = {"value": val, "unit": "cycles/s", "cores": 1, "kind": "oracle", "sample": sample,
+               "host_cpu": model, "host_cores": cores}
+
+    B, A = model_bytes(nx, ny, kind, L, 0)
+    cs = clocks.summary()
+    line = {
+        "metric": METRIC,
+        "value": cycles_per_s,
+        "unit": "cycles/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": desc, "nx": nx, "ny": ny, "levels": L, "cycle": "V(2,1)",
+                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (one problem per GPU)",
+                   "l2": "inputs > L2 (level-0 arrays 537 MB each); no flush needed",
+                   "fused": bool(prm.fused)},
+        "munknowns_per_s": cycles_per_s * nx * ny / 1e6,
+        "model_B_GBps": B / (ms_per_step / 1e3) / 1e9,
+        "model_B_frac": B / (ms_per_step / 1e3) / 1e9 / peak,
+        "model_A_frac": A / (ms_per_step / 1e3) / 1e9 / peak,
+        "final_rel_residual": rnorm / fnorm,
+        "gpu_launches": kpc * args.steps,
+        "kernels_per_cycle": kpc,
+        "roofline": rl,
+        "clocks": {"sm_mhz": cs["sm_mhz"], "sm_max_mhz": cs["sm_max_mhz"], "reasons": cs["reasons"],
+                   "samples": cs["samples"]},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def roofline(solver, bmg, torch, f, x, nx, ny, kind, peak, peak_src, ms_per_step, args):
+    """Dominant kernel: the level-0 down leg.  Algorithmic bytes per launch =
+    per-fine-unknown bytes x nx*ny."""
+    stream = torch.cuda.current_stream()
+    fc = solver.level_grid(1)
+    uc = solver.level_grid(1)
+    u = x.clone()
+    nrep = 20
+    for _ in range(3):
+        bmg.bmg_smooth_restrict(solver.h, 0, f, u, fc, uc)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(nrep):
+        bmg.bmg_smooth_restrict(solver.h, 0, f, u, fc, uc)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    dur_ms = ev0.elapsed_time(ev1) / nrep
+    s_planes = 3 if kind == 5 else 5
+    # compulsory bytes of the down leg per fine unknown: read u, f and the
+    # s operator planes, write u, read the 2N-double CI planes, write f_c and zero u_c (N/4 each)
+    per_unk = 8.0 * (s_planes + 2 + 1 + 2 + 0.25 + 0.25)
+    algo = per_unk * nx * ny
+    achieved = algo / (dur_ms / 1e3) / 1e9
+    return {"bound": "hbm", "kernel": "level-0 down leg (bmg_smooth_restrict: nu1 GS sweeps + residual + "
+                                      "restriction)", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+            "algorithmic_bytes_per_unknown": per_unk, "launch_ms": dur_ms,
+            "share_of_step": dur_ms / ms_per_step}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,182 @@
+/*
+ * include/bmg.h -- C ABI of the B200-native BoxMG V-cycle library (libbmg.so).
+ *
+ * The problem (Eq. (1)): -div(D grad u) = f discretised by
+ * a "standard finite-difference scheme which leads to a stencil-based
+ * description of the resulting linear system, Ax = b", where the stencil
+ * "may be different at each point" (fig:stencil_operator).  The
+ * solver is the BoxMG V-cycle of fig:vcycle_flowchart: Gauss-Seidel
+ * relaxation, residual, operator-induced restriction (fig:restrict_kernel,
+ * P:165-189) and interpolation, Cholesky coarse solve, driven
+ * by a setup that builds operator-induced interpolation and Galerkin coarse
+ * operators "through local stencil operations".  The readings of
+ * everything the paper leaves to Dendy/Reisner are listed in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *  - Every array is IEEE fp64, row-major, x fastest.  A grid function g of an
+ *    nx*ny interior has element (i,j) at g[j*pitch + i], i in [0,nx+1],
+ *    j in [0,ny+1]; the interior is [1,nx]x[1,ny]; the ring is the
+ *    homogeneous Dirichlet ghost.  Ring values of inputs are ignored, ring
+ *    values of outputs are written as 0 only where stated.
+ *  - Unless stated otherwise, pointers are DEVICE pointers on the current
+ *    CUDA device, must not alias each other, and stay owned by the caller.
+ *  - `cuda_stream` is a cudaStream_t (NULL = legacy default stream).  All
+ *    work is enqueued on it; calls that return host values synchronise it.
+ *  - Errors are returned as bmg_status_t; nothing is thrown across the ABI.
+ *    bmg_last_error_detail() gives thread-local text for the last failure.
+ *  - A solver handle is used by one host thread at a time.
+ */
+#ifndef BMG_H
+#define BMG_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bmg_solver *bmg_solver_t; /* opaque, library-owned */
+
+typedef enum {
+    BMG_OK = 0,
+    BMG_EINVAL = 1,   /* bad sizes/pointers/kind, a_O <= 0, interpolation denominator <= 0 */
+    BMG_ENOMEM = 2,   /* device allocation failed */
+    BMG_ECUDA = 3,    /* CUDA runtime error (detail in bmg_last_error_detail) */
+    BMG_ENCCL = 4,    /* reserved for the multi-GPU path */
+    BMG_ENOTSPD = 5,  /* coarsest-level Cholesky pivot <= 0 */
+    BMG_ENOTCONV = 6  /* bmg_solve reached maxiter; x and hist stay valid */
+} bmg_status_t;
+
+/*
+ * The fine-level operator, stored as its symmetric half with matrix-entry
+ * signs (D == 1 gives O=4, W=S=-1):
+ *   plane[0] = O  (diagonal),        plane[1] = W = A[p, p-(1,0)],
+ *   plane[2] = S  = A[p, p-(0,1)],   plane[3] = SW = A[p, p-(1,1)]  (kind 9),
+ *   plane[4] = NW = A[p, p+(-1,1)]   (kind 9).
+ * The other half follows by symmetry: E(i,j)=W(i+1,j), N(i,j)=S(i,j+1),
+ * NE(i,j)=SW(i+1,j+1), SE(i,j)=NW(i+1,j-1).  Each plane is a grid function
+ * with `pitch` elements per row; entries on the ghost ring and couplings that
+ * point into the ring are dropped (Dirichlet elimination).
+ * Plane pointers are DEVICE pointers, read only during bmg_setup (copied).
+ */
+typedef struct {
+    int kind;              /* 5 -> planes {O,W,S}; 9 -> planes {O,W,S,SW,NW} */
+    int nx, ny;            /* interior sizes, >= 1 */
+    long long pitch;       /* elements per row, >= nx+2; also the pitch of rhs/x */
+    const double *plane[5];
+} bmg_stencil_t;
+
+typedef struct {
+    int nu1, nu2;    /* pre-/post-smoothing sweeps, default 2, 1 (V(2,1)) */
+    int coarsest;    /* stop coarsening when min(nx,ny) <= coarsest; default 3 */
+    int max_levels;  /* 0 = unlimited */
+    int agglom_rows; /* multi-GPU: agglomerate below this many rows per rank (default 128) */
+    int cycle_sym;   /* 0 = same colour order on both legs (default); 1 reserved */
+    int fused;       /* 1 = fused streaming kernels on large levels (default), 0 = one kernel per step */
+} bmg_params_t;
+
+/* Fill *p with the defaults above. */
+void bmg_params_default(bmg_params_t *p);
+
+/*
+ * Setup (fig:vcycle_flowchart's setup phase): copy the stencil
+ * (S0), then on every level l < L-1 build the operator-induced interpolation
+ * weights (S1, DESIGN §3 c3) and the Galerkin operator A_{l+1} = P^T A_l P
+ * (S2, c4); factor the coarsest level densely by Cholesky (S3, c8).
+ * Levels: n_{l+1} = floor(n_l/2) until min(nx,ny) <= coarsest (c1).
+ * params may be NULL (defaults).  On success *out owns all device memory.
+ * Errors: EINVAL (sizes, kind, pitch, a_O <= 0, den <= 0), ENOMEM, ENOTSPD,
+ * ECUDA.  Synchronises cuda_stream.
+ */
+bmg_status_t bmg_setup(const bmg_stencil_t *stencil, const bmg_params_t *params, void *cuda_stream,
+                       bmg_solver_t *out);
+
+/*
+ * ncycles V(nu1,nu2) cycles (fig:vcycle_flowchart) on the fine
+ * level: x <- V(x) with right-hand side rhs.  rhs, x: device grid functions
+ * with the setup pitch; x is read (initial guess) and overwritten.  Ring of x
+ * is not written.  Asynchronous (no host sync).  The cycle is replayed as a
+ * CUDA graph cached per (rhs, x) pointer pair.
+ */
+bmg_status_t bmg_vcycle(bmg_solver_t h, const double *rhs, double *x, int ncycles, void *cuda_stream);
+
+/*
+ * Same as bmg_vcycle, but rhs_host / x_host are HOST arrays (pinned or
+ * pageable) with the setup pitch: copies rhs and x host->device, runs the
+ * cycles, copies x device->host.  Synchronises cuda_stream.
+ */
+bmg_status_t bmg_vcycle_host(bmg_solver_t h, const double *rhs_host, double *x_host, int ncycles,
+                             void *cuda_stream);
+
+/*
+ * Solve loop: hist[0] = ||rhs - A x0||_2; repeat V-cycles
+ * until ||r_k||_2 <= tol*||rhs||_2 or maxiter cycles.  ||rhs|| = 0 sets
+ * x = 0 (interior) and returns 0 iterations.  iters_out (host, may be NULL)
+ * receives the cycle count; hist_host (host, maxiter+1 doubles, may be NULL)
+ * the absolute residual norms.  Returns ENOTCONV if maxiter was reached.
+ */
+bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol, int maxiter, int *iters_out,
+                       double *hist_host, void *cuda_stream);
+
+/* ||rhs - A x||_2 over the fine interior ("l2 norm"), deterministic
+ * fixed-tree reduction; optional r_out (device, setup pitch, ring untouched)
+ * receives the residual.  *norm_host is a host double.  Synchronises. */
+bmg_status_t bmg_residual_norm(bmg_solver_t h, const double *rhs, const double *x, double *r_out,
+                               double *norm_host, void *cuda_stream);
+
+/* Hierarchy queries (host outputs). */
+bmg_status_t bmg_num_levels(bmg_solver_t h, int *L);
+bmg_status_t bmg_level_shape(bmg_solver_t h, int level, int *nx, int *ny, int *kind);
+/* Elements per row of level `level`'s grid functions (level 0: the setup pitch). */
+bmg_status_t bmg_level_pitch(bmg_solver_t h, int level, long long *pitch);
+
+/*
+ * Copy level `level`'s operator and interpolation weights to HOST memory, for
+ * tests.  stencil_host: 5 planes (O,W,S,SW,NW), each (ny+2)*(nx+2) with pitch
+ * nx+2 (SW,NW are 0 on a 5-point level).  ci_host (may be NULL; ignored on
+ * the coarsest level): 8 planes LNE,LA,LNW,LR,LL,LSE,LB,LSW (fig:restrict_kernel
+ * names), each (ncy+2)*(ncx+2) with pitch ncx+2, ncx = nx/2, ncy = ny/2.
+ * Synchronises the legacy stream.
+ */
+bmg_status_t bmg_export_level(bmg_solver_t h, int level, double *stencil_host, double *ci_host);
+
+/*
+ * Single method steps on one level, for per-kernel parity tests.  All arrays
+ * are device grid functions of that level with bmg_level_pitch(level); for
+ * restriction/interpolation the coarse array uses bmg_level_pitch(level+1).
+ *  bmg_relax:      nsweeps multicolour GS sweeps (c6), u in/out.
+ *  bmg_residual:   r = f - A u on the interior; r's ring set to 0.
+ *  bmg_restrict:   fc = P^T r, the fig:restrict_kernel listing (c5); ring 0.
+ *  bmg_interp_add: u += P ec (c7); ec's ring must be 0.
+ * Asynchronous.
+ */
+bmg_status_t bmg_relax(bmg_solver_t h, int level, const double *f, double *u, int nsweeps, void *cuda_stream);
+bmg_status_t bmg_residual(bmg_solver_t h, int level, const double *f, const double *u, double *r,
+                          void *cuda_stream);
+bmg_status_t bmg_restrict(bmg_solver_t h, int level, const double *r, double *fc, void *cuda_stream);
+bmg_status_t bmg_interp_add(bmg_solver_t h, int level, const double *ec, double *u, void *cuda_stream);
+
+/*
+ * The two legs of one level of the V-cycle, as the cycle runs them (the fused
+ * streaming kernel where the level is fused, else the per-step kernels):
+ *  bmg_smooth_restrict: nu1 GS sweeps on (f,u), then fc = P^T (f - A u) and,
+ *                       if uc != NULL, uc = 0 (the coarse correction's start).
+ *  bmg_correct_smooth:  u += P ec, then nu2 GS sweeps.
+ * fc, uc, ec use bmg_level_pitch(level+1).  Asynchronous.
+ */
+bmg_status_t bmg_smooth_restrict(bmg_solver_t h, int level, const double *f, double *u, double *fc, double *uc,
+                                 void *cuda_stream);
+bmg_status_t bmg_correct_smooth(bmg_solver_t h, int level, const double *f, double *u, const double *ec,
+                                void *cuda_stream);
+
+/* Number of kernels one bmg_vcycle cycle launches (the captured graph's kernel nodes). */
+bmg_status_t bmg_cycle_kernel_count(bmg_solver_t h, int *count);
+
+/* Free everything owned by the handle (synchronises the device). NULL is OK. */
+bmg_status_t bmg_destroy(bmg_solver_t h);
+
+const char *bmg_strerror(bmg_status_t s);
+const char *bmg_last_error_detail(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BMG_H */

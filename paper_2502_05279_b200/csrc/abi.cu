@@ -1,0 +1,559 @@
+// abi.cu -- the extern "C" boundary of libbmg.so (include/bmg.h): hierarchy
+// construction (setup), CUDA-graph-captured V-cycles, the solve loop, and the
+// single-step entry points used by the parity tests.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "bmg.h"
+#include "bmg_internal.cuh"
+#include "fused.cuh"
+
+using namespace bmg;
+
+namespace {
+
+thread_local std::string g_detail;
+
+bmg_status_t fail(bmg_status_t s, const std::string &msg)
+{
+    g_detail = msg;
+    return s;
+}
+
+#define CK(call)                                                                                    \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return fail(e_ == cudaErrorMemoryAllocation ? BMG_ENOMEM : BMG_ECUDA,                   \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                        \
+    } while (0)
+
+struct Level {
+    int nx = 0, ny = 0, kind = 5;
+    long long pitch = 0;
+    double *pl[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // O W S SW NW
+    double *u = nullptr, *f = nullptr, *r = nullptr;                // u,f unused on level 0
+    double *ci[8] = {nullptr};                                       // weights from level l+1 (coarse pitch)
+    Op op() const
+    {
+        Op A;
+        A.nx = nx;
+        A.ny = ny;
+        A.kind = kind;
+        A.pitch = pitch;
+        A.O = pl[0];
+        A.W = pl[1];
+        A.S = pl[2];
+        A.SW = pl[3];
+        A.NW = pl[4];
+        return A;
+    }
+};
+
+long long round_pitch(int nx) { return ((long long)nx + 2 + 31) / 32 * 32; }
+
+}  // namespace
+
+struct bmg_solver {
+    bmg_params_t prm;
+    int L = 0;
+    std::vector<Level> lv;
+    std::vector<void *> allocs;
+    double *chol = nullptr;  // coarsest factor
+    int nco = 0;
+    int *d_err = nullptr;
+    double *partials = nullptr, *d_norm = nullptr, *h_norm = nullptr;  // h_norm pinned
+    double *stage_f = nullptr, *stage_x = nullptr;                     // bmg_vcycle_host staging
+    cudaStream_t cap = nullptr;                                        // capture stream
+    std::map<std::pair<const void *, const void *>, cudaGraphExec_t> graphs;
+    int kernels_per_cycle = 0;
+    FusedPlan fplan;
+
+    CIv civ(int l) const
+    {
+        CIv v;
+        v.pitch = lv[l + 1].pitch;
+        for (int k = 0; k < 8; k++)
+            v.w[k] = lv[l].ci[k];
+        return v;
+    }
+};
+
+static bmg_status_t dalloc(bmg_solver *h, double **p, size_t n)
+{
+    void *q = nullptr;
+    CK(cudaMalloc(&q, n * sizeof(double)));
+    h->allocs.push_back(q);
+    *p = (double *)q;
+    return BMG_OK;
+}
+
+#define TRY(x)                    \
+    do {                          \
+        bmg_status_t s_ = (x);    \
+        if (s_ != BMG_OK)         \
+            return s_;            \
+    } while (0)
+
+extern "C" {
+
+void bmg_params_default(bmg_params_t *p)
+{
+    p->nu1 = 2;
+    p->nu2 = 1;
+    p->coarsest = 3;
+    p->max_levels = 0;
+    p->agglom_rows = 128;
+    p->cycle_sym = 0;
+    p->fused = 1;
+}
+
+const char *bmg_strerror(bmg_status_t s)
+{
+    switch (s) {
+    case BMG_OK: return "ok";
+    case BMG_EINVAL: return "invalid argument or operator";
+    case BMG_ENOMEM: return "out of device memory";
+    case BMG_ECUDA: return "CUDA error";
+    case BMG_ENCCL: return "NCCL error";
+    case BMG_ENOTSPD: return "coarsest operator not SPD (Cholesky pivot <= 0)";
+    case BMG_ENOTCONV: return "not converged within maxiter";
+    }
+    return "unknown status";
+}
+
+const char *bmg_last_error_detail(void) { return g_detail.c_str(); }
+
+bmg_status_t bmg_destroy(bmg_solver_t h)
+{
+    if (!h)
+        return BMG_OK;
+    cudaDeviceSynchronize();
+    for (auto &kv : h->graphs)
+        cudaGraphExecDestroy(kv.second);
+    for (void *p : h->allocs)
+        cudaFree(p);
+    if (h->h_norm)
+        cudaFreeHost(h->h_norm);
+    if (h->cap)
+        cudaStreamDestroy(h->cap);
+    delete h;
+    return BMG_OK;
+}
+
+static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStream_t s)
+{
+    const bmg_params_t &pr = h->prm;
+    // level ladder (c1): n_{l+1} = floor(n_l/2) until min(nx,ny) <= coarsest
+    {
+        int nx = st->nx, ny = st->ny;
+        h->L = 1;
+        while ((nx < ny ? nx : ny) > pr.coarsest && (pr.max_levels <= 0 || h->L < pr.max_levels)) {
+            nx /= 2;
+            ny /= 2;
+            h->L++;
+        }
+    }
+    h->lv.resize(h->L);
+    for (int l = 0; l < h->L; l++) {
+        Level &v = h->lv[l];
+        v.nx = l == 0 ? st->nx : h->lv[l - 1].nx / 2;
+        v.ny = l == 0 ? st->ny : h->lv[l - 1].ny / 2;
+        v.kind = l == 0 ? st->kind : 9;
+        v.pitch = l == 0 ? st->pitch : round_pitch(v.nx);
+        size_t np = (size_t)(v.ny + 2) * (size_t)v.pitch;
+        int npl = v.kind == 9 ? 5 : 3;
+        for (int k = 0; k < npl; k++)
+            TRY(dalloc(h, &v.pl[k], np));
+        TRY(dalloc(h, &v.r, np));
+        if (l > 0) {
+            TRY(dalloc(h, &v.u, np));
+            TRY(dalloc(h, &v.f, np));
+            for (int k = 0; k < npl; k++)
+                CK(cudaMemsetAsync(v.pl[k], 0, np * sizeof(double), s));
+            CK(cudaMemsetAsync(v.u, 0, np * sizeof(double), s));
+            CK(cudaMemsetAsync(v.f, 0, np * sizeof(double), s));
+        }
+    }
+    for (int l = 0; l + 1 < h->L; l++) {
+        Level &c = h->lv[l + 1];
+        size_t np = (size_t)(c.ny + 2) * (size_t)c.pitch;
+        for (int k = 0; k < 8; k++) {
+            TRY(dalloc(h, &h->lv[l].ci[k], np));
+            CK(cudaMemsetAsync(h->lv[l].ci[k], 0, np * sizeof(double), s));
+        }
+    }
+    {
+        void *q;
+        CK(cudaMalloc(&q, 64 * sizeof(int)));
+        h->allocs.push_back(q);
+        h->d_err = (int *)q;
+        CK(cudaMemsetAsync(h->d_err, 0, 64 * sizeof(int), s));
+    }
+    TRY(dalloc(h, &h->partials, NORM_BLOCKS + 8));
+    TRY(dalloc(h, &h->d_norm, 8));
+    CK(cudaMallocHost(&h->h_norm, 8 * sizeof(double)));
+
+    // S0 ingest
+    {
+        Level &v = h->lv[0];
+        const double *src[5] = {st->plane[0], st->plane[1], st->plane[2], st->plane[3], st->plane[4]};
+        launch_ingest(v.nx, v.ny, v.kind, v.pitch, src, v.pl, h->d_err, s);
+        CK(cudaGetLastError());
+    }
+    // S1 + S2 per level
+    for (int l = 0; l + 1 < h->L; l++) {
+        Level &v = h->lv[l], &c = h->lv[l + 1];
+        launch_setup_interp(v.op(), v.ci, c.pitch, h->d_err, s);
+        CK(cudaGetLastError());
+        launch_setup_rap(v.op(), h->civ(l), c.nx, c.ny, c.pitch, c.pl, s);
+        CK(cudaGetLastError());
+    }
+    // S3 coarsest dense Cholesky
+    {
+        Level &c = h->lv[h->L - 1];
+        h->nco = c.nx * c.ny;
+        if (h->nco > 6144)
+            return fail(BMG_EINVAL, "coarsest level has more than 6144 unknowns; raise max_levels or lower coarsest");
+        TRY(dalloc(h, &h->chol, (size_t)h->nco * h->nco));
+        launch_assemble_dense(c.op(), h->chol, s);
+        launch_chol_factor(h->nco, h->chol, h->d_err, s);
+        CK(cudaGetLastError());
+    }
+    int herr = 0;
+    CK(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (herr & ERR_DIAG)
+        return fail(BMG_EINVAL, "stencil diagonal a_O <= 0 at an interior point");
+    if (herr & ERR_DEN)
+        return fail(BMG_EINVAL, "interpolation denominator <= 0 (operator not suited to BoxMG collapse)");
+    if (herr & ERR_PIVOT)
+        return fail(BMG_ENOTSPD, "coarsest-level Cholesky pivot <= 0");
+    CK(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+    TRY(fused_plan(h->fplan, h->lv[0].nx, h->lv[0].ny, h->lv[0].pitch, h->lv[0].kind, h->prm));
+    return BMG_OK;
+}
+
+bmg_status_t bmg_setup(const bmg_stencil_t *st, const bmg_params_t *params, void *cuda_stream, bmg_solver_t *out)
+{
+    if (!st || !out)
+        return fail(BMG_EINVAL, "null stencil or out pointer");
+    *out = nullptr;
+    if (st->nx < 1 || st->ny < 1 || (st->kind != 5 && st->kind != 9) || st->pitch < (long long)st->nx + 2)
+        return fail(BMG_EINVAL, "bad sizes: need nx,ny >= 1, kind in {5,9}, pitch >= nx+2");
+    int npl = st->kind == 9 ? 5 : 3;
+    for (int k = 0; k < npl; k++)
+        if (!st->plane[k])
+            return fail(BMG_EINVAL, "null stencil plane");
+    bmg_solver *h = new bmg_solver();
+    if (params)
+        h->prm = *params;
+    else
+        bmg_params_default(&h->prm);
+    if (h->prm.nu1 < 0 || h->prm.nu2 < 0 || h->prm.coarsest < 1) {
+        delete h;
+        return fail(BMG_EINVAL, "bad params");
+    }
+    bmg_status_t rc = setup_impl(h, st, (cudaStream_t)cuda_stream);
+    if (rc != BMG_OK) {
+        std::string d = g_detail;
+        bmg_destroy(h);
+        g_detail = d;
+        return rc;
+    }
+    *out = h;
+    return BMG_OK;
+}
+
+}  // extern "C"
+
+// Down leg of level l: nu1 sweeps, fc = P^T (f - A u), uc = 0 (if non-null).
+static void enqueue_down(bmg_solver *h, int l, const double *f, double *u, double *fc, double *uc, cudaStream_t s,
+                         int *n)
+{
+    Level &v = h->lv[l], &c = h->lv[l + 1];
+    if (fused_down(h->fplan, l, v.op(), h->civ(l), f, u, fc, uc, c.op(), h->prm.nu1, s, n))
+        return;
+    launch_relax(v.op(), f, u, h->prm.nu1, s, n);
+    launch_residual(v.op(), f, u, v.r, s);
+    launch_restrict(v.op(), h->civ(l), v.r, fc, uc, s);
+    *n += 2;
+}
+
+// Up leg of level l: u += P ec, then nu2 sweeps.
+static void enqueue_up(bmg_solver *h, int l, const double *f, double *u, const double *ec, cudaStream_t s, int *n)
+{
+    Level &v = h->lv[l];
+    if (fused_up(h->fplan, l, v.op(), h->civ(l), f, u, ec, h->prm.nu2, s, n))
+        return;
+    launch_interp_add(v.op(), h->civ(l), ec, u, s);
+    *n += 1;
+    launch_relax(v.op(), f, u, h->prm.nu2, s, n);
+}
+
+// Enqueue one V(nu1,nu2) cycle (fig:vcycle_flowchart; DESIGN §3 c9) on s.
+static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream_t s)
+{
+    int n = 0;
+    const int L = h->L;
+    auto F = [&](int l) { return l == 0 ? f0 : (const double *)h->lv[l].f; };
+    auto U = [&](int l) { return l == 0 ? u0 : h->lv[l].u; };
+    for (int l = 0; l + 1 < L; l++)
+        enqueue_down(h, l, F(l), U(l), h->lv[l + 1].f, h->lv[l + 1].u, s, &n);
+    {
+        Level &c = h->lv[L - 1];
+        launch_coarse_solve(c.op(), h->chol, F(L - 1), U(L - 1), s);
+        n += 1;
+    }
+    for (int l = L - 2; l >= 0; l--)
+        enqueue_up(h, l, F(l), U(l), h->lv[l + 1].u, s, &n);
+    return n;
+}
+
+static bmg_status_t get_graph(bmg_solver *h, const double *f, double *x, cudaGraphExec_t *out)
+{
+    auto key = std::make_pair((const void *)f, (const void *)x);
+    auto it = h->graphs.find(key);
+    if (it != h->graphs.end()) {
+        *out = it->second;
+        return BMG_OK;
+    }
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+    int n = enqueue_cycle(h, f, x, h->cap);
+    cudaError_t e = cudaStreamEndCapture(h->cap, &g);
+    if (e != cudaSuccess)
+        return fail(BMG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    cudaGraphExec_t ex;
+    CK(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    h->kernels_per_cycle = n;
+    if (h->graphs.size() > 16) {  // bound the cache
+        for (auto &kv : h->graphs)
+            cudaGraphExecDestroy(kv.second);
+        h->graphs.clear();
+    }
+    h->graphs[key] = ex;
+    *out = ex;
+    return BMG_OK;
+}
+
+extern "C" {
+
+bmg_status_t bmg_vcycle(bmg_solver_t h, const double *rhs, double *x, int ncycles, void *cuda_stream)
+{
+    if (!h || !rhs || !x || ncycles < 0)
+        return fail(BMG_EINVAL, "bad arguments to bmg_vcycle");
+    cudaGraphExec_t ex;
+    TRY(get_graph(h, rhs, x, &ex));
+    for (int k = 0; k < ncycles; k++)
+        CK(cudaGraphLaunch(ex, (cudaStream_t)cuda_stream));
+    return BMG_OK;
+}
+
+bmg_status_t bmg_vcycle_host(bmg_solver_t h, const double *rhs_host, double *x_host, int ncycles, void *cuda_stream)
+{
+    if (!h || !rhs_host || !x_host || ncycles < 0)
+        return fail(BMG_EINVAL, "bad arguments to bmg_vcycle_host");
+    Level &v = h->lv[0];
+    size_t bytes = (size_t)(v.ny + 2) * v.pitch * sizeof(double);
+    if (!h->stage_f) {
+        TRY(dalloc(h, &h->stage_f, bytes / sizeof(double)));
+        TRY(dalloc(h, &h->stage_x, bytes / sizeof(double)));
+    }
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    CK(cudaMemcpyAsync(h->stage_f, rhs_host, bytes, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(h->stage_x, x_host, bytes, cudaMemcpyHostToDevice, s));
+    TRY(bmg_vcycle(h, h->stage_f, h->stage_x, ncycles, cuda_stream));
+    CK(cudaMemcpyAsync(x_host, h->stage_x, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return BMG_OK;
+}
+
+bmg_status_t bmg_residual_norm(bmg_solver_t h, const double *rhs, const double *x, double *r_out, double *norm_host,
+                               void *cuda_stream)
+{
+    if (!h || !rhs || !x || !norm_host)
+        return fail(BMG_EINVAL, "bad arguments to bmg_residual_norm");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    launch_resid_norm(h->lv[0].op(), rhs, x, r_out, h->partials, h->d_norm, s);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h->h_norm, h->d_norm, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *norm_host = h->h_norm[0];
+    return BMG_OK;
+}
+
+bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol, int maxiter, int *iters_out,
+                       double *hist_host, void *cuda_stream)
+{
+    if (!h || !rhs || !x || maxiter < 0 || !(tol >= 0))
+        return fail(BMG_EINVAL, "bad arguments to bmg_solve");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    Level &v = h->lv[0];
+    if (iters_out)
+        *iters_out = 0;
+    launch_norm(v.op(), rhs, h->partials, h->d_norm, s);
+    CK(cudaMemcpyAsync(h->h_norm, h->d_norm, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double fn = h->h_norm[0];
+    if (fn == 0.0) {  // b = 0 -> x = 0 immediately
+        launch_zero_interior(v.op(), x, s);
+        CK(cudaStreamSynchronize(s));
+        if (hist_host)
+            hist_host[0] = 0.0;
+        return BMG_OK;
+    }
+    double rn;
+    TRY(bmg_residual_norm(h, rhs, x, nullptr, &rn, cuda_stream));
+    if (hist_host)
+        hist_host[0] = rn;
+    int k = 0;
+    while (rn > tol * fn && k < maxiter) {
+        TRY(bmg_vcycle(h, rhs, x, 1, cuda_stream));
+        k++;
+        TRY(bmg_residual_norm(h, rhs, x, nullptr, &rn, cuda_stream));
+        if (hist_host)
+            hist_host[k] = rn;
+    }
+    if (iters_out)
+        *iters_out = k;
+    return rn <= tol * fn ? BMG_OK : fail(BMG_ENOTCONV, "maxiter reached");
+}
+
+bmg_status_t bmg_num_levels(bmg_solver_t h, int *L)
+{
+    if (!h || !L)
+        return fail(BMG_EINVAL, "null argument");
+    *L = h->L;
+    return BMG_OK;
+}
+
+bmg_status_t bmg_level_shape(bmg_solver_t h, int level, int *nx, int *ny, int *kind)
+{
+    if (!h || level < 0 || level >= h->L)
+        return fail(BMG_EINVAL, "bad level");
+    if (nx)
+        *nx = h->lv[level].nx;
+    if (ny)
+        *ny = h->lv[level].ny;
+    if (kind)
+        *kind = h->lv[level].kind;
+    return BMG_OK;
+}
+
+bmg_status_t bmg_level_pitch(bmg_solver_t h, int level, long long *pitch)
+{
+    if (!h || !pitch || level < 0 || level >= h->L)
+        return fail(BMG_EINVAL, "bad level");
+    *pitch = h->lv[level].pitch;
+    return BMG_OK;
+}
+
+bmg_status_t bmg_cycle_kernel_count(bmg_solver_t h, int *count)
+{
+    if (!h || !count)
+        return fail(BMG_EINVAL, "null argument");
+    if (h->kernels_per_cycle == 0) {  // count by a dry capture
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+        int n = enqueue_cycle(h, h->lv[0].r, h->lv[0].r, h->cap);
+        CK(cudaStreamEndCapture(h->cap, &g));
+        cudaGraphDestroy(g);
+        h->kernels_per_cycle = n;
+    }
+    *count = h->kernels_per_cycle;
+    return BMG_OK;
+}
+
+bmg_status_t bmg_export_level(bmg_solver_t h, int level, double *stencil_host, double *ci_host)
+{
+    if (!h || level < 0 || level >= h->L || !stencil_host)
+        return fail(BMG_EINVAL, "bad arguments to bmg_export_level");
+    CK(cudaDeviceSynchronize());
+    Level &v = h->lv[level];
+    size_t w = (size_t)v.nx + 2, rows = (size_t)v.ny + 2;
+    for (int k = 0; k < 5; k++) {
+        double *dst = stencil_host + k * w * rows;
+        if (v.pl[k])
+            CK(cudaMemcpy2D(dst, w * sizeof(double), v.pl[k], v.pitch * sizeof(double), w * sizeof(double), rows,
+                            cudaMemcpyDeviceToHost));
+        else
+            memset(dst, 0, w * rows * sizeof(double));
+    }
+    if (ci_host && level + 1 < h->L) {
+        Level &c = h->lv[level + 1];
+        size_t cw = (size_t)c.nx + 2, crows = (size_t)c.ny + 2;
+        for (int k = 0; k < 8; k++)
+            CK(cudaMemcpy2D(ci_host + k * cw * crows, cw * sizeof(double), v.ci[k], c.pitch * sizeof(double),
+                            cw * sizeof(double), crows, cudaMemcpyDeviceToHost));
+    }
+    return BMG_OK;
+}
+
+static bmg_status_t check_level(bmg_solver_t h, int level, bool need_coarse)
+{
+    if (!h || level < 0 || level >= h->L || (need_coarse && level + 1 >= h->L))
+        return fail(BMG_EINVAL, "bad level");
+    return BMG_OK;
+}
+
+bmg_status_t bmg_relax(bmg_solver_t h, int level, const double *f, double *u, int nsweeps, void *cuda_stream)
+{
+    TRY(check_level(h, level, false));
+    launch_relax(h->lv[level].op(), f, u, nsweeps, (cudaStream_t)cuda_stream, nullptr);
+    CK(cudaGetLastError());
+    return BMG_OK;
+}
+
+bmg_status_t bmg_residual(bmg_solver_t h, int level, const double *f, const double *u, double *r, void *cuda_stream)
+{
+    TRY(check_level(h, level, false));
+    launch_residual(h->lv[level].op(), f, u, r, (cudaStream_t)cuda_stream);
+    CK(cudaGetLastError());
+    return BMG_OK;
+}
+
+bmg_status_t bmg_restrict(bmg_solver_t h, int level, const double *r, double *fc, void *cuda_stream)
+{
+    TRY(check_level(h, level, true));
+    launch_restrict(h->lv[level].op(), h->civ(level), r, fc, nullptr, (cudaStream_t)cuda_stream);
+    CK(cudaGetLastError());
+    return BMG_OK;
+}
+
+bmg_status_t bmg_interp_add(bmg_solver_t h, int level, const double *ec, double *u, void *cuda_stream)
+{
+    TRY(check_level(h, level, true));
+    launch_interp_add(h->lv[level].op(), h->civ(level), ec, u, (cudaStream_t)cuda_stream);
+    CK(cudaGetLastError());
+    return BMG_OK;
+}
+
+bmg_status_t bmg_smooth_restrict(bmg_solver_t h, int level, const double *f, double *u, double *fc, double *uc,
+                                 void *cuda_stream)
+{
+    TRY(check_level(h, level, true));
+    int n = 0;
+    enqueue_down(h, level, f, u, fc, uc, (cudaStream_t)cuda_stream, &n);
+    CK(cudaGetLastError());
+    return BMG_OK;
+}
+
+bmg_status_t bmg_correct_smooth(bmg_solver_t h, int level, const double *f, double *u, const double *ec,
+                                void *cuda_stream)
+{
+    TRY(check_level(h, level, true));
+    int n = 0;
+    enqueue_up(h, level, f, u, ec, (cudaStream_t)cuda_stream, &n);
+    CK(cudaGetLastError());
+    return BMG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,81 @@
+// bmg_internal.cuh -- device-side data views and launcher declarations of
+// libbmg.so (product code; shares nothing with oracle/).
+//
+// Layout in HBM: every level stores its operator as the
+// symmetric half in structure-of-arrays planes O, W, S (5-point) or
+// O, W, S, SW, NW (9-point), each a pitched (ny+2) x pitch fp64 grid with the
+// Dirichlet ring zero and couplings into the ring zeroed at ingest, so a
+// kernel never branches on the boundary.  The interpolation weights from
+// level l+1 to l are 8 planes (LNE, LA, LNW, LR, LL, LSE, LB, LSW) on the
+// coarse index range with the coarse pitch.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bmg {
+
+enum { CI_LNE = 0, CI_LA = 1, CI_LNW = 2, CI_LR = 3, CI_LL = 4, CI_LSE = 5, CI_LB = 6, CI_LSW = 7 };
+
+// error bits raised by setup kernels (device int, OR-ed)
+enum { ERR_DIAG = 1, ERR_DEN = 2, ERR_PIVOT = 4 };
+
+// One level's operator (read-only view).  SW/NW are nullptr on 5-point levels.
+struct Op {
+    int nx, ny, kind;
+    long long pitch;
+    const double *O, *W, *S, *SW, *NW;
+};
+
+// Interpolation weights between a level (fine) and the next (coarse).
+struct CIv {
+    long long pitch;  // coarse pitch
+    const double *w[8];
+};
+
+// Full 9-entry row of the operator at an interior point, reconstructed from
+// the symmetric half (E=W(i+1,j), N=S(i,j+1), NE=SW(i+1,j+1), SE=NW(i+1,j-1)).
+struct Row9 {
+    double sw, s, se, w, o, e, nw, n, ne;
+};
+
+__device__ __forceinline__ Row9 load_row9(const Op &A, long long p)
+{
+    Row9 a;
+    a.o = A.O[p];
+    a.w = A.W[p];
+    a.e = A.W[p + 1];
+    a.s = A.S[p];
+    a.n = A.S[p + A.pitch];
+    if (A.kind == 9) {
+        a.sw = A.SW[p];
+        a.ne = A.SW[p + A.pitch + 1];
+        a.nw = A.NW[p];
+        a.se = A.NW[p - A.pitch + 1];
+    } else {
+        a.sw = a.ne = a.nw = a.se = 0.0;
+    }
+    return a;
+}
+
+// ---- launchers (kernels.cu) ----
+void launch_ingest(int nx, int ny, int kind, long long pitch, const double *const src[5], double *const dst[5],
+                   int *err, cudaStream_t s);
+void launch_setup_interp(const Op &A, double *const ci[8], long long cpitch, int *err, cudaStream_t s);
+void launch_setup_rap(const Op &A, const CIv &ci, int ncx, int ncy, long long cpitch, double *const dst[5],
+                      cudaStream_t s);
+void launch_assemble_dense(const Op &A, double *M, cudaStream_t s);
+void launch_chol_factor(int n, double *M, int *err, cudaStream_t s);
+void launch_coarse_solve(const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s);
+
+void launch_relax(const Op &A, const double *f, double *u, int nsweeps, cudaStream_t s, int *nlaunch);
+void launch_residual(const Op &A, const double *f, const double *u, double *r, cudaStream_t s);
+void launch_restrict(const Op &A, const CIv &ci, const double *r, double *fc, double *uc, cudaStream_t s);
+void launch_interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s);
+void launch_resid_norm(const Op &A, const double *f, const double *u, double *r_out, double *partials,
+                       double *result, cudaStream_t s);
+void launch_norm(const Op &A, const double *g, double *partials, double *result, cudaStream_t s);
+void launch_zero_interior(const Op &A, double *x, cudaStream_t s);
+
+constexpr int NORM_BLOCKS = 592;  // 4 x 148 SMs; fixed so the reduction tree is fixed
+
+}  // namespace bmg

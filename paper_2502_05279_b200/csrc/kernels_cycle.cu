@@ -1,0 +1,305 @@
+// kernels_cycle.cu -- per-step V-cycle kernels (one kernel per method step):
+// multicolour Gauss-Seidel, residual, restriction (fig:restrict_kernel),
+// interpolation + correction, residual norm, coarsest Cholesky solve.
+//
+// These are the reference-shaped ("model B") kernels: each step
+// reads its operands once and writes its outputs once.  They run every level
+// in the unfused mode and the small levels in the fused mode; the fused
+// streaming kernels for large levels are in kernels_fused.cu.
+#include "bmg_internal.cuh"
+
+namespace bmg {
+
+// off-diagonal part of (A u)_p in fig:stencil_operator order SW,S,SE,W,E,NW,N,NE
+__device__ __forceinline__ double offdiag(const Row9 &a, const double *__restrict__ u, long long p, long long P)
+{
+    double s = a.sw * u[p - P - 1];
+    s += a.s * u[p - P];
+    s += a.se * u[p - P + 1];
+    s += a.w * u[p - 1];
+    s += a.e * u[p + 1];
+    s += a.nw * u[p + P - 1];
+    s += a.n * u[p + P];
+    s += a.ne * u[p + P + 1];
+    return s;
+}
+
+// 5-point levels: colour (i+j)&1; updates u_p <- (f_p - sum_{q!=p} a_pq u_q)/a_pp
+// One thread per point of the colour (DESIGN §3 c6).
+__global__ void k_relax5(Op A, const double *__restrict__ f, double *__restrict__ u, int colour)
+{
+    int j = blockIdx.y * blockDim.y + threadIdx.y + 1;
+    if (j > A.ny)
+        return;
+    int i0 = (((1 + j) & 1) == colour) ? 1 : 2;
+    int i = i0 + 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i > A.nx)
+        return;
+    long long P = A.pitch, p = j * P + i;
+    double o = A.O[p], w = A.W[p], e = A.W[p + 1], s = A.S[p], n = A.S[p + P];
+    double acc = s * u[p - P];
+    acc += w * u[p - 1];
+    acc += e * u[p + 1];
+    acc += n * u[p + P];
+    u[p] = (f[p] - acc) / o;
+}
+
+// 9-point levels: colour (i&1) + 2(j&1), 4 colours.
+__global__ void k_relax9(Op A, const double *__restrict__ f, double *__restrict__ u, int colour)
+{
+    int j = 2 * (blockIdx.y * blockDim.y + threadIdx.y) + ((colour >> 1) ? 1 : 2);
+    if (j > A.ny)
+        return;
+    int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x) + ((colour & 1) ? 1 : 2);
+    if (i > A.nx)
+        return;
+    long long P = A.pitch, p = j * P + i;
+    Row9 a = load_row9(A, p);
+    u[p] = (f[p] - offdiag(a, u, p, P)) / a.o;
+}
+
+void launch_relax(const Op &A, const double *f, double *u, int nsweeps, cudaStream_t s, int *nlaunch)
+{
+    dim3 b(32, 8);
+    for (int sw = 0; sw < nsweeps; sw++) {
+        if (A.kind == 5) {
+            dim3 g((A.nx / 2 + 1 + 31) / 32, (A.ny + 7) / 8);
+            for (int c = 0; c < 2; c++)
+                k_relax5<<<g, b, 0, s>>>(A, f, u, c);
+            if (nlaunch)
+                *nlaunch += 2;
+        } else {
+            dim3 g((A.nx / 2 + 1 + 31) / 32, (A.ny / 2 + 1 + 7) / 8);
+            for (int c = 0; c < 4; c++)
+                k_relax9<<<g, b, 0, s>>>(A, f, u, c);
+            if (nlaunch)
+                *nlaunch += 4;
+        }
+    }
+}
+
+// r = f - A u on the interior, ring of r set to 0 (fig:vcycle_flowchart "Residual").
+__global__ void k_residual(Op A, const double *__restrict__ f, const double *__restrict__ u, double *__restrict__ r)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int j = blockIdx.y * blockDim.y + threadIdx.y;
+    if (i > A.nx + 1 || j > A.ny + 1)
+        return;
+    long long P = A.pitch, p = j * P + i;
+    if (i == 0 || j == 0 || i > A.nx || j > A.ny) {
+        r[p] = 0.0;
+        return;
+    }
+    Row9 a = load_row9(A, p);
+    r[p] = f[p] - (a.o * u[p] + offdiag(a, u, p, P));
+}
+
+void launch_residual(const Op &A, const double *f, const double *u, double *r, cudaStream_t s)
+{
+    dim3 b(32, 8), g((A.nx + 2 + 31) / 32, (A.ny + 2 + 7) / 8);
+    k_residual<<<g, b, 0, s>>>(A, f, u, r);
+}
+
+// Restriction, fig:restrict_kernel in 0-based indices (fine 2I = Fortran istart+(ic-1)*2):
+//  QC(I,J) = Ci(I,J,LNE)Q(2I-1,2J-1) + Ci(I,J,LA)Q(2I,2J-1) + Ci(I+1,J,LNW)Q(2I+1,2J-1)
+//          + Ci(I,J,LR)Q(2I-1,2J) + Q(2I,2J) + Ci(I+1,J,LL)Q(2I+1,2J)
+//          + Ci(I,J+1,LSE)Q(2I-1,2J+1) + Ci(I,J+1,LB)Q(2I,2J+1) + Ci(I+1,J+1,LSW)Q(2I+1,2J+1)
+// One thread per coarse point, all (ncx+2)(ncy+2) written (ring 0).
+// If uc != nullptr it is zeroed at the same points (the coarse correction's
+// zero start, DESIGN §3 c9), saving a separate memset launch.
+__global__ void k_restrict(Op A, CIv ci, const double *__restrict__ q, double *__restrict__ qc, double *__restrict__ uc)
+{
+    int ncx = A.nx / 2, ncy = A.ny / 2;
+    int I = blockIdx.x * blockDim.x + threadIdx.x;
+    int J = blockIdx.y * blockDim.y + threadIdx.y;
+    if (I > ncx + 1 || J > ncy + 1)
+        return;
+    long long C = ci.pitch, c = J * C + I;
+    if (uc)
+        uc[c] = 0.0;
+    if (I == 0 || J == 0 || I > ncx || J > ncy) {
+        qc[c] = 0.0;
+        return;
+    }
+    long long P = A.pitch, p = (2 * J) * P + 2 * I;
+    double v = ci.w[CI_LNE][c] * q[p - P - 1];
+    v += ci.w[CI_LA][c] * q[p - P];
+    v += ci.w[CI_LNW][c + 1] * q[p - P + 1];
+    v += ci.w[CI_LR][c] * q[p - 1];
+    v += q[p];
+    v += ci.w[CI_LL][c + 1] * q[p + 1];
+    v += ci.w[CI_LSE][c + C] * q[p + P - 1];
+    v += ci.w[CI_LB][c + C] * q[p + P];
+    v += ci.w[CI_LSW][c + C + 1] * q[p + P + 1];
+    qc[c] = v;
+}
+
+void launch_restrict(const Op &A, const CIv &ci, const double *r, double *fc, double *uc, cudaStream_t s)
+{
+    dim3 b(32, 8), g((A.nx / 2 + 2 + 31) / 32, (A.ny / 2 + 2 + 7) / 8);
+    k_restrict<<<g, b, 0, s>>>(A, ci, r, fc, uc);
+}
+
+// u += P e (DESIGN §3 c7), one thread per fine interior point; e's ring is 0.
+__global__ void k_interp_add(Op A, CIv ci, const double *__restrict__ e, double *__restrict__ u)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    int j = blockIdx.y * blockDim.y + threadIdx.y + 1;
+    if (i > A.nx || j > A.ny)
+        return;
+    long long C = ci.pitch;
+    long long p = j * A.pitch + i;
+    int I = (i + 1) >> 1, J = (j + 1) >> 1;  // storage index of X/Y/Z weights; C point: (i/2, j/2)
+    long long c = J * C + I;
+    double s;
+    if (!(i & 1) && !(j & 1)) {
+        s = e[(j >> 1) * C + (i >> 1)];
+    } else if ((i & 1) && !(j & 1)) {  // X at (2I-1, 2J): J = j/2
+        c = (j >> 1) * C + I;
+        s = ci.w[CI_LL][c] * e[c - 1];
+        s += ci.w[CI_LR][c] * e[c];
+    } else if (!(i & 1) && (j & 1)) {  // Y at (2I, 2J-1): I = i/2
+        c = J * C + (i >> 1);
+        s = ci.w[CI_LB][c] * e[c - C];
+        s += ci.w[CI_LA][c] * e[c];
+    } else {  // Z
+        s = ci.w[CI_LSW][c] * e[c - C - 1];
+        s += ci.w[CI_LSE][c] * e[c - C];
+        s += ci.w[CI_LNW][c] * e[c - 1];
+        s += ci.w[CI_LNE][c] * e[c];
+    }
+    u[p] += s;
+}
+
+void launch_interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s)
+{
+    dim3 b(32, 8), g((A.nx + 31) / 32, (A.ny + 7) / 8);
+    k_interp_add<<<g, b, 0, s>>>(A, ci, ec, u);
+}
+
+// zero the interior (and ring) of a level grid function
+__global__ void k_zero(long long n, double *x)
+{
+    long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t < n)
+        x[t] = 0.0;
+}
+
+void launch_zero_interior(const Op &A, double *x, cudaStream_t s)
+{
+    long long n = (A.ny + 2) * A.pitch;
+    k_zero<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, x);
+}
+
+// ---------------------------------------------------------------- norms
+// Deterministic two-pass l2 norm: NORM_BLOCKS fixed blocks each reduce a
+// fixed row set (warp shuffle tree + fixed smem tree), then one block sums
+// the partials in a fixed tree.  Bitwise run-to-run reproducible.
+__device__ __forceinline__ double block_sum(double v)
+{
+    __shared__ double sh[32];
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_down_sync(0xffffffffu, v, o);
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0)
+        sh[wid] = v;
+    __syncthreads();
+    int nw = blockDim.x >> 5;
+    v = (threadIdx.x < nw) ? sh[threadIdx.x] : 0.0;
+    if (wid == 0)
+        for (int o = 16; o > 0; o >>= 1)
+            v += __shfl_down_sync(0xffffffffu, v, o);
+    __syncthreads();
+    return v;
+}
+
+template <bool RESID>
+__global__ void k_norm_partial(Op A, const double *__restrict__ f, const double *__restrict__ u,
+                               double *__restrict__ r_out, double *__restrict__ partials)
+{
+    double acc = 0.0;
+    long long P = A.pitch;
+    for (int j = 1 + blockIdx.x; j <= A.ny; j += gridDim.x) {
+        for (int i = 1 + threadIdx.x; i <= A.nx; i += blockDim.x) {
+            long long p = j * P + i;
+            double v;
+            if (RESID) {
+                Row9 a = load_row9(A, p);
+                v = f[p] - (a.o * u[p] + offdiag(a, u, p, P));
+                if (r_out)
+                    r_out[p] = v;
+            } else {
+                v = f[p];
+            }
+            acc += v * v;
+        }
+    }
+    acc = block_sum(acc);
+    if (threadIdx.x == 0)
+        partials[blockIdx.x] = acc;
+}
+
+__global__ void k_norm_final(const double *__restrict__ partials, int n, double *result)
+{
+    double acc = 0.0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x)
+        acc += partials[k];
+    acc = block_sum(acc);
+    if (threadIdx.x == 0)
+        *result = sqrt(acc);
+}
+
+void launch_resid_norm(const Op &A, const double *f, const double *u, double *r_out, double *partials,
+                       double *result, cudaStream_t s)
+{
+    k_norm_partial<true><<<NORM_BLOCKS, 256, 0, s>>>(A, f, u, r_out, partials);
+    k_norm_final<<<1, 1024, 0, s>>>(partials, NORM_BLOCKS, result);
+}
+
+void launch_norm(const Op &A, const double *g, double *partials, double *result, cudaStream_t s)
+{
+    k_norm_partial<false><<<NORM_BLOCKS, 256, 0, s>>>(A, g, nullptr, nullptr, partials);
+    k_norm_final<<<1, 1024, 0, s>>>(partials, NORM_BLOCKS, result);
+}
+
+// ---------------------------------------------------------------- coarsest solve
+// u = A_L^{-1} f with the setup Cholesky factor: forward then backward
+// substitution (fig:vcycle_flowchart "Cholesky"), one CTA, the
+// right-hand side staged in shared memory (n <= 6144).
+__global__ void k_coarse_solve(Op A, const double *__restrict__ Lf, const double *__restrict__ f, double *__restrict__ u)
+{
+    extern __shared__ double b[];
+    int n = A.nx * A.ny;
+    for (int p = threadIdx.x; p < n; p += blockDim.x)
+        b[p] = f[(p / A.nx + 1) * A.pitch + p % A.nx + 1];
+    __syncthreads();
+    for (int k = 0; k < n; k++) {  // L y = b
+        double bk = b[k] / Lf[(long long)k * n + k];
+        __syncthreads();
+        if (threadIdx.x == 0)
+            b[k] = bk;
+        for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x)
+            b[i] -= Lf[(long long)i * n + k] * bk;
+        __syncthreads();
+    }
+    for (int k = n - 1; k >= 0; k--) {  // L^T x = y
+        double bk = b[k] / Lf[(long long)k * n + k];
+        __syncthreads();
+        if (threadIdx.x == 0)
+            b[k] = bk;
+        for (int i = threadIdx.x; i < k; i += blockDim.x)
+            b[i] -= Lf[(long long)k * n + i] * bk;
+        __syncthreads();
+    }
+    for (int p = threadIdx.x; p < n; p += blockDim.x)
+        u[(p / A.nx + 1) * A.pitch + p % A.nx + 1] = b[p];
+}
+
+void launch_coarse_solve(const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s)
+{
+    int n = A.nx * A.ny;
+    int threads = n < 32 ? 32 : (n < 1024 ? ((n + 31) / 32) * 32 : 1024);
+    k_coarse_solve<<<1, threads, sizeof(double) * n, s>>>(A, Lf, f, u);
+}
+
+}  // namespace bmg

@@ -1,0 +1,216 @@
+"""GPU <-> oracle parity through the C ABI (tolerances DESIGN §7).
+
+* level-0 ingest and interpolation weights: bitwise (same inputs, same
+  arithmetic with no contraction in setup);
+* coarse operators / weights: 1e-12 relative per entry, floor = the row's |O|
+  (weights: 1e-12 absolute, they are O(1) ratios);
+* one V-cycle iterate: 1e-12 relative per component, floor 1e-12 * max|x|
+  (DESIGN §7 derives the floor);
+* per-cycle residual norms: 1e-10 relative.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from paper_2502_05279_b200 import bmg, problems as P  # noqa: E402
+
+OST = {"O": 4, "W": 3, "S": 1, "SW": 0, "NW": 6}  # oracle full-stencil entry index of each plane
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as ge
+
+    ge.build_lib()
+
+
+def planes_of_full(st9, kind):
+    names = ["O", "W", "S"] + (["SW", "NW"] if kind == 9 else [])
+    return {n: st9[..., OST[n]] for n in names}
+
+
+def assert_operator_close(gpu_planes, orc_st9, kind, exact=False):
+    ref = planes_of_full(orc_st9, kind)
+    floor = np.abs(orc_st9[..., 4])
+    for k, name in enumerate(["O", "W", "S", "SW", "NW"]):
+        if name not in ref:
+            assert np.all(gpu_planes[k] == 0)
+            continue
+        g, o = gpu_planes[k], ref[name]
+        if exact:
+            assert np.array_equal(g, o), name
+        else:
+            tol = 1e-12 * np.maximum(np.abs(o), floor)
+            bad = np.abs(g - o) > tol
+            assert not bad.any(), (name, np.abs(g - o).max(), np.argwhere(bad)[:5])
+
+
+def assert_iterate_close(g, o, rtol=1e-12):
+    tol = rtol * np.maximum(np.abs(o), np.abs(o).max())
+    err = np.abs(g - o)
+    assert np.all(err <= tol), (err.max(), (err / np.maximum(np.abs(o), 1e-300)).max())
+
+
+CASES = [("poisson", 31, 31), ("lognormal", 63, 63), ("checker", 127, 127), ("aniso", 63, 63), ("random9", 33, 33),
+         ("lognormal", 64, 30), ("checker_off3", 95, 47), ("poisson", 1, 1), ("lognormal", 5, 9), ("poisson", 2, 40)]
+
+
+@pytest.mark.parametrize("wl,nx,ny", CASES)
+@pytest.mark.parametrize("fused", [1, 0])
+def test_setup_parity(orc, wl, nx, ny, fused):
+    st = P.workload(wl, nx, ny)
+    prm = bmg.bmg_params_default()
+    prm.fused = fused
+    s = bmg.Solver(st, prm)
+    h = orc.Hierarchy(st)
+    assert s.L == h.num_levels
+    for l in range(s.L):
+        assert bmg.bmg_level_shape(s.h, l) == h.level_shape(l)
+        gst, gci = bmg.bmg_export_level(s.h, l)
+        ost, oci = h.export_level(l)
+        kind = h.level_shape(l)[2]
+        assert_operator_close(gst, ost, kind, exact=(l == 0))
+        if oci is not None:
+            gci = np.moveaxis(gci, 0, -1)
+            if l == 0:
+                assert np.array_equal(gci, oci)
+            else:
+                assert np.abs(gci - oci).max() <= 1e-12
+    s.close()
+
+
+@pytest.mark.parametrize("wl,nx,ny", CASES)
+def test_step_parity_level0(orc, wl, nx, ny):
+    """Each method step on level 0 (identical operator and weights on both sides)."""
+    st = P.workload(wl, nx, ny)
+    s = bmg.Solver(st)
+    if s.L < 2:
+        pytest.skip("single level")
+    st9 = orc.expand_stencil(st)
+    _, ci = orc.Hierarchy(st).export_level(0)
+    f = P.field_uniform(nx, ny, seed=21)
+    u0 = P.field_uniform(nx, ny, seed=22)
+    for nsw in (1, 2):
+        u = s.grid(u0)
+        bmg.bmg_relax(s.h, 0, s.grid(f), u, nsw)
+        assert_iterate_close(bmg.from_device(u, nx), orc.relax(st9, st.kind, f, u0, nsw), rtol=1e-13)
+    r = s.grid()
+    bmg.bmg_residual(s.h, 0, s.grid(f), s.grid(u0), r)
+    ro = orc.residual(st9, f, u0)
+    assert np.abs(bmg.from_device(r, nx) - ro).max() <= 1e-13 * np.abs(ro).max()
+    fc = s.level_grid(1)
+    bmg.bmg_restrict(s.h, 0, s.grid(ro), fc)
+    fco = orc.restrict(ci, ro)
+    assert np.abs(bmg.from_device(fc, nx // 2) - fco).max() <= 1e-14 * np.abs(fco).max()
+    ec0 = P.field_uniform(nx // 2, ny // 2, seed=23)
+    u = s.grid(u0)
+    bmg.bmg_interp_add(s.h, 0, s.level_grid(1, ec0), u)
+    uo = orc.interp_add(ci, ec0, u0)
+    assert np.abs(bmg.from_device(u, nx) - uo).max() <= 1e-15 * np.abs(uo).max() * 4
+    s.close()
+
+
+@pytest.mark.parametrize("wl,nx,ny", CASES)
+@pytest.mark.parametrize("fused", [1, 0])
+def test_vcycle_parity(orc, wl, nx, ny, fused):
+    st = P.workload(wl, nx, ny)
+    prm = bmg.bmg_params_default()
+    prm.fused = fused
+    s = bmg.Solver(st, prm)
+    h = orc.Hierarchy(st)
+    f = P.field_uniform(nx, ny, seed=31)
+    x0 = P.field_uniform(nx, ny, seed=32)
+    x = s.grid(x0)
+    fd = s.grid(f)
+    s.vcycle(fd, x, 1)
+    torch.cuda.synchronize()
+    ref = h.vcycle(f, x0, 1)
+    assert_iterate_close(bmg.from_device(x, nx), ref)
+    # ring untouched, padding untouched
+    xg = x.cpu().numpy()
+    assert np.all(xg[0, :] == 0) and np.all(xg[-1, :] == 0) and np.all(xg[:, 0] == 0)
+    assert np.all(xg[:, nx + 1:] == 0)
+    s.close()
+
+
+@pytest.mark.parametrize("wl,n,tol,maxit", [("poisson", 31, 1e-10, 50), ("checker", 127, 1e-10, 200),
+                                            ("lognormal", 63, 1e-10, 100), ("aniso", 31, 1e-6, 400)])
+def test_solve_parity(orc, wl, n, tol, maxit):
+    st = P.workload(wl, n, n)
+    s = bmg.Solver(st)
+    h = orc.Hierarchy(st)
+    f = P.rhs_const(n, n)
+    x = s.grid()
+    it, hist, rc = s.solve(s.grid(f), x, tol, maxit)
+    uo, ito, histo, rco = h.solve(f, np.zeros_like(f), tol, maxit)
+    assert rc == rco == 0
+    assert it == ito
+    floor = 1e-12 * histo[0]  # below this the norms are rounding noise of both sides
+    assert np.all(np.abs(hist - histo) <= 1e-10 * histo + floor), np.abs(hist / histo - 1).max()
+    assert_iterate_close(bmg.from_device(x, n), uo, rtol=1e-10)
+    s.close()
+
+
+def test_config1_gpu(orc):
+    """Config 1 on the GPU: 7 cycles to 1e-10 with the oracle's history."""
+    n = 31
+    s = bmg.Solver(P.workload("poisson", n, n))
+    f = P.rhs_const(n, n)
+    x = s.grid()
+    it, hist, rc = s.solve(s.grid(f), x, 1e-10, 50)
+    assert rc == 0 and it == 7
+    assert hist[0] == pytest.approx(0.0302734375, rel=1e-15)
+    assert np.all(np.diff(hist) < 0)
+    s.close()
+
+
+def test_zero_rhs_and_errors():
+    n = 15
+    s = bmg.Solver(P.workload("poisson", n, n))
+    x = s.grid(P.field_uniform(n, n))
+    it, hist, rc = s.solve(s.grid(), x, 1e-8, 10)
+    assert it == 0 and rc == 0 and float(x.abs().max()) == 0.0
+    it, hist, rc = s.solve(s.grid(P.rhs_const(n, n)), x, 1e-30, 2)
+    assert rc == bmg.BMG_ENOTCONV and it == 2 and len(hist) == 3
+    s.close()
+    bad = P.workload("poisson", n, n)
+    bad.planes["O"][5, 5] = -1.0
+    with pytest.raises(bmg.BmgError) as ei:
+        bmg.Solver(bad)
+    assert ei.value.status == bmg.BMG_EINVAL
+
+
+def test_determinism_and_graph_reuse():
+    n = 127
+    s = bmg.Solver(P.workload("lognormal", n, n))
+    f = s.grid(P.field_uniform(n, n, seed=3))
+    outs, norms = [], []
+    for _ in range(2):
+        x = s.grid(P.field_uniform(n, n, seed=4))
+        s.vcycle(f, x, 3)
+        norms.append(s.residual_norm(f, x))
+        outs.append(x.clone())
+    assert torch.equal(outs[0], outs[1])
+    assert norms[0] == norms[1]
+    assert bmg.bmg_cycle_kernel_count(s.h) > 0
+    s.close()
+
+
+def test_vcycle_host_matches_device():
+    n = 63
+    st = P.workload("lognormal", n, n)
+    s = bmg.Solver(st)
+    f = s.grid(P.field_uniform(n, n, seed=5))
+    x = s.grid(P.field_uniform(n, n, seed=6))
+    fh = f.cpu().pin_memory()
+    xh = x.cpu().pin_memory()
+    s.vcycle(f, x, 2)
+    bmg.bmg_vcycle_host(s.h, fh, xh, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(x.cpu(), xh)
+    s.close()
