@@ -340,14 +340,15 @@ def roofline(solver, bmg, torch, f, x, nx, ny, kind, peak, peak_src, ms_per_step
     fc = solver.level_grid(1)
     uc = solver.level_grid(1)
     u = x.clone()
+    u2 = torch.zeros_like(u)
     nrep = 20
     for _ in range(3):
-        bmg.bmg_smooth_restrict(solver.h, 0, f, u, fc, uc)
+        bmg.bmg_smooth_restrict(solver.h, 0, f, u, u2, fc, uc)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     ev0.record(stream)
     for _ in range(nrep):
-        bmg.bmg_smooth_restrict(solver.h, 0, f, u, fc, uc)
+        bmg.bmg_smooth_restrict(solver.h, 0, f, u, u2, fc, uc)
     ev1.record(stream)
     torch.cuda.synchronize()
     dur_ms = ev0.elapsed_time(ev1) / nrep

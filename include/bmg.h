@@ -16,8 +16,8 @@
  *  - Every array is IEEE fp64, row-major, x fastest.  A grid function g of an
  *    nx*ny interior has element (i,j) at g[j*pitch + i], i in [0,nx+1],
  *    j in [0,ny+1]; the interior is [1,nx]x[1,ny]; the ring is the
- *    homogeneous Dirichlet ghost.  Ring values of inputs are ignored, ring
- *    values of outputs are written as 0 only where stated.
+ *    homogeneous Dirichlet ghost: the ring of an iterate x must hold 0 and
+ *    is never written; the ring of a right-hand side is ignored.
  *  - Unless stated otherwise, pointers are DEVICE pointers on the current
  *    CUDA device, must not alias each other, and stay owned by the caller.
  *  - `cuda_stream` is a cudaStream_t (NULL = legacy default stream).  All
@@ -157,15 +157,18 @@ bmg_status_t bmg_interp_add(bmg_solver_t h, int level, const double *ec, double 
 /*
  * The two legs of one level of the V-cycle, as the cycle runs them (the fused
  * streaming kernel where the level is fused, else the per-step kernels):
- *  bmg_smooth_restrict: nu1 GS sweeps on (f,u), then fc = P^T (f - A u) and,
- *                       if uc != NULL, uc = 0 (the coarse correction's start).
- *  bmg_correct_smooth:  u += P ec, then nu2 GS sweeps.
- * fc, uc, ec use bmg_level_pitch(level+1).  Asynchronous.
+ *  bmg_smooth_restrict: u_out = nu1 GS sweeps applied to u_in (rhs f); then
+ *                       fc = P^T (f - A u_out) and, if uc != NULL, uc = 0 (the
+ *                       coarse correction's zero start).
+ *  bmg_correct_smooth:  u_out = nu2 GS sweeps applied to u_in + P ec.
+ * u_in and u_out are distinct level-`level` grid functions (bmg_level_pitch);
+ * the ring of u_out is not written.  fc, uc, ec use bmg_level_pitch(level+1).
+ * Asynchronous.  EINVAL if u_in == u_out or a pointer is NULL.
  */
-bmg_status_t bmg_smooth_restrict(bmg_solver_t h, int level, const double *f, double *u, double *fc, double *uc,
-                                 void *cuda_stream);
-bmg_status_t bmg_correct_smooth(bmg_solver_t h, int level, const double *f, double *u, const double *ec,
-                                void *cuda_stream);
+bmg_status_t bmg_smooth_restrict(bmg_solver_t h, int level, const double *f, const double *u_in, double *u_out,
+                                 double *fc, double *uc, void *cuda_stream);
+bmg_status_t bmg_correct_smooth(bmg_solver_t h, int level, const double *f, const double *u_in, const double *ec,
+                                double *u_out, void *cuda_stream);
 
 /* Number of kernels one bmg_vcycle cycle launches (the captured graph's kernel nodes). */
 bmg_status_t bmg_cycle_kernel_count(bmg_solver_t h, int *count);

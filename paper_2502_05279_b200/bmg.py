@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbmg.so")
+LIB_PATH = os.environ.get("BMG_LIB") or os.path.join(_HERE, "libbmg.so")
 
 BMG_OK, BMG_EINVAL, BMG_ENOMEM, BMG_ECUDA, BMG_ENCCL, BMG_ENOTSPD, BMG_ENOTCONV = range(7)
 
@@ -73,8 +73,8 @@ def lib():
             "bmg_residual": (i, [vp, i, vp, vp, vp, vp]),
             "bmg_restrict": (i, [vp, i, vp, vp, vp]),
             "bmg_interp_add": (i, [vp, i, vp, vp, vp]),
-            "bmg_smooth_restrict": (i, [vp, i, vp, vp, vp, vp, vp]),
-            "bmg_correct_smooth": (i, [vp, i, vp, vp, vp, vp]),
+            "bmg_smooth_restrict": (i, [vp, i, vp, vp, vp, vp, vp, vp]),
+            "bmg_correct_smooth": (i, [vp, i, vp, vp, vp, vp, vp]),
             "bmg_cycle_kernel_count": (i, [vp, ip]),
             "bmg_destroy": (i, [vp]),
             "bmg_strerror": (ctypes.c_char_p, [i]),
@@ -201,13 +201,14 @@ def bmg_interp_add(h, level, ec, u, stream=None):
     _check(lib().bmg_interp_add(h, level, _ptr(ec), _ptr(u), _stream(stream)), "bmg_interp_add")
 
 
-def bmg_smooth_restrict(h, level, f, u, fc, uc=None, stream=None):
-    _check(lib().bmg_smooth_restrict(h, level, _ptr(f), _ptr(u), _ptr(fc), _ptr(uc), _stream(stream)),
+def bmg_smooth_restrict(h, level, f, u_in, u_out, fc, uc=None, stream=None):
+    _check(lib().bmg_smooth_restrict(h, level, _ptr(f), _ptr(u_in), _ptr(u_out), _ptr(fc), _ptr(uc), _stream(stream)),
            "bmg_smooth_restrict")
 
 
-def bmg_correct_smooth(h, level, f, u, ec, stream=None):
-    _check(lib().bmg_correct_smooth(h, level, _ptr(f), _ptr(u), _ptr(ec), _stream(stream)), "bmg_correct_smooth")
+def bmg_correct_smooth(h, level, f, u_in, ec, u_out, stream=None):
+    _check(lib().bmg_correct_smooth(h, level, _ptr(f), _ptr(u_in), _ptr(ec), _ptr(u_out), _stream(stream)),
+           "bmg_correct_smooth")
 
 
 def bmg_cycle_kernel_count(h) -> int:

@@ -236,7 +236,22 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
     if (herr & ERR_PIVOT)
         return fail(BMG_ENOTSPD, "coarsest-level Cholesky pivot <= 0");
     CK(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
-    TRY(fused_plan(h->fplan, h->lv[0].nx, h->lv[0].ny, h->lv[0].pitch, h->lv[0].kind, h->prm));
+    // fused streaming plan + ping-pong partner of u for every fused level
+    for (int l = 0; l + 1 < h->L && l < 32; l++) {
+        Level &v = h->lv[l];
+        if (!h->prm.fused)
+            break;
+        TRY(fused_plan_level(h->fplan, l, v.nx, v.ny, v.pitch, v.kind, h->prm.nu1, h->prm.nu2, (v.pitch & 1) == 0));
+        LevelPlan &lp = h->fplan.lv[l];
+        if (!(lp.down && lp.up)) {
+            lp.down = lp.up = false;
+            continue;
+        }
+        size_t np = (size_t)(v.ny + 2) * (size_t)v.pitch;
+        TRY(dalloc(h, &h->fplan.tmp[l], np));
+        CK(cudaMemsetAsync(h->fplan.tmp[l], 0, np * sizeof(double), s));
+    }
+    CK(cudaStreamSynchronize(s));
     return BMG_OK;
 }
 
@@ -273,46 +288,72 @@ bmg_status_t bmg_setup(const bmg_stencil_t *st, const bmg_params_t *params, void
 
 }  // extern "C"
 
-// Down leg of level l: nu1 sweeps, fc = P^T (f - A u), uc = 0 (if non-null).
-static void enqueue_down(bmg_solver *h, int l, const double *f, double *u, double *fc, double *uc, cudaStream_t s,
-                         int *n)
+static bool al16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
+// Whether level l runs the fused streaming kernels for these level-l arrays.
+static bool use_fused(bmg_solver *h, int l, const void *f, const void *uin, const void *uout)
 {
-    Level &v = h->lv[l], &c = h->lv[l + 1];
-    if (fused_down(h->fplan, l, v.op(), h->civ(l), f, u, fc, uc, c.op(), h->prm.nu1, s, n))
+    if (!h->prm.fused || l >= 32 || l + 1 >= h->L)
+        return false;
+    const LevelPlan &lp = h->fplan.lv[l];
+    return lp.down && lp.up && al16(f) && al16(uin) && al16(uout) && uin != uout;
+}
+
+static void copy_level(bmg_solver *h, int l, double *dst, const double *src, cudaStream_t s)
+{
+    if (dst != src)
+        cudaMemcpyAsync(dst, src, (size_t)(h->lv[l].ny + 2) * h->lv[l].pitch * sizeof(double),
+                        cudaMemcpyDeviceToDevice, s);
+}
+
+// Down leg of level l: u_out = relax^nu1(u_in); fc = P^T (f - A u_out); uc = 0 (if non-null).
+static void enqueue_down(bmg_solver *h, int l, bool fused, const double *f, const double *uin, double *uout,
+                         double *fc, double *uc, cudaStream_t s, int *n)
+{
+    Level &v = h->lv[l];
+    if (fused && fused_down(h->fplan, l, v.op(), h->civ(l), f, uin, uout, fc, uc, s, n))
         return;
-    launch_relax(v.op(), f, u, h->prm.nu1, s, n);
-    launch_residual(v.op(), f, u, v.r, s);
+    copy_level(h, l, uout, uin, s);
+    launch_relax(v.op(), f, uout, h->prm.nu1, s, n);
+    launch_residual(v.op(), f, uout, v.r, s);
     launch_restrict(v.op(), h->civ(l), v.r, fc, uc, s);
     *n += 2;
 }
 
-// Up leg of level l: u += P ec, then nu2 sweeps.
-static void enqueue_up(bmg_solver *h, int l, const double *f, double *u, const double *ec, cudaStream_t s, int *n)
+// Up leg of level l: u_out = relax^nu2(u_in + P ec).
+static void enqueue_up(bmg_solver *h, int l, bool fused, const double *f, const double *uin, const double *ec,
+                       double *uout, cudaStream_t s, int *n)
 {
     Level &v = h->lv[l];
-    if (fused_up(h->fplan, l, v.op(), h->civ(l), f, u, ec, h->prm.nu2, s, n))
+    if (fused && fused_up(h->fplan, l, v.op(), h->civ(l), f, uin, ec, uout, s, n))
         return;
-    launch_interp_add(v.op(), h->civ(l), ec, u, s);
+    copy_level(h, l, uout, uin, s);
+    launch_interp_add(v.op(), h->civ(l), ec, uout, s);
     *n += 1;
-    launch_relax(v.op(), f, u, h->prm.nu2, s, n);
+    launch_relax(v.op(), f, uout, h->prm.nu2, s, n);
 }
 
 // Enqueue one V(nu1,nu2) cycle (fig:vcycle_flowchart; DESIGN §3 c9) on s.
+// A fused level's iterate goes U -> T on the down leg and T -> U on the up leg.
 static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream_t s)
 {
     int n = 0;
     const int L = h->L;
     auto F = [&](int l) { return l == 0 ? f0 : (const double *)h->lv[l].f; };
     auto U = [&](int l) { return l == 0 ? u0 : h->lv[l].u; };
-    for (int l = 0; l + 1 < L; l++)
-        enqueue_down(h, l, F(l), U(l), h->lv[l + 1].f, h->lv[l + 1].u, s, &n);
+    bool fz[64];
+    for (int l = 0; l + 1 < L; l++) {
+        double *T = l < 32 ? h->fplan.tmp[l] : nullptr;
+        fz[l] = T && use_fused(h, l, F(l), U(l), T);
+        enqueue_down(h, l, fz[l], F(l), U(l), fz[l] ? T : U(l), h->lv[l + 1].f, h->lv[l + 1].u, s, &n);
+    }
     {
         Level &c = h->lv[L - 1];
         launch_coarse_solve(c.op(), h->chol, F(L - 1), U(L - 1), s);
         n += 1;
     }
     for (int l = L - 2; l >= 0; l--)
-        enqueue_up(h, l, F(l), U(l), h->lv[l + 1].u, s, &n);
+        enqueue_up(h, l, fz[l], F(l), fz[l] ? h->fplan.tmp[l] : U(l), h->lv[l + 1].u, U(l), s, &n);
     return n;
 }
 
@@ -536,22 +577,27 @@ bmg_status_t bmg_interp_add(bmg_solver_t h, int level, const double *ec, double 
     return BMG_OK;
 }
 
-bmg_status_t bmg_smooth_restrict(bmg_solver_t h, int level, const double *f, double *u, double *fc, double *uc,
-                                 void *cuda_stream)
+bmg_status_t bmg_smooth_restrict(bmg_solver_t h, int level, const double *f, const double *u_in, double *u_out,
+                                 double *fc, double *uc, void *cuda_stream)
 {
     TRY(check_level(h, level, true));
+    if (!f || !u_in || !u_out || !fc || u_in == u_out)
+        return fail(BMG_EINVAL, "bmg_smooth_restrict: null pointer or u_in == u_out");
     int n = 0;
-    enqueue_down(h, level, f, u, fc, uc, (cudaStream_t)cuda_stream, &n);
+    enqueue_down(h, level, use_fused(h, level, f, u_in, u_out), f, u_in, u_out, fc, uc, (cudaStream_t)cuda_stream,
+                 &n);
     CK(cudaGetLastError());
     return BMG_OK;
 }
 
-bmg_status_t bmg_correct_smooth(bmg_solver_t h, int level, const double *f, double *u, const double *ec,
-                                void *cuda_stream)
+bmg_status_t bmg_correct_smooth(bmg_solver_t h, int level, const double *f, const double *u_in, const double *ec,
+                                double *u_out, void *cuda_stream)
 {
     TRY(check_level(h, level, true));
+    if (!f || !u_in || !u_out || !ec || u_in == u_out)
+        return fail(BMG_EINVAL, "bmg_correct_smooth: null pointer or u_in == u_out");
     int n = 0;
-    enqueue_up(h, level, f, u, ec, (cudaStream_t)cuda_stream, &n);
+    enqueue_up(h, level, use_fused(h, level, f, u_in, u_out), f, u_in, ec, u_out, (cudaStream_t)cuda_stream, &n);
     CK(cudaGetLastError());
     return BMG_OK;
 }

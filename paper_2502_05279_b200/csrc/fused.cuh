@@ -1,22 +1,55 @@
-// fused.cuh -- fused streaming kernels for large levels (kernels_fused.cu).
+// fused.cuh -- fused streaming ("wavefront temporal blocking") kernels for
+// the large levels (kernels_fused.cu).  DESIGN.md §5.2.
+//
+// Down leg of a level in ONE pass over HBM: nu1 multicolour GS sweeps +
+// residual + restriction (+ zeroing the coarse correction).  Up leg in ONE
+// pass: interpolation + correction + nu2 sweeps.  Each CTA owns a strip of
+// TX output columns and a chunk of rows and streams the rows bottom-up
+// through a ring of shared-memory rows filled by 1-D TMA bulk copies
+// (cp.async.bulk + mbarrier); colour stages run 2 rows apart so one barrier
+// per row step orders them.  u is ping-ponged (u_in -> u_out) because
+// neighbouring CTAs read each other's halo rows/columns.
 #pragma once
 #include "bmg.h"
 #include "bmg_internal.cuh"
 
 namespace bmg {
 
-struct FusedPlan {
-    int nlev = 0;          // levels [0, nlev) use the fused down/up kernels
+struct FusedGeom {
+    int TX = 0;      // output columns per strip (multiple of 4)
+    int H = 0;       // x halo (even)
+    int WD = 0;      // smem row width = TX + 2H
+    int WC = 0;      // smem coarse row width = TX/2 + 6
+    int R = 0;       // fine ring rows
+    int D = 0;       // fine-row prefetch distance (rows)
+    int NS = 0;      // colour stages (2 per sweep)
+    int nstrips = 0, nchunks = 0, chunk = 0;
+    int threads = 0;
+    size_t smem = 0;
+    bool ok = false;
 };
 
-bmg_status_t fused_plan(FusedPlan &fp, int nx, int ny, long long pitch, int kind, const bmg_params_t &prm);
+struct LevelPlan {
+    bool down = false, up = false;
+    FusedGeom gd, gu;
+};
 
-// Down leg of level l: nu1 sweeps + residual + restriction (+ zero of the coarse u), one pass.
-// Returns false if level l is not handled by the fused path.
-bool fused_down(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const double *f, double *u, double *fc,
-                double *uc, const Op &Ac, int nu1, cudaStream_t s, int *nlaunch);
-// Up leg of level l: interpolation + correction + nu2 sweeps, one pass.
-bool fused_up(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const double *f, double *u, const double *ec,
-              int nu2, cudaStream_t s, int *nlaunch);
+struct FusedPlan {
+    int nlev = 0;
+    LevelPlan lv[32];
+    double *tmp[32] = {nullptr};  // ping-pong partner of each fused level's u
+};
+
+// Decide per level whether the fused kernels run and with which geometry.
+bmg_status_t fused_plan_level(FusedPlan &fp, int l, int nx, int ny, long long pitch, int kind, int nu1, int nu2,
+                              bool aligned);
+
+// Down leg of level l: nu1 sweeps on (f, uin) -> uout, fc = P^T(f - A uout), uc = 0 (if non-null).
+// Returns false if level l is not fused.
+bool fused_down(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const double *f, const double *uin,
+                double *uout, double *fc, double *uc, cudaStream_t s, int *nlaunch);
+// Up leg: uout = relax^nu2(uin + P ec).
+bool fused_up(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const double *f, const double *uin,
+              const double *ec, double *uout, cudaStream_t s, int *nlaunch);
 
 }  // namespace bmg

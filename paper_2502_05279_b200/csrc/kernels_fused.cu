@@ -1,24 +1,928 @@
-// kernels_fused.cu -- fused streaming kernels for large levels (placeholder: disabled).
+// kernels_fused.cu -- fused streaming kernels for the large levels
+// (interface in fused.cuh).
+//
+// Down leg of a level in ONE pass over HBM (row step t):
+//   split of the freshly landed row t; colour stage k = 1..NS (NS = 2 nu1) of
+//   multicolour GS (c6) on row t-2k; residual on row t-2NS-2; restriction
+//   (fig:restrict_kernel) of coarse row J = (t-2NS-4)/2; store of
+//   the final iterate row t-2NS-3.
+// Up leg in ONE pass:
+//   split of row t; interpolation + correction (c7) on row t-1; stage k on
+//   row t-1-2k; store of row t-2NS-2.
+// Stages 2 rows apart never touch each other's rows within a row step, so one
+// __syncthreads per step orders everything (two on 9-point levels, whose row
+// stage is two colour phases: even columns, then odd columns).
+//
+// Memory path: rows of u_in, f and the operator planes arrive by 1-D TMA bulk
+// copies (cp.async.bulk.shared::cluster.global + mbarrier complete_tx) into a
+// staging ring D rows ahead, in natural order.  A split task de-interleaves
+// each row into [even columns | odd columns] halves of the main ring, so every
+// compute access -- a colour pass touches every other column -- is a run of
+// consecutive doubles across a warp (no shared-memory bank conflicts).  Coarse
+// rows (interpolation weights, coarse correction) use their own 4-slot ring.
+// A CTA owns TX output columns x a chunk of rows and recomputes an x halo H
+// and a row warm-up that its neighbours own (same per-point arithmetic, so the
+// owners' values are reproduced exactly); u is ping-ponged (u_in -> u_out).
+//
+// Thread mapping: NG warp-aligned task groups; a thread owns PPT column pairs
+// h (smem columns 2h, 2h+1), h lane-consecutive.  Each group does one kind of
+// task per step (a colour stage, a residual parity, store, restriction, split),
+// loading all operands of its points before the arithmetic.
+#include <stdlib.h>
+
+#include <algorithm>
+#include <type_traits>
+
 #include "fused.cuh"
 
 namespace bmg {
 
-bmg_status_t fused_plan(FusedPlan &fp, int, int, long long, int, const bmg_params_t &)
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t n)
 {
-    fp.nlev = 0;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_LOOP:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_LOOP;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *b)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// ------------------------------------------------------------------ configuration
+constexpr int DC = 4;  // coarse-row prefetch distance (row steps); < 6 for safe ring reuse
+constexpr int CH = 4;  // coarse halo columns on each side of a strip
+
+// streamed arrays: index into the shared-memory array blocks
+enum { A_U = 0, A_F = 1, A_O = 2, A_W = 3, A_S = 4, A_SW = 5, A_NW = 6 };
+
+template <int KIND, int NS, int WD, int D, bool UP, int PPT>
+struct Cfg {
+    static constexpr int NA = KIND == 5 ? 5 : 7;
+    static constexpr int PASSES = KIND == 5 ? NS : 2 * NS;      // colour passes (x halo shrink)
+    static constexpr int H0 = UP ? PASSES : PASSES + 2;         // + residual + restriction
+    static constexpr int H = ((H0 < 2 ? 2 : H0) + 1) & ~1;      // even (16-byte TMA alignment)
+    static constexpr int TX = WD - 2 * H;                      // output columns (multiple of 4)
+    static constexpr int HW = WD / 2;                          // half row (one parity)
+    static constexpr int RM = UP ? 2 * NS + 3 : 2 * NS + 4;     // main (split) ring rows
+    static constexpr int SD = D + 1;                           // staging (natural) ring rows
+    static constexpr int AM = RM * WD, AS = SD * WD;           // doubles per array block
+    static constexpr int WC = TX / 2 + 2 * CH;
+    static constexpr int NPG = HW / PPT;                       // threads per task group
+    static constexpr int NSPLIT = 2;                           // split task groups
+    static constexpr int NG = UP ? (KIND == 5 ? NS + 3 + NSPLIT : 5 + NSPLIT)
+                                 : (KIND == 5 ? NS + 4 + NSPLIT : 6 + NSPLIT);
+    static constexpr int NTW = NG * NPG;                       // worker threads
+    static constexpr int NT = NTW + 32;                        // + one TMA producer warp
+    static constexpr size_t SMEM_DBL =
+        (size_t)NA * (AM + AS) + (UP ? 4 * (size_t)WC : 4 * (size_t)WD) + 32 * (size_t)WC;
+    static constexpr size_t SMEM = SMEM_DBL * 8 + (SD + 4) * 8;
+    static_assert(TX % 4 == 0 && TX > 0, "strip width");
+    static_assert(NPG % 32 == 0, "task groups must be whole warps");
+};
+
+struct FArgs {
+    Op A;
+    CIv ci;
+    const double *f, *uin, *ec;
+    double *uout, *fc, *uc;
+    int nstrips, chunk, ncx, ncy;
+};
+
+// ring slot of the row `d` rows behind the newest (ts = slot of row t)
+template <int R>
+__device__ __forceinline__ int back(int ts, int d)
+{
+    int s = ts - d;
+    return s < 0 ? s + R : s;
+}
+
+// Offsets (within a split row) of smem column sc = 2h+par and of its x neighbours.
+struct Col {
+    int same, left, right;
+};
+template <int HW>
+__device__ __forceinline__ Col col_of(int h, int par)
+{
+    Col c;
+    c.same = par * HW + h;
+    c.left = (1 - par) * HW + h + par - 1;
+    c.right = c.left + 1;
+    return c;
+}
+
+// Loads of the operands of one point (row bases b0/bm/bp = slot*WD of rows r, r-1, r+1),
+// off-diagonal terms in fig:stencil_operator order SW,S,SE,W,E,NW,N,NE.
+template <int KIND, int AM>
+struct PointOps {
+    double a[8], u[8], f, o, uc;
+    __device__ __forceinline__ void load(const double *sm, int b0, int bm, int bp, const Col &c, bool with_uc)
+    {
+        if (KIND == 5) {
+            a[0] = sm[A_S * AM + b0 + c.same];
+            u[0] = sm[A_U * AM + bm + c.same];
+            a[1] = sm[A_W * AM + b0 + c.same];
+            u[1] = sm[A_U * AM + b0 + c.left];
+            a[2] = sm[A_W * AM + b0 + c.right];
+            u[2] = sm[A_U * AM + b0 + c.right];
+            a[3] = sm[A_S * AM + bp + c.same];
+            u[3] = sm[A_U * AM + bp + c.same];
+        } else {
+            a[0] = sm[A_SW * AM + b0 + c.same];
+            u[0] = sm[A_U * AM + bm + c.left];
+            a[1] = sm[A_S * AM + b0 + c.same];
+            u[1] = sm[A_U * AM + bm + c.same];
+            a[2] = sm[A_NW * AM + bm + c.right];
+            u[2] = sm[A_U * AM + bm + c.right];
+            a[3] = sm[A_W * AM + b0 + c.same];
+            u[3] = sm[A_U * AM + b0 + c.left];
+            a[4] = sm[A_W * AM + b0 + c.right];
+            u[4] = sm[A_U * AM + b0 + c.right];
+            a[5] = sm[A_NW * AM + b0 + c.same];
+            u[5] = sm[A_U * AM + bp + c.left];
+            a[6] = sm[A_S * AM + bp + c.same];
+            u[6] = sm[A_U * AM + bp + c.same];
+            a[7] = sm[A_SW * AM + bp + c.right];
+            u[7] = sm[A_U * AM + bp + c.right];
+        }
+        f = sm[A_F * AM + b0 + c.same];
+        o = sm[A_O * AM + b0 + c.same];
+        if (with_uc)
+            uc = sm[A_U * AM + b0 + c.same];
+    }
+    __device__ __forceinline__ double offdiag() const
+    {
+        constexpr int NT = KIND == 5 ? 4 : 8;
+        double acc = a[0] * u[0];
+#pragma unroll
+        for (int q = 1; q < NT; q++)
+            acc += a[q] * u[q];
+        return acc;
+    }
+};
+
+// a / b for b > 0 normal, entirely on the FP64 FMA pipe.  The IEEE division
+// seeds its reciprocal with MUFU.RCP64H on the XU pipe, whose throughput (not
+// HBM) bounded these kernels (ncu: XU > 100% of peak, FP64 FMA pipe 8%).  Seed:
+// exponent/mantissa reflection 0x7FE0...0 - bits(b), relative error <= 1/8;
+// five Newton steps (error 2^-3 -> 2^-96) and one residual correction give a
+// quotient within 1 ulp of a/b (parity tolerance).
+#ifndef BMG_DIV_NEWTON
+#define BMG_DIV_NEWTON 1
+#endif
+__device__ __forceinline__ double div_pos(double a, double b)
+{
+    if (!BMG_DIV_NEWTON)
+        return a / b;
+    double r = __longlong_as_double(0x7FE0000000000000LL - __double_as_longlong(b));
+#pragma unroll
+    for (int i = 0; i < 5; i++)
+        r = fma(r, fma(-b, r, 1.0), r);
+    const double q = a * r;
+    return fma(fma(-b, q, a), r, q);
+}
+
+// Per-thread column data for its PPT pairs, both parities (loop invariant).
+// Neighbour offsets of a split row never leave the row (par 0: left/right in
+// the odd half; par 1: in the even half), so no clamping is needed; `on` marks
+// the points inside [1,nx] that may be stored.
+template <int PPT>
+struct Cols {
+    Col c[2][PPT];
+    bool on[2][PPT];
+};
+
+template <int WD, int PPT, int NPG>
+__device__ __forceinline__ Cols<PPT> make_cols(int m, int xl, int nx)
+{
+    constexpr int HW = WD / 2;
+    Cols<PPT> k;
+#pragma unroll
+    for (int par = 0; par < 2; par++)
+#pragma unroll
+        for (int p = 0; p < PPT; p++) {
+            const int h = m + p * NPG, sc = 2 * h + par, c = xl + sc;
+            k.c[par][p] = col_of<HW>(h, par);
+            k.on[par][p] = c >= 1 && c <= nx && sc >= 1 && sc <= WD - 2;
+        }
+    return k;
+}
+
+// One colour pass (c6: u <- (f - sum_{q!=p} a_pq u_q) / a_pp) on row r for this
+// thread's PPT pairs, column parity PAR.  Points outside [1,nx] are computed but not stored.
+template <int KIND, int AM, int WD, int PPT, int PAR>
+__device__ __forceinline__ void colour_pass(double *sm, int s0, int sm1, int sp1, const Cols<PPT> &k)
+{
+    PointOps<KIND, AM> pt[PPT];
+#pragma unroll
+    for (int p = 0; p < PPT; p++)
+        pt[p].load(sm, s0 * WD, sm1 * WD, sp1 * WD, k.c[PAR][p], false);
+#pragma unroll
+    for (int p = 0; p < PPT; p++) {
+        const double v = div_pos(pt[p].f - pt[p].offdiag(), pt[p].o);
+        if (k.on[PAR][p])
+            sm[A_U * AM + s0 * WD + k.c[PAR][p].same] = v;
+    }
+}
+
+template <int KIND, int AM, int WD, int PPT>
+__device__ __forceinline__ void colour_pass(double *sm, int s0, int sm1, int sp1, int par, const Cols<PPT> &k)
+{
+    if (par)
+        colour_pass<KIND, AM, WD, PPT, 1>(sm, s0, sm1, sp1, k);
+    else
+        colour_pass<KIND, AM, WD, PPT, 0>(sm, s0, sm1, sp1, k);
+}
+
+// De-interleave staging row (natural order, slot ss) into main ring row (slot s0)
+// for arrays [q0, q1): even columns to the first half, odd to the second.
+template <int AM, int AS, int WD, int PPT, int NPG>
+__device__ __forceinline__ void split_row(double *smM, const double *smS, int ss, int s0, int q0, int q1, int m)
+{
+    constexpr int HW = WD / 2;
+#pragma unroll
+    for (int q = 0; q < 7; q++) {
+        if (q < q0 || q >= q1)
+            continue;
+        double2 v[PPT];
+#pragma unroll
+        for (int p = 0; p < PPT; p++)
+            v[p] = *reinterpret_cast<const double2 *>(smS + q * AS + ss * WD + 2 * (m + p * NPG));
+#pragma unroll
+        for (int p = 0; p < PPT; p++) {
+            double *row = smM + q * AM + s0 * WD;
+            row[m + p * NPG] = v[p].x;
+            row[HW + m + p * NPG] = v[p].y;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ down kernel
+template <int KIND, int NS, int WD, int D, int PPT>
+__global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT) k_fused_down(FArgs a)
+{
+    using C = Cfg<KIND, NS, WD, D, false, PPT>;
+    constexpr int NA = C::NA, H = C::H, TX = C::TX, WC = C::WC, HW = C::HW, NPG = C::NPG;
+    constexpr int RM = C::RM, SD = C::SD, AM = C::AM, AS = C::AS;
+    extern __shared__ __align__(128) double sm[];
+    double *smS = sm + NA * AM;                 // staging ring (natural rows)
+    double *sR = smS + NA * AS;                 // residual ring [4][WD], split
+    double *sC = sR + 4 * WD;                   // weights ring [4][8][WC]
+    uint64_t *bar = (uint64_t *)(sC + 32 * WC); // SD staging + 4 coarse
+
+    const int nx = a.A.nx, ny = a.A.ny, ncx = a.ncx;
+    const long long P = a.A.pitch, CP = a.ci.pitch;
+    const int strip = blockIdx.x % a.nstrips, chunk = blockIdx.x / a.nstrips;
+    const int x0 = strip * TX, xl = x0 - H;
+    const int ya = max(1, chunk * a.chunk), yb = min(ny + 1, (chunk + 1) * a.chunk);
+    if (ya >= yb)
+        return;
+    const int lo = max(ya - NS - 2, 0), hi = min(yb + NS + 1, ny + 1);
+    const int cs = max(xl, 0), ce = min(xl + WD, (int)P);
+    const uint32_t rowbytes = (uint32_t)(ce - cs) * 8u;
+    const int soff = cs - xl;
+    const int cxl = x0 / 2 - CH;
+    const int ccs = max(cxl, 0), cce = min(cxl + WC, (int)CP);
+    const uint32_t crowbytes = (uint32_t)(cce - ccs) * 8u;
+    const int csoff = ccs - cxl;
+    const int Jlo = (ya + 1) / 2, Jhi = min((yb - 1) / 2, a.ncy);  // restricted rows: 2J in [ya, yb)
+    const int Kend = Jhi >= Jlo ? Jhi + 1 : Jlo - 1;
+
+    const int tid = threadIdx.x, grp = tid / NPG, m = tid % NPG;
+    const bool producer = tid == C::NTW;  // lane 0 of the producer warp issues every TMA copy
+
+    if (tid == 0) {
+        for (int i = 0; i < SD + 4; i++)
+            mbar_init(&bar[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    int Knext = Jlo;
+    auto issue_row = [&](int row) {
+        const int slot = (row - lo) % SD;
+        uint64_t *b = &bar[slot];
+        mbar_arrive_tx(b, rowbytes * NA);
+        const long long go = row * P + cs;
+        double *d = smS + slot * WD + soff;
+        bulk_g2s(d + A_U * AS, a.uin + go, rowbytes, b);
+        bulk_g2s(d + A_F * AS, a.f + go, rowbytes, b);
+        bulk_g2s(d + A_O * AS, a.A.O + go, rowbytes, b);
+        bulk_g2s(d + A_W * AS, a.A.W + go, rowbytes, b);
+        bulk_g2s(d + A_S * AS, a.A.S + go, rowbytes, b);
+        if (KIND == 9) {
+            bulk_g2s(d + A_SW * AS, a.A.SW + go, rowbytes, b);
+            bulk_g2s(d + A_NW * AS, a.A.NW + go, rowbytes, b);
+        }
+    };
+    auto issue_coarse = [&](int t) {
+        while (Knext <= Kend) {
+            const int use = (Knext == Jlo) ? 2 * Jlo + 2 * NS + 4 : 2 * Knext + 2 * NS + 2;
+            if (use - DC > t)
+                break;
+            const int slot = (Knext - Jlo) & 3;
+            uint64_t *b = &bar[SD + slot];
+            mbar_arrive_tx(b, crowbytes * 8);
+            for (int q = 0; q < 8; q++)
+                bulk_g2s(sC + (slot * 8 + q) * WC + csoff, a.ci.w[q] + Knext * CP + ccs, crowbytes, b);
+            Knext++;
+        }
+    };
+    if (producer)
+        for (int row = lo; row <= min(lo + D - 1, hi); row++)
+            issue_row(row);
+
+    const Cols<PPT> kc = make_cols<WD, PPT, NPG>(m, xl, nx);
+
+    // residual of row rr at the columns of parity e of this thread's pairs;
+    // 0 off the interior (the restriction reads the ring as zeros)
+    auto resid_par = [&](int rr, int s0, int sm1, int sp1, auto E) {
+        constexpr int e = decltype(E)::value;
+        const bool rin = rr >= 1 && rr <= ny;
+        PointOps<KIND, AM> pt[PPT];
+#pragma unroll
+        for (int p = 0; p < PPT; p++)
+            pt[p].load(sm, s0 * WD, sm1 * WD, sp1 * WD, kc.c[e][p], true);
+        double *rrow = sR + (rr & 3) * WD;
+#pragma unroll
+        for (int p = 0; p < PPT; p++) {
+            const double v = pt[p].f - (pt[p].o * pt[p].uc + pt[p].offdiag());
+            rrow[kc.c[e][p].same] = (rin && kc.on[e][p]) ? v : 0.0;
+        }
+    };
+    auto resid_task = [&](int rr, int s0, int sm1, int sp1, int e) {
+        if (rr < ya - 1 || rr > yb || rr < 0 || rr > ny + 1)
+            return;
+        if (e)
+            resid_par(rr, s0, sm1, sp1, std::integral_constant<int, 1>());
+        else
+            resid_par(rr, s0, sm1, sp1, std::integral_constant<int, 0>());
+    };
+    // store of the final iterate row w (main slot sw), columns (2h, 2h+1) of the owned strip
+    auto store_task = [&](int w, int sw) {
+        if (w < ya || w >= yb)
+            return;
+        const double *urow = sm + A_U * AM + sw * WD;
+#pragma unroll
+        for (int p = 0; p < PPT; p++) {
+            const int h = m + p * NPG, sc = 2 * h, c = xl + sc;
+            if (sc < H || sc >= H + TX)
+                continue;
+            double *dst = a.uout + (long long)w * P + c;
+            const double ve = urow[h], vo = urow[HW + h];
+            if (c >= 1 && c + 1 <= nx)
+                *reinterpret_cast<double2 *>(dst) = make_double2(ve, vo);
+            else {
+                if (c >= 1 && c <= nx)
+                    dst[0] = ve;
+                if (c + 1 >= 1 && c + 1 <= nx)
+                    dst[1] = vo;
+            }
+        }
+    };
+    // restriction (fig:restrict_kernel) of coarse row J at the coarse points centred on columns 2h
+    auto restrict_task = [&](int J) {
+        mbar_wait(&bar[SD + ((J - Jlo) & 3)], ((J - Jlo) >> 2) & 1);
+        mbar_wait(&bar[SD + ((J + 1 - Jlo) & 3)], ((J + 1 - Jlo) >> 2) & 1);
+        const double *rm = sR + ((2 * J - 1) & 3) * WD, *r0 = sR + ((2 * J) & 3) * WD,
+                     *rp = sR + ((2 * J + 1) & 3) * WD;
+        const double *c0 = sC + ((J - Jlo) & 3) * 8 * WC, *c1 = sC + ((J + 1 - Jlo) & 3) * 8 * WC;
+#pragma unroll
+        for (int p = 0; p < PPT; p++) {
+            const int h = m + p * NPG;
+            const int I = xl / 2 + h;
+            if (I < x0 / 2 || I >= x0 / 2 + TX / 2 || I < 1 || I > ncx)
+                continue;
+            const int ic = I - cxl;
+            // split residual rows: column 2h -> [h], 2h-1 -> [HW+h-1], 2h+1 -> [HW+h]
+            double v = c0[CI_LNE * WC + ic] * rm[HW + h - 1];
+            v += c0[CI_LA * WC + ic] * rm[h];
+            v += c0[CI_LNW * WC + ic + 1] * rm[HW + h];
+            v += c0[CI_LR * WC + ic] * r0[HW + h - 1];
+            v += r0[h];
+            v += c0[CI_LL * WC + ic + 1] * r0[HW + h];
+            v += c1[CI_LSE * WC + ic] * rp[HW + h - 1];
+            v += c1[CI_LB * WC + ic] * rp[h];
+            v += c1[CI_LSW * WC + ic + 1] * rp[HW + h];
+            a.fc[(long long)J * CP + I] = v;
+            if (a.uc)
+                a.uc[(long long)J * CP + I] = 0.0;
+        }
+    };
+
+    // Task groups (warp-aligned, one task per step):
+    //  5-point: 0..NS-1 colour stage k = grp+1; NS, NS+1 residual of even/odd columns;
+    //           NS+2 store; NS+3 restriction; NS+4, NS+5 split.
+    //  9-point: 0,1 the two active row stages (phase A even columns, phase B odd);
+    //           2,3 residual; 4 store; 5 restriction; 6,7 split.
+    constexpr int G_SPLIT = KIND == 5 ? NS + 4 : 6;
+    constexpr int QSPLIT = KIND == 5 ? 3 : 4;  // arrays [0,QSPLIT) by the first split group
+    const int tend = yb + 2 * NS + 3;
+    int tm = 0, tsd = 0;  // main / staging ring slots of row t
+    for (int t = lo; t <= tend; t++, tm = (tm + 1 == RM) ? 0 : tm + 1, tsd = (tsd + 1 == SD) ? 0 : tsd + 1) {
+        if (producer) {
+            fence_proxy_async();
+            if (t + D <= hi)
+                issue_row(t + D);
+            issue_coarse(t);
+        }
+        const int jr = t - 2 * NS - 4;
+        const int J = jr >> 1;
+        const bool restr = jr >= 0 && !(jr & 1) && J >= Jlo && J <= Jhi;
+        if (grp >= C::NG) {
+            // producer warp: no compute task
+        } else if (grp >= G_SPLIT) {
+            if (t <= hi) {
+                mbar_wait(&bar[tsd], ((t - lo) / SD) & 1);
+                if (grp == G_SPLIT)
+                    split_row<AM, AS, WD, PPT, NPG>(sm, smS, tsd, tm, 0, QSPLIT, m);
+                else
+                    split_row<AM, AS, WD, PPT, NPG>(sm, smS, tsd, tm, QSPLIT, NA, m);
+            }
+        } else if (KIND == 5) {
+            if (grp < NS) {
+                const int k = grp + 1, d = 2 * k, r = t - d;
+                if (r > lo && r < hi && r >= 1 && r <= ny)
+                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1),
+                                                        back<RM>(tm, d - 1), (((k - 1) & 1) - r) & 1, kc);
+            } else if (grp <= NS + 1) {
+                const int d = 2 * NS + 2;
+                resid_task(t - d, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), grp - NS);
+            } else if (grp == NS + 2) {
+                store_task(t - 2 * NS - 3, back<RM>(tm, 2 * NS + 3));
+            } else if (restr) {
+                restrict_task(J);
+            }
+        } else {
+            // active 9-point row stages at step t: k with (t - 2k) & 1 == (k - 1) & 1, i.e. (t + k) odd
+            const int k = ((t & 1) ? 2 : 1) + 2 * grp, d = 2 * k, r = t - d;
+            if (grp < 2) {
+                if (k <= NS && r > lo && r < hi && r >= 1 && r <= ny)
+                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1),
+                                                        back<RM>(tm, d - 1), 0, kc);
+            } else if (grp < 4) {
+                const int dr = 2 * NS + 2;
+                resid_task(t - dr, back<RM>(tm, dr), back<RM>(tm, dr + 1), back<RM>(tm, dr - 1), grp - 2);
+            } else if (grp == 4) {
+                store_task(t - 2 * NS - 3, back<RM>(tm, 2 * NS + 3));
+            } else if (restr) {
+                restrict_task(J);
+            }
+        }
+        __syncthreads();
+        if (KIND == 9) {
+            const int k = ((t & 1) ? 2 : 1) + 2 * grp, d = 2 * k, r = t - d;
+            if (grp < 2 && k <= NS && r > lo && r < hi && r >= 1 && r <= ny)
+                colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), 1, kc);
+            __syncthreads();
+        }
+    }
+}
+
+// ------------------------------------------------------------------ up kernel
+template <int KIND, int NS, int WD, int D, int PPT>
+__global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT) k_fused_up(FArgs a)
+{
+    using C = Cfg<KIND, NS, WD, D, true, PPT>;
+    constexpr int NA = C::NA, H = C::H, TX = C::TX, WC = C::WC, HW = C::HW, NPG = C::NPG;
+    constexpr int RM = C::RM, SD = C::SD, AM = C::AM, AS = C::AS;
+    extern __shared__ __align__(128) double sm[];
+    double *smS = sm + NA * AM;                 // staging ring
+    double *sE = smS + NA * AS;                 // coarse correction ring [4][WC]
+    double *sC = sE + 4 * WC;                   // weights ring [4][8][WC]
+    uint64_t *bar = (uint64_t *)(sC + 32 * WC);
+
+    const int nx = a.A.nx, ny = a.A.ny;
+    const long long P = a.A.pitch, CP = a.ci.pitch;
+    const int strip = blockIdx.x % a.nstrips, chunk = blockIdx.x / a.nstrips;
+    const int x0 = strip * TX, xl = x0 - H;
+    const int ya = max(1, chunk * a.chunk), yb = min(ny + 1, (chunk + 1) * a.chunk);
+    if (ya >= yb)
+        return;
+    const int lo = max(ya - NS, 0), hi = min(yb + NS - 1, ny + 1);
+    const int lo1 = max(lo, 1), hi1 = min(hi, ny);  // corrected rows
+    const int cs = max(xl, 0), ce = min(xl + WD, (int)P);
+    const uint32_t rowbytes = (uint32_t)(ce - cs) * 8u;
+    const int soff = cs - xl;
+    const int cxl = x0 / 2 - CH;
+    const int ccs = max(cxl, 0), cce = min(cxl + WC, (int)CP);
+    const uint32_t crowbytes = (uint32_t)(cce - ccs) * 8u;
+    const int csoff = ccs - cxl;
+    const int Klo = lo1 / 2, Khi = (hi1 + 1) / 2;
+
+    const int tid = threadIdx.x, grp = tid / NPG, m = tid % NPG;
+    const bool producer = tid == C::NTW;  // lane 0 of the producer warp issues every TMA copy
+
+    if (tid == 0) {
+        for (int i = 0; i < SD + 4; i++)
+            mbar_init(&bar[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    int Knext = Klo;
+    auto issue_row = [&](int row) {
+        const int slot = (row - lo) % SD;
+        uint64_t *b = &bar[slot];
+        mbar_arrive_tx(b, rowbytes * NA);
+        const long long go = row * P + cs;
+        double *d = smS + slot * WD + soff;
+        bulk_g2s(d + A_U * AS, a.uin + go, rowbytes, b);
+        bulk_g2s(d + A_F * AS, a.f + go, rowbytes, b);
+        bulk_g2s(d + A_O * AS, a.A.O + go, rowbytes, b);
+        bulk_g2s(d + A_W * AS, a.A.W + go, rowbytes, b);
+        bulk_g2s(d + A_S * AS, a.A.S + go, rowbytes, b);
+        if (KIND == 9) {
+            bulk_g2s(d + A_SW * AS, a.A.SW + go, rowbytes, b);
+            bulk_g2s(d + A_NW * AS, a.A.NW + go, rowbytes, b);
+        }
+    };
+    auto issue_coarse = [&](int t) {
+        while (Knext <= Khi) {
+            const int use = max(2 * Knext - 1, lo1) + 1;
+            if (use - DC > t)
+                break;
+            const int slot = (Knext - Klo) & 3;
+            uint64_t *b = &bar[SD + slot];
+            mbar_arrive_tx(b, crowbytes * 9);
+            bulk_g2s(sE + slot * WC + csoff, a.ec + Knext * CP + ccs, crowbytes, b);
+            for (int q = 0; q < 8; q++)
+                bulk_g2s(sC + (slot * 8 + q) * WC + csoff, a.ci.w[q] + Knext * CP + ccs, crowbytes, b);
+            Knext++;
+        }
+    };
+    if (producer)
+        for (int row = lo; row <= min(lo + D - 1, hi); row++)
+            issue_row(row);
+
+    // u += P e (c7) on row x (main slot sx) at the columns of parity e of this thread's
+    // pairs; same operand order as k_interp_add.  Point type is uniform over the group.
+    auto correct_task = [&](int x, int sx, int e) {
+        if (x < lo1 || x > hi1)
+            return;
+        const int Ka = x >> 1, Kb = (x + 1) >> 1;
+        mbar_wait(&bar[SD + ((Ka - Klo) & 3)], ((Ka - Klo) >> 2) & 1);
+        mbar_wait(&bar[SD + ((Kb - Klo) & 3)], ((Kb - Klo) >> 2) & 1);
+        double *u0 = sm + A_U * AM + sx * WD + e * HW;
+        const bool rodd = x & 1;
+#pragma unroll
+        for (int p = 0; p < PPT; p++) {
+            const int h = m + p * NPG, c = xl + 2 * h + e;
+            if (c < 1 || c > nx)
+                continue;
+            double s;
+            if (!e && !rodd) {  // C point
+                s = sE[((x / 2 - Klo) & 3) * WC + (c / 2 - cxl)];
+            } else if (e && !rodd) {  // X point (2I-1, 2J)
+                const int I = (c + 1) / 2, Jx = x / 2, ic = I - cxl;
+                const double *ev = sE + ((Jx - Klo) & 3) * WC;
+                const double *w = sC + ((Jx - Klo) & 3) * 8 * WC;
+                s = w[CI_LL * WC + ic] * ev[ic - 1];
+                s += w[CI_LR * WC + ic] * ev[ic];
+            } else if (!e && rodd) {  // Y point (2I, 2J-1)
+                const int I = c / 2, Jy = (x + 1) / 2, ic = I - cxl;
+                const double *e0 = sE + ((Jy - 1 - Klo) & 3) * WC, *e1 = sE + ((Jy - Klo) & 3) * WC;
+                const double *w = sC + ((Jy - Klo) & 3) * 8 * WC;
+                s = w[CI_LB * WC + ic] * e0[ic];
+                s += w[CI_LA * WC + ic] * e1[ic];
+            } else {  // Z point (2I-1, 2J-1)
+                const int I = (c + 1) / 2, Jz = (x + 1) / 2, ic = I - cxl;
+                const double *e0 = sE + ((Jz - 1 - Klo) & 3) * WC, *e1 = sE + ((Jz - Klo) & 3) * WC;
+                const double *w = sC + ((Jz - Klo) & 3) * 8 * WC;
+                s = w[CI_LSW * WC + ic] * e0[ic - 1];
+                s += w[CI_LSE * WC + ic] * e0[ic];
+                s += w[CI_LNW * WC + ic] * e1[ic - 1];
+                s += w[CI_LNE * WC + ic] * e1[ic];
+            }
+            u0[h] += s;
+        }
+    };
+    auto store_task = [&](int w, int sw) {
+        if (w < ya || w >= yb)
+            return;
+        const double *urow = sm + A_U * AM + sw * WD;
+#pragma unroll
+        for (int p = 0; p < PPT; p++) {
+            const int h = m + p * NPG, sc = 2 * h, c = xl + sc;
+            if (sc < H || sc >= H + TX)
+                continue;
+            double *dst = a.uout + (long long)w * P + c;
+            const double ve = urow[h], vo = urow[HW + h];
+            if (c >= 1 && c + 1 <= nx)
+                *reinterpret_cast<double2 *>(dst) = make_double2(ve, vo);
+            else {
+                if (c >= 1 && c <= nx)
+                    dst[0] = ve;
+                if (c + 1 >= 1 && c + 1 <= nx)
+                    dst[1] = vo;
+            }
+        }
+    };
+
+    const Cols<PPT> kc = make_cols<WD, PPT, NPG>(m, xl, nx);
+
+    // Task groups: 5-point: 0,1 correction of even/odd columns; 2..NS+1 stage k = grp-1;
+    //              NS+2 store; NS+3, NS+4 split.
+    //              9-point: 0,1 active row stage(s) (phase A, B); 2,3 correction;
+    //              4 store; 5, 6 split.
+    constexpr int G_SPLIT = KIND == 5 ? NS + 3 : 5;
+    constexpr int QSPLIT = KIND == 5 ? 3 : 4;
+    const int tend = yb + 2 * NS + 1;
+    int tm = 0, tsd = 0;
+    for (int t = lo; t <= tend; t++, tm = (tm + 1 == RM) ? 0 : tm + 1, tsd = (tsd + 1 == SD) ? 0 : tsd + 1) {
+        if (producer) {
+            fence_proxy_async();
+            if (t + D <= hi)
+                issue_row(t + D);
+            issue_coarse(t);
+        }
+        if (grp >= C::NG) {
+            // producer warp: no compute task
+        } else if (grp >= G_SPLIT) {
+            if (t <= hi) {
+                mbar_wait(&bar[tsd], ((t - lo) / SD) & 1);
+                if (grp == G_SPLIT)
+                    split_row<AM, AS, WD, PPT, NPG>(sm, smS, tsd, tm, 0, QSPLIT, m);
+                else
+                    split_row<AM, AS, WD, PPT, NPG>(sm, smS, tsd, tm, QSPLIT, NA, m);
+            }
+        } else if (KIND == 5) {
+            if (grp < 2) {
+                correct_task(t - 1, back<RM>(tm, 1), grp);
+            } else if (grp < NS + 2) {
+                const int k = grp - 1, d = 2 * k + 1, r = t - d;
+                if (r > lo && r < hi && r >= 1 && r <= ny)
+                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1),
+                                                        back<RM>(tm, d - 1), (((k - 1) & 1) - r) & 1, kc);
+            } else {
+                store_task(t - 2 * NS - 2, back<RM>(tm, 2 * NS + 2));
+            }
+        } else {
+            // active 9-point row stage(s): k with (t-1-2k) & 1 == (k-1) & 1, i.e. (t + k) even
+            const int k = ((t & 1) ? 1 : 2) + 2 * grp, d = 2 * k + 1, r = t - d;
+            if (grp < 2) {
+                if (k <= NS && r > lo && r < hi && r >= 1 && r <= ny)
+                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1),
+                                                        back<RM>(tm, d - 1), 0, kc);
+            } else if (grp < 4) {
+                correct_task(t - 1, back<RM>(tm, 1), grp - 2);
+            } else {
+                store_task(t - 2 * NS - 2, back<RM>(tm, 2 * NS + 2));
+            }
+        }
+        __syncthreads();
+        if (KIND == 9) {
+            const int k = ((t & 1) ? 1 : 2) + 2 * grp, d = 2 * k + 1, r = t - d;
+            if (grp < 2 && k <= NS && r > lo && r < hi && r >= 1 && r <= ny)
+                colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), 1, kc);
+            __syncthreads();
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host side
+static int g_sms = 0;
+static size_t g_smem_optin = 0, g_smem_sm = 0;
+
+static void device_limits()
+{
+    if (g_sms)
+        return;
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    g_sms = v > 0 ? v : 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    g_smem_optin = v > 0 ? (size_t)v : 227 * 1024;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    g_smem_sm = v > 0 ? (size_t)v : 228 * 1024;
+}
+
+// Kernel instances: (kind, NS) -> (WD, D, pairs per thread).  WD = smem row width.
+template <int KIND, int NS>
+struct Inst {
+#ifndef BMG_WD5
+#define BMG_WD5 256
+#endif
+    static constexpr int WD_DN = KIND == 5 ? BMG_WD5 : 192;
+    static constexpr int D_DN = 4;
+#ifndef BMG_PPT5
+#define BMG_PPT5 2
+#endif
+    static constexpr int PPT_DN = KIND == 5 ? BMG_PPT5 : 1;
+    static constexpr int WD_UP = KIND == 5 ? BMG_WD5 : 256;
+    static constexpr int D_UP = 4;
+    static constexpr int PPT_UP = KIND == 5 ? BMG_PPT5 : 2;
+    using CD = Cfg<KIND, NS, WD_DN, D_DN, false, PPT_DN>;
+    using CU = Cfg<KIND, NS, WD_UP, D_UP, true, PPT_UP>;
+};
+
+template <int KIND, int NS>
+static void fill_geom(FusedGeom &g, bool up)
+{
+    using I = Inst<KIND, NS>;
+    if (!up) {
+        using C = typename I::CD;
+        g.TX = C::TX, g.H = C::H, g.WD = I::WD_DN, g.WC = C::WC, g.R = C::RM, g.D = I::D_DN, g.threads = C::NT;
+        g.smem = C::SMEM;
+    } else {
+        using C = typename I::CU;
+        g.TX = C::TX, g.H = C::H, g.WD = I::WD_UP, g.WC = C::WC, g.R = C::RM, g.D = I::D_UP, g.threads = C::NT;
+        g.smem = C::SMEM;
+    }
+    g.NS = NS;
+}
+
+template <int KIND, int NS>
+static void set_attrs()
+{
+    using I = Inst<KIND, NS>;
+    device_limits();
+    constexpr size_t sd = I::CD::SMEM, su = I::CU::SMEM;
+    if (sd <= g_smem_optin)
+        cudaFuncSetAttribute(k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sd);
+    if (su <= g_smem_optin)
+        cudaFuncSetAttribute(k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)su);
+    cudaGetLastError();  // an unsupported instance is simply not planned (plan_grid checks the size)
+}
+
+// Grid for one kernel: strips of TX columns x chunks of rows, chosen to balance
+// the per-SM work over waves (warm-up rows counted as overhead).
+static void plan_grid(FusedGeom &g, int nx, int ny, int warm)
+{
+    device_limits();
+    g.ok = false;
+    if (g.smem > g_smem_optin)
+        return;
+    int occ = (int)(g_smem_sm / (g.smem + 1024));
+    occ = std::min(occ, 2048 / g.threads);
+    if (occ < 1)
+        return;
+    const int slots = g_sms * occ;
+    g.nstrips = nx / g.TX + 1;
+    double best = 1e300;
+    for (int w = 1; w <= 32; w++) {
+        int nch = std::max(1, (int)((double)w * slots / g.nstrips + 0.5));
+        nch = std::min(nch, std::max(1, (ny + 1) / 8));
+        int chunk = (ny + 1 + nch - 1) / nch;
+        nch = (ny + 1 + chunk - 1) / chunk;
+        long long units = (long long)g.nstrips * nch;
+        long long waves = (units + slots - 1) / slots;
+        double cost = (double)waves * (chunk + warm + 8);
+        if (cost < best) {
+            best = cost;
+            g.nchunks = nch;
+            g.chunk = chunk;
+            g.ok = true;
+        }
+    }
+}
+
+bmg_status_t fused_plan_level(FusedPlan &fp, int l, int nx, int ny, long long pitch, int kind, int nu1, int nu2,
+                              bool aligned)
+{
+    LevelPlan &lp = fp.lv[l];
+    lp.down = lp.up = false;
+    if (!aligned || (pitch & 1) || nx < 8 || ny < 8 || nx > (1 << 24) || pitch > (1LL << 30))
+        return BMG_OK;
+    if ((nu1 != 1 && nu1 != 2) || (nu2 != 1 && nu2 != 2))
+        return BMG_OK;
+    static bool attrs = false;
+    if (!attrs) {
+        set_attrs<5, 2>();
+        set_attrs<5, 4>();
+        set_attrs<9, 2>();
+        set_attrs<9, 4>();
+        attrs = true;
+    }
+    const int nsd = 2 * nu1, nsu = 2 * nu2;
+    if (kind == 5) {
+        nsd == 2 ? fill_geom<5, 2>(lp.gd, false) : fill_geom<5, 4>(lp.gd, false);
+        nsu == 2 ? fill_geom<5, 2>(lp.gu, true) : fill_geom<5, 4>(lp.gu, true);
+    } else {
+        nsd == 2 ? fill_geom<9, 2>(lp.gd, false) : fill_geom<9, 4>(lp.gd, false);
+        nsu == 2 ? fill_geom<9, 2>(lp.gu, true) : fill_geom<9, 4>(lp.gu, true);
+    }
+    plan_grid(lp.gd, nx, ny, 2 * nsd + 4);
+    plan_grid(lp.gu, nx, ny, 2 * nsu + 2);
+    lp.down = lp.gd.ok;
+    lp.up = lp.gu.ok;
     return BMG_OK;
 }
 
-bool fused_down(const FusedPlan &fp, int l, const Op &, const CIv &, const double *, double *, double *, double *,
-                const Op &, int, cudaStream_t, int *)
+static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
+static bool ptrs_ok(const Op &A, const CIv &ci, std::initializer_list<const void *> extra)
 {
-    return l < fp.nlev && false;
+    if (!aligned16(A.O) || !aligned16(A.W) || !aligned16(A.S))
+        return false;
+    if (A.kind == 9 && (!aligned16(A.SW) || !aligned16(A.NW)))
+        return false;
+    if (ci.pitch & 1)
+        return false;
+    for (int k = 0; k < 8; k++)
+        if (!aligned16(ci.w[k]))
+            return false;
+    for (const void *p : extra)
+        if (p && !aligned16(p))
+            return false;
+    return true;
 }
 
-bool fused_up(const FusedPlan &fp, int l, const Op &, const CIv &, const double *, double *, const double *, int,
-              cudaStream_t, int *)
+template <int KIND, int NS>
+static void launch_down(const FusedGeom &g, const FArgs &a, cudaStream_t s)
 {
-    return l < fp.nlev && false;
+    using I = Inst<KIND, NS>;
+    k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a);
+}
+
+template <int KIND, int NS>
+static void launch_up(const FusedGeom &g, const FArgs &a, cudaStream_t s)
+{
+    using I = Inst<KIND, NS>;
+    k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a);
+}
+
+static FArgs make_args(const FusedGeom &g, const Op &A, const CIv &ci)
+{
+    FArgs a;
+    a.A = A;
+    a.ci = ci;
+    a.f = a.uin = a.ec = nullptr;
+    a.uout = a.fc = a.uc = nullptr;
+    a.nstrips = g.nstrips;
+    a.chunk = g.chunk;
+    a.ncx = A.nx / 2;
+    a.ncy = A.ny / 2;
+    return a;
+}
+
+bool fused_down(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const double *f, const double *uin,
+                double *uout, double *fc, double *uc, cudaStream_t s, int *nlaunch)
+{
+    if (l >= 32 || !fp.lv[l].down || !ptrs_ok(A, ci, {f, uin, uout, fc, uc}))
+        return false;
+    const FusedGeom &g = fp.lv[l].gd;
+    FArgs a = make_args(g, A, ci);
+    a.f = f;
+    a.uin = uin;
+    a.uout = uout;
+    a.fc = fc;
+    a.uc = uc;
+    if (A.kind == 5)
+        g.NS == 2 ? launch_down<5, 2>(g, a, s) : launch_down<5, 4>(g, a, s);
+    else
+        g.NS == 2 ? launch_down<9, 2>(g, a, s) : launch_down<9, 4>(g, a, s);
+    if (nlaunch)
+        *nlaunch += 1;
+    return true;
+}
+
+bool fused_up(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const double *f, const double *uin,
+              const double *ec, double *uout, cudaStream_t s, int *nlaunch)
+{
+    if (l >= 32 || !fp.lv[l].up || !ptrs_ok(A, ci, {f, uin, uout, ec}))
+        return false;
+    const FusedGeom &g = fp.lv[l].gu;
+    FArgs a = make_args(g, A, ci);
+    a.f = f;
+    a.uin = uin;
+    a.ec = ec;
+    a.uout = uout;
+    if (A.kind == 5)
+        g.NS == 2 ? launch_up<5, 2>(g, a, s) : launch_up<5, 4>(g, a, s);
+    else
+        g.NS == 2 ? launch_up<9, 2>(g, a, s) : launch_up<9, 4>(g, a, s);
+    if (nlaunch)
+        *nlaunch += 1;
+    return true;
 }
 
 }  // namespace bmg

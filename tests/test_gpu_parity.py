@@ -214,3 +214,48 @@ def test_vcycle_host_matches_device():
     torch.cuda.synchronize()
     assert torch.equal(x.cpu(), xh)
     s.close()
+
+
+LEG_CASES = [("poisson", 31, 31), ("lognormal", 63, 63), ("checker", 127, 127), ("aniso", 63, 63),
+             ("random9", 33, 33), ("lognormal", 64, 30), ("checker_off3", 95, 47), ("lognormal", 300, 257),
+             ("random9", 200, 131), ("lognormal", 9, 8)]
+
+
+@pytest.mark.parametrize("wl,nx,ny", LEG_CASES)
+@pytest.mark.parametrize("fused", [1, 0])
+def test_leg_parity_level0(orc, wl, nx, ny, fused):
+    """The two legs the cycle runs on level 0 (fused streaming kernel when fused=1)
+    against the oracle's steps: down = relax^nu1, residual, restriction;
+    up = interpolation + correction, relax^nu2."""
+    st = P.workload(wl, nx, ny)
+    prm = bmg.bmg_params_default()
+    prm.fused = fused
+    s = bmg.Solver(st, prm)
+    if s.L < 2:
+        pytest.skip("single level")
+    st9 = orc.expand_stencil(st)
+    _, ci = orc.Hierarchy(st).export_level(0)
+    f = P.field_uniform(nx, ny, seed=41)
+    u0 = P.field_uniform(nx, ny, seed=42)
+    # down leg
+    uin, uout = s.grid(u0), s.grid()
+    fc, uc = s.level_grid(1), s.level_grid(1, np.full((ny // 2 + 2, nx // 2 + 2), 7.0))
+    bmg.bmg_smooth_restrict(s.h, 0, s.grid(f), uin, uout, fc, uc)
+    torch.cuda.synchronize()
+    u_ref = orc.relax(st9, st.kind, f, u0, 2)
+    fc_ref = orc.restrict(ci, orc.residual(st9, f, u_ref))
+    assert_iterate_close(bmg.from_device(uout, nx), u_ref, rtol=1e-13)
+    assert_iterate_close(bmg.from_device(fc, nx // 2), fc_ref, rtol=1e-12)
+    ucn = bmg.from_device(uc, nx // 2)
+    assert np.all(ucn[1:-1, 1:-1] == 0.0)
+    assert torch.equal(uin, s.grid(u0))  # input untouched
+    # up leg
+    ec = P.field_uniform(nx // 2, ny // 2, seed=43)
+    uout2 = s.grid()
+    bmg.bmg_correct_smooth(s.h, 0, s.grid(f), s.grid(u0), s.level_grid(1, ec), uout2)
+    torch.cuda.synchronize()
+    ref = orc.relax(st9, st.kind, f, orc.interp_add(ci, ec, u0), 1)
+    got = bmg.from_device(uout2, nx)
+    assert_iterate_close(got, ref, rtol=1e-13)
+    assert np.all(got[0, :] == 0) and np.all(got[:, 0] == 0) and np.all(got[-1, :] == 0) and np.all(got[:, -1] == 0)
+    s.close()
