@@ -169,8 +169,12 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
         v.pitch = l == 0 ? st->pitch : round_pitch(v.nx);
         size_t np = (size_t)(v.ny + 2) * (size_t)v.pitch;
         int npl = v.kind == 9 ? 5 : 3;
-        for (int k = 0; k < npl; k++)
-            TRY(dalloc(h, &v.pl[k], np));
+        {  // the planes of a level form one block (plane stride np): one 3-D TMA box per row
+            double *blk = nullptr;
+            TRY(dalloc(h, &blk, np * npl));
+            for (int k = 0; k < npl; k++)
+                v.pl[k] = blk + k * np;
+        }
         TRY(dalloc(h, &v.r, np));
         if (l > 0) {
             TRY(dalloc(h, &v.u, np));
@@ -184,10 +188,11 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
     for (int l = 0; l + 1 < h->L; l++) {
         Level &c = h->lv[l + 1];
         size_t np = (size_t)(c.ny + 2) * (size_t)c.pitch;
-        for (int k = 0; k < 8; k++) {
-            TRY(dalloc(h, &h->lv[l].ci[k], np));
-            CK(cudaMemsetAsync(h->lv[l].ci[k], 0, np * sizeof(double), s));
-        }
+        double *blk = nullptr;  // the 8 weight planes form one block (plane stride np)
+        TRY(dalloc(h, &blk, np * 8));
+        CK(cudaMemsetAsync(blk, 0, 8 * np * sizeof(double), s));
+        for (int k = 0; k < 8; k++)
+            h->lv[l].ci[k] = blk + k * np;
     }
     {
         void *q;

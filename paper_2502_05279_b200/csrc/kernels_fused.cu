@@ -28,6 +28,8 @@
 // h (smem columns 2h, 2h+1), h lane-consecutive.  Each group does one kind of
 // task per step (a colour stage, a residual parity, store, restriction, split),
 // loading all operands of its points before the arithmetic.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -71,10 +73,32 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  : "memory");
 }
 
+// Tiled tensor TMA: one box (out-of-bounds elements zero-filled) into smem.
+__device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *m, int x, int y, uint64_t *b)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(smem_u32(b))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_3d(void *dst, const CUtensorMap *m, int x, int y, int z, uint64_t *b)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(b))
+        : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
 // ------------------------------------------------------------------ configuration
+#ifndef BMG_EXP
+#define BMG_EXP 0  // timing-study mask: skip 1 stages, 2 residual, 4 restriction, 8 split, 16 store, 32 TMA
+#endif
 constexpr int DC = 4;  // coarse-row prefetch distance (row steps); < 6 for safe ring reuse
 constexpr int CH = 4;  // coarse halo columns on each side of a strip
 
@@ -92,7 +116,7 @@ struct Cfg {
     static constexpr int RM = UP ? 2 * NS + 3 : 2 * NS + 4;     // main (split) ring rows
     static constexpr int SD = D + 1;                           // staging (natural) ring rows
     static constexpr int AM = RM * WD, AS = SD * WD;           // doubles per array block
-    static constexpr int WC = TX / 2 + 2 * CH;
+    static constexpr int WC = (TX / 2 + 2 * CH + 15) / 16 * 16;  // coarse box width (128-B rows)
     static constexpr int NPG = HW / PPT;                       // threads per task group
     static constexpr int NSPLIT = 2;                           // split task groups
     static constexpr int NG = UP ? (KIND == 5 ? NS + 3 + NSPLIT : 5 + NSPLIT)
@@ -112,6 +136,13 @@ struct FArgs {
     const double *f, *uin, *ec;
     double *uout, *fc, *uc;
     int nstrips, chunk, ncx, ncy;
+};
+
+// TMA descriptors of one launch (kernel parameter, __grid_constant__):
+// u (rows of u_in), f, a (the operator's plane block, 3-D), c (the 8 weight
+// planes, 3-D), e (coarse correction, up leg).
+struct TMaps {
+    CUtensorMap u, f, a, c, e;
 };
 
 // ring slot of the row `d` rows behind the newest (ts = slot of row t)
@@ -261,7 +292,7 @@ __device__ __forceinline__ void colour_pass(double *sm, int s0, int sm1, int sp1
 
 // De-interleave staging row (natural order, slot ss) into main ring row (slot s0)
 // for arrays [q0, q1): even columns to the first half, odd to the second.
-template <int AM, int AS, int WD, int PPT, int NPG>
+template <int NA, int AM, int WD, int PPT, int NPG>
 __device__ __forceinline__ void split_row(double *smM, const double *smS, int ss, int s0, int q0, int q1, int m)
 {
     constexpr int HW = WD / 2;
@@ -272,7 +303,7 @@ __device__ __forceinline__ void split_row(double *smM, const double *smS, int ss
         double2 v[PPT];
 #pragma unroll
         for (int p = 0; p < PPT; p++)
-            v[p] = *reinterpret_cast<const double2 *>(smS + q * AS + ss * WD + 2 * (m + p * NPG));
+            v[p] = *reinterpret_cast<const double2 *>(smS + (ss * NA + q) * WD + 2 * (m + p * NPG));
 #pragma unroll
         for (int p = 0; p < PPT; p++) {
             double *row = smM + q * AM + s0 * WD;
@@ -284,7 +315,8 @@ __device__ __forceinline__ void split_row(double *smM, const double *smS, int ss
 
 // ------------------------------------------------------------------ down kernel
 template <int KIND, int NS, int WD, int D, int PPT>
-__global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT) k_fused_down(FArgs a)
+__global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT)
+    k_fused_down(FArgs a, const __grid_constant__ TMaps tmaps)
 {
     using C = Cfg<KIND, NS, WD, D, false, PPT>;
     constexpr int NA = C::NA, H = C::H, TX = C::TX, WC = C::WC, HW = C::HW, NPG = C::NPG;
@@ -323,22 +355,19 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT) k_fused_
     }
     __syncthreads();
 
+    // Staging slot s holds NA natural rows [U | F | O W S (SW NW)], one TMA box
+    // each for u and f and ONE 3-D box for the operator's plane block.
     int Knext = Jlo;
     auto issue_row = [&](int row) {
         const int slot = (row - lo) % SD;
         uint64_t *b = &bar[slot];
-        mbar_arrive_tx(b, rowbytes * NA);
-        const long long go = row * P + cs;
-        double *d = smS + slot * WD + soff;
-        bulk_g2s(d + A_U * AS, a.uin + go, rowbytes, b);
-        bulk_g2s(d + A_F * AS, a.f + go, rowbytes, b);
-        bulk_g2s(d + A_O * AS, a.A.O + go, rowbytes, b);
-        bulk_g2s(d + A_W * AS, a.A.W + go, rowbytes, b);
-        bulk_g2s(d + A_S * AS, a.A.S + go, rowbytes, b);
-        if (KIND == 9) {
-            bulk_g2s(d + A_SW * AS, a.A.SW + go, rowbytes, b);
-            bulk_g2s(d + A_NW * AS, a.A.NW + go, rowbytes, b);
-        }
+        mbar_arrive_tx(b, (BMG_EXP & 32) ? 0u : (uint32_t)(NA * WD * 8));
+        if (BMG_EXP & 32)
+            return;
+        double *d = smS + slot * (NA * WD);
+        tma_2d(d + A_U * WD, &tmaps.u, xl, row, b);
+        tma_2d(d + A_F * WD, &tmaps.f, xl, row, b);
+        tma_3d(d + A_O * WD, &tmaps.a, xl, row, 0, b);
     };
     auto issue_coarse = [&](int t) {
         while (Knext <= Kend) {
@@ -347,9 +376,8 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT) k_fused_
                 break;
             const int slot = (Knext - Jlo) & 3;
             uint64_t *b = &bar[SD + slot];
-            mbar_arrive_tx(b, crowbytes * 8);
-            for (int q = 0; q < 8; q++)
-                bulk_g2s(sC + (slot * 8 + q) * WC + csoff, a.ci.w[q] + Knext * CP + ccs, crowbytes, b);
+            mbar_arrive_tx(b, (uint32_t)(8 * WC * 8));
+            tma_3d(sC + slot * 8 * WC, &tmaps.c, cxl, Knext, 0, b);
             Knext++;
         }
     };
@@ -446,10 +474,12 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT) k_fused_
     int tm = 0, tsd = 0;  // main / staging ring slots of row t
     for (int t = lo; t <= tend; t++, tm = (tm + 1 == RM) ? 0 : tm + 1, tsd = (tsd + 1 == SD) ? 0 : tsd + 1) {
         if (producer) {
-            fence_proxy_async();
+            // No proxy fence: staging slots are only READ by generic-proxy code before the
+            // TMA (async proxy) overwrites them, and the step barrier orders that WAR.
             if (t + D <= hi)
                 issue_row(t + D);
-            issue_coarse(t);
+            if (!(BMG_EXP & 64))
+                issue_coarse(t);
         }
         const int jr = t - 2 * NS - 4;
         const int J = jr >> 1;
@@ -459,23 +489,26 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT) k_fused_
         } else if (grp >= G_SPLIT) {
             if (t <= hi) {
                 mbar_wait(&bar[tsd], ((t - lo) / SD) & 1);
-                if (grp == G_SPLIT)
-                    split_row<AM, AS, WD, PPT, NPG>(sm, smS, tsd, tm, 0, QSPLIT, m);
+                if (BMG_EXP & 8) {
+                } else if (grp == G_SPLIT)
+                    split_row<NA, AM, WD, PPT, NPG>(sm, smS, tsd, tm, 0, QSPLIT, m);
                 else
-                    split_row<AM, AS, WD, PPT, NPG>(sm, smS, tsd, tm, QSPLIT, NA, m);
+                    split_row<NA, AM, WD, PPT, NPG>(sm, smS, tsd, tm, QSPLIT, NA, m);
             }
         } else if (KIND == 5) {
             if (grp < NS) {
                 const int k = grp + 1, d = 2 * k, r = t - d;
-                if (r > lo && r < hi && r >= 1 && r <= ny)
+                if (!(BMG_EXP & 1) && r > lo && r < hi && r >= 1 && r <= ny)
                     colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1),
                                                         back<RM>(tm, d - 1), (((k - 1) & 1) - r) & 1, kc);
             } else if (grp <= NS + 1) {
                 const int d = 2 * NS + 2;
-                resid_task(t - d, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), grp - NS);
+                if (!(BMG_EXP & 2))
+                    resid_task(t - d, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), grp - NS);
             } else if (grp == NS + 2) {
-                store_task(t - 2 * NS - 3, back<RM>(tm, 2 * NS + 3));
-            } else if (restr) {
+                if (!(BMG_EXP & 16))
+                    store_task(t - 2 * NS - 3, back<RM>(tm, 2 * NS + 3));
+            } else if (restr && !(BMG_EXP & 4)) {
                 restrict_task(J);
             }
         } else {
@@ -506,7 +539,8 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT) k_fused_
 
 // ------------------------------------------------------------------ up kernel
 template <int KIND, int NS, int WD, int D, int PPT>
-__global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT) k_fused_up(FArgs a)
+__global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT)
+    k_fused_up(FArgs a, const __grid_constant__ TMaps tmaps)
 {
     using C = Cfg<KIND, NS, WD, D, true, PPT>;
     constexpr int NA = C::NA, H = C::H, TX = C::TX, WC = C::WC, HW = C::HW, NPG = C::NPG;
@@ -549,18 +583,13 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT) k_fused_u
     auto issue_row = [&](int row) {
         const int slot = (row - lo) % SD;
         uint64_t *b = &bar[slot];
-        mbar_arrive_tx(b, rowbytes * NA);
-        const long long go = row * P + cs;
-        double *d = smS + slot * WD + soff;
-        bulk_g2s(d + A_U * AS, a.uin + go, rowbytes, b);
-        bulk_g2s(d + A_F * AS, a.f + go, rowbytes, b);
-        bulk_g2s(d + A_O * AS, a.A.O + go, rowbytes, b);
-        bulk_g2s(d + A_W * AS, a.A.W + go, rowbytes, b);
-        bulk_g2s(d + A_S * AS, a.A.S + go, rowbytes, b);
-        if (KIND == 9) {
-            bulk_g2s(d + A_SW * AS, a.A.SW + go, rowbytes, b);
-            bulk_g2s(d + A_NW * AS, a.A.NW + go, rowbytes, b);
-        }
+        mbar_arrive_tx(b, (BMG_EXP & 32) ? 0u : (uint32_t)(NA * WD * 8));
+        if (BMG_EXP & 32)
+            return;
+        double *d = smS + slot * (NA * WD);
+        tma_2d(d + A_U * WD, &tmaps.u, xl, row, b);
+        tma_2d(d + A_F * WD, &tmaps.f, xl, row, b);
+        tma_3d(d + A_O * WD, &tmaps.a, xl, row, 0, b);
     };
     auto issue_coarse = [&](int t) {
         while (Knext <= Khi) {
@@ -569,10 +598,9 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT) k_fused_u
                 break;
             const int slot = (Knext - Klo) & 3;
             uint64_t *b = &bar[SD + slot];
-            mbar_arrive_tx(b, crowbytes * 9);
-            bulk_g2s(sE + slot * WC + csoff, a.ec + Knext * CP + ccs, crowbytes, b);
-            for (int q = 0; q < 8; q++)
-                bulk_g2s(sC + (slot * 8 + q) * WC + csoff, a.ci.w[q] + Knext * CP + ccs, crowbytes, b);
+            mbar_arrive_tx(b, (uint32_t)(9 * WC * 8));
+            tma_2d(sE + slot * WC, &tmaps.e, cxl, Knext, b);
+            tma_3d(sC + slot * 8 * WC, &tmaps.c, cxl, Knext, 0, b);
             Knext++;
         }
     };
@@ -656,10 +684,12 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT) k_fused_u
     int tm = 0, tsd = 0;
     for (int t = lo; t <= tend; t++, tm = (tm + 1 == RM) ? 0 : tm + 1, tsd = (tsd + 1 == SD) ? 0 : tsd + 1) {
         if (producer) {
-            fence_proxy_async();
+            // No proxy fence: staging slots are only READ by generic-proxy code before the
+            // TMA (async proxy) overwrites them, and the step barrier orders that WAR.
             if (t + D <= hi)
                 issue_row(t + D);
-            issue_coarse(t);
+            if (!(BMG_EXP & 64))
+                issue_coarse(t);
         }
         if (grp >= C::NG) {
             // producer warp: no compute task
@@ -667,9 +697,9 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT) k_fused_u
             if (t <= hi) {
                 mbar_wait(&bar[tsd], ((t - lo) / SD) & 1);
                 if (grp == G_SPLIT)
-                    split_row<AM, AS, WD, PPT, NPG>(sm, smS, tsd, tm, 0, QSPLIT, m);
+                    split_row<NA, AM, WD, PPT, NPG>(sm, smS, tsd, tm, 0, QSPLIT, m);
                 else
-                    split_row<AM, AS, WD, PPT, NPG>(sm, smS, tsd, tm, QSPLIT, NA, m);
+                    split_row<NA, AM, WD, PPT, NPG>(sm, smS, tsd, tm, QSPLIT, NA, m);
             }
         } else if (KIND == 5) {
             if (grp < 2) {
@@ -856,18 +886,79 @@ static bool ptrs_ok(const Op &A, const CIv &ci, std::initializer_list<const void
     return true;
 }
 
-template <int KIND, int NS>
-static void launch_down(const FusedGeom &g, const FArgs &a, cudaStream_t s)
+// ---- TMA tensor maps (driver entry point fetched through the runtime; no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
 {
-    using I = Inst<KIND, NS>;
-    k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a);
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+        cudaGetLastError();
+    }
+    return fn;
+}
+
+// rank-3 fp64 map over `planes` planes of rows x width elements (row pitch, plane
+// stride in elements); box = bw columns x 1 row x planes.  Rank 2 when planes == 0.
+static bool make_map(CUtensorMap *m, const double *base, long long width, long long rows, long long pitch,
+                     long long pstride, int planes, int bw)
+{
+    auto fn = encode_fn();
+    if (!fn)
+        return false;
+    cuuint64_t dims[3] = {(cuuint64_t)width, (cuuint64_t)rows, (cuuint64_t)(planes > 0 ? planes : 1)};
+    cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)pstride * 8};
+    cuuint32_t box[3] = {(cuuint32_t)bw, 1, (cuuint32_t)(planes > 0 ? planes : 1)};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, planes > 0 ? 3 : 2, (void *)base, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// Maps of one fused launch: the planes and the weights must be contiguous blocks.
+static bool make_maps(TMaps &tm, const FusedGeom &g, const Op &A, const CIv &ci, const double *uin, const double *f,
+                      const double *ec)
+{
+    const long long np = (A.ny + 2) * A.pitch;
+    const int npl = A.kind == 9 ? 5 : 3;
+    const double *pl[5] = {A.O, A.W, A.S, A.SW, A.NW};
+    for (int k = 1; k < npl; k++)
+        if (pl[k] != A.O + k * np)
+            return false;
+    const int ncx = A.nx / 2, ncy = A.ny / 2;
+    const long long npc = (ncy + 2) * ci.pitch;
+    for (int k = 1; k < 8; k++)
+        if (ci.w[k] != ci.w[0] + k * npc)
+            return false;
+    bool ok = make_map(&tm.u, uin, A.nx + 2, A.ny + 2, A.pitch, 0, 0, g.WD) &&
+              make_map(&tm.f, f, A.nx + 2, A.ny + 2, A.pitch, 0, 0, g.WD) &&
+              make_map(&tm.a, A.O, A.nx + 2, A.ny + 2, A.pitch, np, npl, g.WD) &&
+              make_map(&tm.c, ci.w[0], ncx + 2, ncy + 2, ci.pitch, npc, 8, g.WC);
+    if (ok && ec)
+        ok = make_map(&tm.e, ec, ncx + 2, ncy + 2, ci.pitch, 0, 0, g.WC);
+    else
+        tm.e = tm.c;
+    return ok;
 }
 
 template <int KIND, int NS>
-static void launch_up(const FusedGeom &g, const FArgs &a, cudaStream_t s)
+static void launch_down(const FusedGeom &g, const FArgs &a, const TMaps &tm, cudaStream_t s)
 {
     using I = Inst<KIND, NS>;
-    k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a);
+    k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a, tm);
+}
+
+template <int KIND, int NS>
+static void launch_up(const FusedGeom &g, const FArgs &a, const TMaps &tm, cudaStream_t s)
+{
+    using I = Inst<KIND, NS>;
+    k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a, tm);
 }
 
 static FArgs make_args(const FusedGeom &g, const Op &A, const CIv &ci)
@@ -896,10 +987,13 @@ bool fused_down(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const do
     a.uout = uout;
     a.fc = fc;
     a.uc = uc;
+    TMaps tm;
+    if (!make_maps(tm, g, A, ci, uin, f, nullptr))
+        return false;
     if (A.kind == 5)
-        g.NS == 2 ? launch_down<5, 2>(g, a, s) : launch_down<5, 4>(g, a, s);
+        g.NS == 2 ? launch_down<5, 2>(g, a, tm, s) : launch_down<5, 4>(g, a, tm, s);
     else
-        g.NS == 2 ? launch_down<9, 2>(g, a, s) : launch_down<9, 4>(g, a, s);
+        g.NS == 2 ? launch_down<9, 2>(g, a, tm, s) : launch_down<9, 4>(g, a, tm, s);
     if (nlaunch)
         *nlaunch += 1;
     return true;
@@ -916,10 +1010,13 @@ bool fused_up(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const doub
     a.uin = uin;
     a.ec = ec;
     a.uout = uout;
+    TMaps tm;
+    if (!make_maps(tm, g, A, ci, uin, f, ec))
+        return false;
     if (A.kind == 5)
-        g.NS == 2 ? launch_up<5, 2>(g, a, s) : launch_up<5, 4>(g, a, s);
+        g.NS == 2 ? launch_up<5, 2>(g, a, tm, s) : launch_up<5, 4>(g, a, tm, s);
     else
-        g.NS == 2 ? launch_up<9, 2>(g, a, s) : launch_up<9, 4>(g, a, s);
+        g.NS == 2 ? launch_up<9, 2>(g, a, tm, s) : launch_up<9, 4>(g, a, tm, s);
     if (nlaunch)
         *nlaunch += 1;
     return true;

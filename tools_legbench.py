@@ -6,6 +6,7 @@ from paper_2502_05279_b200 import bmg, problems as P
 
 n = int(os.environ.get("N", "8191"))
 wl = os.environ.get("WL", "poisson")
+legs = os.environ.get("LEGS", "down,up,cycle").split(",")
 st = P.workload(wl, n, n)
 s = bmg.Solver(st)
 f = s.grid(P.rhs_const(n, n)); u = s.grid(); u2 = s.grid()
@@ -16,9 +17,14 @@ def timeit(fn, rep=10):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); [fn() for _ in range(rep)]; e1.record(); torch.cuda.synchronize()
     return e0.elapsed_time(e1) / rep
-td = timeit(lambda: bmg.bmg_smooth_restrict(s.h, 0, f, u, u2, fc, uc))
-tu = timeit(lambda: bmg.bmg_correct_smooth(s.h, 0, f, u, uc, u2))
-tv = timeit(lambda: s.vcycle(f, u, 1))
+out = {"lib": os.environ.get("BMG_LIB", "").split("/")[-1], "wl": wl, "n": n}
 N = n * n
-print(json.dumps({"tx": os.environ.get("BMG_FUSED_TX"), "wl": wl, "down_ms": td, "up_ms": tu, "cycle_ms": tv,
-                  "down_GBps_68B": 68 * N / td / 1e6, "up_GBps_66B": 66 * N / tu / 1e6}))
+if "down" in legs:
+    out["down_ms"] = timeit(lambda: bmg.bmg_smooth_restrict(s.h, 0, f, u, u2, fc, uc))
+    out["down_GBps_68B"] = 68 * N / out["down_ms"] / 1e6
+if "up" in legs:
+    out["up_ms"] = timeit(lambda: bmg.bmg_correct_smooth(s.h, 0, f, u, uc, u2))
+    out["up_GBps_66B"] = 66 * N / out["up_ms"] / 1e6
+if "cycle" in legs:
+    out["cycle_ms"] = timeit(lambda: s.vcycle(f, u, 1))
+print(json.dumps(out))

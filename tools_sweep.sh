@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
 timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 600 python bench.py 2>&1 | tail -1 > gpurun_out/bench1.json; cat gpurun_out/bench1.json
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches1.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
+timeout 120 python tools_legbench.py 2>&1 | tail -1
+WL=aniso N=4095 timeout 120 python tools_legbench.py 2>&1 | tail -1
+LEGS=down BMG_LIB=$PWD/variants_exp31.so timeout 60 python tools_legbench.py 2>&1 | tail -1
