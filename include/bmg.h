@@ -173,6 +173,52 @@ bmg_status_t bmg_correct_smooth(bmg_solver_t h, int level, const double *f, cons
 /* Number of kernels one bmg_vcycle cycle launches (the captured graph's kernel nodes). */
 bmg_status_t bmg_cycle_kernel_count(bmg_solver_t h, int *count);
 
+/* ---------------------------------------------------------------------------
+ * Multi-GPU: row-slab domain decomposition.
+ *
+ * Rows 1..ny are split into nranks contiguous slabs [y_p, y_{p+1}) whose
+ * starts are multiples of 2^K, K = number of distributed levels (largest K
+ * keeping at least max(agglom_rows, 2*BMG_HALO) rows per rank on level K-1).
+ * Level K and below are replicated on every rank (agglomeration by
+ * all-gather).  A rank's LOCAL arrays hold global rows
+ * [row0, row0+nrows) = [max(y_p - BMG_HALO, 0), min(y_{p+1} + BMG_HALO, ny+2)),
+ * pitch as in bmg_stencil_t: the owned rows plus BMG_HALO ghost rows, which
+ * the library overwrites (also in rhs) with the neighbours' values.
+ * ------------------------------------------------------------------------- */
+#define BMG_HALO 6
+
+typedef struct {
+    int nranks;           /* number of slabs (>= 1) */
+    int rank;             /* this process's slab (NCCL mode) */
+    void *nccl_comm;      /* ncclComm_t over the nranks processes (NCCL mode) */
+    const char *nccl_lib; /* path of the libnccl.so.2 to dlopen (NULL: "libnccl.so.2") */
+    int loopback;         /* 1: all nranks slabs simulated in THIS process on the current
+                             GPU, ghost rows copied device-to-device (tests); stencil,
+                             rhs and x are then GLOBAL arrays */
+} bmg_comm_t;
+
+/* Host-only: slab boundaries ybounds[0..nranks] (y_0 = 1, y_nranks = ny+1) and the
+ * number of distributed levels *kdist for an nx*ny grid.  EINVAL if the grid is too
+ * small for nranks slabs.  params may be NULL. */
+bmg_status_t bmg_partition(int nx, int ny, int nranks, const bmg_params_t *params, int *ybounds, int *kdist);
+
+/*
+ * Distributed setup.  stencil->nx, ny are the GLOBAL sizes; in NCCL mode its planes
+ * are this rank's local arrays (rows [row0, row0+nrows) of bmg_local_rows; only the
+ * owned rows are read), in loopback mode the global arrays.  Collective over the
+ * communicator.  The returned handle works with bmg_vcycle, bmg_solve,
+ * bmg_residual_norm, bmg_num_levels, bmg_local_rows and bmg_destroy; rhs and x are
+ * local arrays (NCCL) or global arrays (loopback).  Errors: EINVAL (grid too small,
+ * params unsupported: needs fused = 1, nu1, nu2 in {1,2}), ENCCL, ENOMEM, ECUDA.
+ */
+bmg_status_t bmg_setup_dist(const bmg_stencil_t *stencil, const bmg_comm_t *comm, const bmg_params_t *params,
+                            void *cuda_stream, bmg_solver_t *out);
+
+/* Local layout of this rank's level-0 arrays: stored global rows [row0, row0+nrows),
+ * owned rows [ylo, yhi), distributed levels kdist.  Any pointer may be NULL.  For a
+ * single-GPU handle: row0 = 0, nrows = ny+2, [1, ny+1), kdist = 0. */
+bmg_status_t bmg_local_rows(bmg_solver_t h, int *row0, int *nrows, int *ylo, int *yhi, int *kdist);
+
 /* Free everything owned by the handle (synchronises the device). NULL is OK. */
 bmg_status_t bmg_destroy(bmg_solver_t h);
 

@@ -23,8 +23,10 @@ EXPORTS = (
     "bmg_params_default", "bmg_setup", "bmg_vcycle", "bmg_vcycle_host", "bmg_solve", "bmg_residual_norm",
     "bmg_num_levels", "bmg_level_shape", "bmg_level_pitch", "bmg_export_level", "bmg_relax", "bmg_residual",
     "bmg_restrict", "bmg_interp_add", "bmg_smooth_restrict", "bmg_correct_smooth", "bmg_cycle_kernel_count", "bmg_destroy", "bmg_strerror",
-    "bmg_last_error_detail",
+    "bmg_last_error_detail", "bmg_partition", "bmg_setup_dist", "bmg_local_rows",
 )
+
+BMG_HALO = 6
 
 
 class bmg_stencil_t(ctypes.Structure):
@@ -36,6 +38,11 @@ class bmg_params_t(ctypes.Structure):
     _fields_ = [("nu1", ctypes.c_int), ("nu2", ctypes.c_int), ("coarsest", ctypes.c_int),
                 ("max_levels", ctypes.c_int), ("agglom_rows", ctypes.c_int), ("cycle_sym", ctypes.c_int),
                 ("fused", ctypes.c_int)]
+
+
+class bmg_comm_t(ctypes.Structure):
+    _fields_ = [("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_comm", ctypes.c_void_p),
+                ("nccl_lib", ctypes.c_char_p), ("loopback", ctypes.c_int)]
 
 
 class BmgError(RuntimeError):
@@ -79,6 +86,10 @@ def lib():
             "bmg_destroy": (i, [vp]),
             "bmg_strerror": (ctypes.c_char_p, [i]),
             "bmg_last_error_detail": (ctypes.c_char_p, []),
+            "bmg_partition": (i, [i, i, i, ctypes.POINTER(bmg_params_t), ip, ip]),
+            "bmg_setup_dist": (i, [ctypes.POINTER(bmg_stencil_t), ctypes.POINTER(bmg_comm_t),
+                                   ctypes.POINTER(bmg_params_t), vp, ctypes.POINTER(vp)]),
+            "bmg_local_rows": (i, [vp, ip, ip, ip, ip, ip]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -215,6 +226,36 @@ def bmg_cycle_kernel_count(h) -> int:
     c = ctypes.c_int()
     _check(lib().bmg_cycle_kernel_count(h, ctypes.byref(c)), "bmg_cycle_kernel_count")
     return c.value
+
+
+def bmg_partition(nx: int, ny: int, nranks: int, params: bmg_params_t | None = None):
+    """Host-only: (slab boundaries y_0..y_nranks, number of distributed levels)."""
+    yb = (ctypes.c_int * (nranks + 1))()
+    k = ctypes.c_int()
+    _check(lib().bmg_partition(nx, ny, nranks, ctypes.byref(params) if params is not None else None, yb,
+                               ctypes.byref(k)), "bmg_partition")
+    return list(yb), k.value
+
+
+def bmg_setup_dist(planes, kind: int, nx: int, ny: int, pitch: int, comm: bmg_comm_t,
+                   params: bmg_params_t | None = None, stream=None) -> ctypes.c_void_p:
+    """planes: device tensors (local arrays in NCCL mode, global arrays in loopback mode)."""
+    st = bmg_stencil_t()
+    st.kind, st.nx, st.ny, st.pitch = kind, nx, ny, pitch
+    for k, p in enumerate(planes):
+        st.plane[k] = p.data_ptr()
+    h = ctypes.c_void_p()
+    _check(lib().bmg_setup_dist(ctypes.byref(st), ctypes.byref(comm),
+                                ctypes.byref(params) if params is not None else None, _stream(stream),
+                                ctypes.byref(h)), "bmg_setup_dist")
+    return h
+
+
+def bmg_local_rows(h):
+    """(row0, nrows, ylo, yhi, kdist) of this handle's level-0 local arrays."""
+    v = [ctypes.c_int() for _ in range(5)]
+    _check(lib().bmg_local_rows(h, *[ctypes.byref(x) for x in v]), "bmg_local_rows")
+    return tuple(x.value for x in v)
 
 
 def bmg_destroy(h):

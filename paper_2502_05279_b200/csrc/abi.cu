@@ -12,6 +12,7 @@
 
 #include "bmg.h"
 #include "bmg_internal.cuh"
+#include "dist.cuh"
 #include "fused.cuh"
 
 using namespace bmg;
@@ -52,6 +53,10 @@ struct Level {
         A.S = pl[2];
         A.SW = pl[3];
         A.NW = pl[4];
+        A.ylo = 1;
+        A.yhi = ny + 1;
+        A.roff = 0;
+        A.nrows = ny + 2;
         return A;
     }
 };
@@ -74,11 +79,17 @@ struct bmg_solver {
     std::map<std::pair<const void *, const void *>, cudaGraphExec_t> graphs;
     int kernels_per_cycle = 0;
     FusedPlan fplan;
+    DistSolver *dist = nullptr;  // row-slab distributed solver (bmg_setup_dist)
+    bmg_solver_t dist_inner = nullptr;  // its replicated coarse solver (owned by dist)
+    long long dist_rows_total = 0;      // doubles of a level-0 rhs/x array of this handle
+    int dist_local_ranks = 1;
 
     CIv civ(int l) const
     {
         CIv v;
         v.pitch = lv[l + 1].pitch;
+        v.roff = 0;
+        v.nrows = lv[l + 1].ny + 2;
         for (int k = 0; k < 8; k++)
             v.w[k] = lv[l].ci[k];
         return v;
@@ -134,6 +145,13 @@ bmg_status_t bmg_destroy(bmg_solver_t h)
 {
     if (!h)
         return BMG_OK;
+    if (h->dist) {
+        dist_destroy(h->dist);
+        for (void *p : h->allocs)
+            cudaFree(p);
+        delete h;
+        return BMG_OK;
+    }
     cudaDeviceSynchronize();
     for (auto &kv : h->graphs)
         cudaGraphExecDestroy(kv.second);
@@ -209,15 +227,15 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
     {
         Level &v = h->lv[0];
         const double *src[5] = {st->plane[0], st->plane[1], st->plane[2], st->plane[3], st->plane[4]};
-        launch_ingest(v.nx, v.ny, v.kind, v.pitch, src, v.pl, h->d_err, s);
+        launch_ingest(v.nx, v.ny, v.kind, v.pitch, src, v.pl, h->d_err, s, 0, v.ny + 2);
         CK(cudaGetLastError());
     }
     // S1 + S2 per level
     for (int l = 0; l + 1 < h->L; l++) {
         Level &v = h->lv[l], &c = h->lv[l + 1];
-        launch_setup_interp(v.op(), v.ci, c.pitch, h->d_err, s);
+        launch_setup_interp(v.op(), v.ci, c.pitch, h->d_err, s, 1, c.ny + 1);
         CK(cudaGetLastError());
-        launch_setup_rap(v.op(), h->civ(l), c.nx, c.ny, c.pitch, c.pl, s);
+        launch_setup_rap(v.op(), h->civ(l), c.nx, c.ny, c.pitch, c.pl, s, 1, c.ny);
         CK(cudaGetLastError());
     }
     // S3 coarsest dense Cholesky
@@ -330,7 +348,7 @@ static void enqueue_up(bmg_solver *h, int l, bool fused, const double *f, const 
                        double *uout, cudaStream_t s, int *n)
 {
     Level &v = h->lv[l];
-    if (fused && fused_up(h->fplan, l, v.op(), h->civ(l), f, uin, ec, uout, s, n))
+    if (fused && fused_up(h->fplan, l, v.op(), h->civ(l), f, uin, ec, 0, h->lv[l + 1].ny + 2, uout, s, n))
         return;
     copy_level(h, l, uout, uin, s);
     launch_interp_add(v.op(), h->civ(l), ec, uout, s);
@@ -396,6 +414,11 @@ bmg_status_t bmg_vcycle(bmg_solver_t h, const double *rhs, double *x, int ncycle
 {
     if (!h || !rhs || !x || ncycles < 0)
         return fail(BMG_EINVAL, "bad arguments to bmg_vcycle");
+    if (h->dist) {
+        std::string err;
+        bmg_status_t rc = dist_vcycle(h->dist, rhs, x, ncycles, (cudaStream_t)cuda_stream, err);
+        return rc == BMG_OK ? rc : fail(rc, err);
+    }
     cudaGraphExec_t ex;
     TRY(get_graph(h, rhs, x, &ex));
     for (int k = 0; k < ncycles; k++)
@@ -405,8 +428,8 @@ bmg_status_t bmg_vcycle(bmg_solver_t h, const double *rhs, double *x, int ncycle
 
 bmg_status_t bmg_vcycle_host(bmg_solver_t h, const double *rhs_host, double *x_host, int ncycles, void *cuda_stream)
 {
-    if (!h || !rhs_host || !x_host || ncycles < 0)
-        return fail(BMG_EINVAL, "bad arguments to bmg_vcycle_host");
+    if (!h || !rhs_host || !x_host || ncycles < 0 || h->dist)
+        return fail(BMG_EINVAL, "bad arguments to bmg_vcycle_host (not for distributed handles)");
     Level &v = h->lv[0];
     size_t bytes = (size_t)(v.ny + 2) * v.pitch * sizeof(double);
     if (!h->stage_f) {
@@ -425,9 +448,14 @@ bmg_status_t bmg_vcycle_host(bmg_solver_t h, const double *rhs_host, double *x_h
 bmg_status_t bmg_residual_norm(bmg_solver_t h, const double *rhs, const double *x, double *r_out, double *norm_host,
                                void *cuda_stream)
 {
-    if (!h || !rhs || !x || !norm_host)
+    if (!h || !rhs || !x || !norm_host || (h->dist && r_out))
         return fail(BMG_EINVAL, "bad arguments to bmg_residual_norm");
     cudaStream_t s = (cudaStream_t)cuda_stream;
+    if (h->dist) {
+        std::string err;
+        bmg_status_t rc = dist_resid_norm(h->dist, rhs, x, norm_host, s, err);
+        return rc == BMG_OK ? rc : fail(rc, err);
+    }
     launch_resid_norm(h->lv[0].op(), rhs, x, r_out, h->partials, h->d_norm, s);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h->h_norm, h->d_norm, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -442,15 +470,32 @@ bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol,
     if (!h || !rhs || !x || maxiter < 0 || !(tol >= 0))
         return fail(BMG_EINVAL, "bad arguments to bmg_solve");
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    Level &v = h->lv[0];
     if (iters_out)
         *iters_out = 0;
-    launch_norm(v.op(), rhs, h->partials, h->d_norm, s);
-    CK(cudaMemcpyAsync(h->h_norm, h->d_norm, sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    double fn = h->h_norm[0];
+    double fn;
+    if (h->dist) {  // ||rhs|| = residual norm of x = 0
+        std::string err;
+        int row0, nrows;
+        dist_local_rows(h->dist, &row0, &nrows, nullptr, nullptr, nullptr);
+        if (!h->stage_x) {
+            TRY(dalloc(h, &h->stage_x, (size_t)h->dist_rows_total));
+            CK(cudaMemsetAsync(h->stage_x, 0, sizeof(double) * (size_t)h->dist_rows_total, s));
+        }
+        bmg_status_t rc = dist_resid_norm(h->dist, rhs, h->stage_x, &fn, s, err);
+        if (rc != BMG_OK)
+            return fail(rc, err);
+    } else {
+        Level &v = h->lv[0];
+        launch_norm(v.op(), rhs, h->partials, h->d_norm, s);
+        CK(cudaMemcpyAsync(h->h_norm, h->d_norm, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        fn = h->h_norm[0];
+    }
     if (fn == 0.0) {  // b = 0 -> x = 0 immediately
-        launch_zero_interior(v.op(), x, s);
+        if (h->dist)
+            CK(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)h->dist_rows_total, s));
+        else
+            launch_zero_interior(h->lv[0].op(), x, s);
         CK(cudaStreamSynchronize(s));
         if (hist_host)
             hist_host[0] = 0.0;
@@ -477,13 +522,20 @@ bmg_status_t bmg_num_levels(bmg_solver_t h, int *L)
 {
     if (!h || !L)
         return fail(BMG_EINVAL, "null argument");
+    if (h->dist) {
+        int K, Li;
+        dist_local_rows(h->dist, nullptr, nullptr, nullptr, nullptr, &K);
+        bmg_num_levels(h->dist_inner, &Li);
+        *L = K + Li;
+        return BMG_OK;
+    }
     *L = h->L;
     return BMG_OK;
 }
 
 bmg_status_t bmg_level_shape(bmg_solver_t h, int level, int *nx, int *ny, int *kind)
 {
-    if (!h || level < 0 || level >= h->L)
+    if (!h || h->dist || level < 0 || level >= h->L)
         return fail(BMG_EINVAL, "bad level");
     if (nx)
         *nx = h->lv[level].nx;
@@ -496,7 +548,7 @@ bmg_status_t bmg_level_shape(bmg_solver_t h, int level, int *nx, int *ny, int *k
 
 bmg_status_t bmg_level_pitch(bmg_solver_t h, int level, long long *pitch)
 {
-    if (!h || !pitch || level < 0 || level >= h->L)
+    if (!h || h->dist || !pitch || level < 0 || level >= h->L)
         return fail(BMG_EINVAL, "bad level");
     *pitch = h->lv[level].pitch;
     return BMG_OK;
@@ -506,6 +558,13 @@ bmg_status_t bmg_cycle_kernel_count(bmg_solver_t h, int *count)
 {
     if (!h || !count)
         return fail(BMG_EINVAL, "null argument");
+    if (h->dist) {  // two fused legs per slab level (per rank) + the inner cycle
+        int K, ni = 0;
+        dist_local_rows(h->dist, nullptr, nullptr, nullptr, nullptr, &K);
+        TRY(bmg_cycle_kernel_count(h->dist_inner, &ni));
+        *count = 2 * K * h->dist_local_ranks + ni;
+        return BMG_OK;
+    }
     if (h->kernels_per_cycle == 0) {  // count by a dry capture
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
@@ -520,7 +579,7 @@ bmg_status_t bmg_cycle_kernel_count(bmg_solver_t h, int *count)
 
 bmg_status_t bmg_export_level(bmg_solver_t h, int level, double *stencil_host, double *ci_host)
 {
-    if (!h || level < 0 || level >= h->L || !stencil_host)
+    if (!h || h->dist || level < 0 || level >= h->L || !stencil_host)
         return fail(BMG_EINVAL, "bad arguments to bmg_export_level");
     CK(cudaDeviceSynchronize());
     Level &v = h->lv[level];
@@ -545,7 +604,7 @@ bmg_status_t bmg_export_level(bmg_solver_t h, int level, double *stencil_host, d
 
 static bmg_status_t check_level(bmg_solver_t h, int level, bool need_coarse)
 {
-    if (!h || level < 0 || level >= h->L || (need_coarse && level + 1 >= h->L))
+    if (!h || h->dist || level < 0 || level >= h->L || (need_coarse && level + 1 >= h->L))
         return fail(BMG_EINVAL, "bad level");
     return BMG_OK;
 }
@@ -607,4 +666,61 @@ bmg_status_t bmg_correct_smooth(bmg_solver_t h, int level, const double *f, cons
     return BMG_OK;
 }
 
+bmg_status_t bmg_partition(int nx, int ny, int nranks, const bmg_params_t *params, int *ybounds, int *kdist)
+{
+    bmg_status_t rc = dist_partition(nx, ny, nranks, params, ybounds, kdist);
+    return rc == BMG_OK ? rc : fail(rc, "grid too small for this many slabs");
+}
+
+bmg_status_t bmg_setup_dist(const bmg_stencil_t *st, const bmg_comm_t *comm, const bmg_params_t *params,
+                            void *cuda_stream, bmg_solver_t *out)
+{
+    if (!st || !comm || !out)
+        return fail(BMG_EINVAL, "null argument to bmg_setup_dist");
+    *out = nullptr;
+    if (st->nx < 1 || st->ny < 1 || (st->kind != 5 && st->kind != 9) || st->pitch < (long long)st->nx + 2 ||
+        comm->nranks < 1 || (!comm->loopback && (comm->rank < 0 || comm->rank >= comm->nranks)))
+        return fail(BMG_EINVAL, "bad sizes or communicator");
+    std::string err;
+    DistSolver *d = nullptr;
+    bmg_status_t rc = dist_setup(st, comm, params, (cudaStream_t)cuda_stream, &d, err);
+    if (rc != BMG_OK)
+        return fail(rc, err);
+    bmg_solver *h = new bmg_solver();
+    if (params)
+        h->prm = *params;
+    else
+        bmg_params_default(&h->prm);
+    h->dist = d;
+    h->dist_inner = dist_inner_solver(d);
+    int row0, nrows;
+    dist_local_rows(d, &row0, &nrows, nullptr, nullptr, nullptr);
+    h->dist_rows_total = comm->loopback ? (long long)(st->ny + 2) * st->pitch : (long long)nrows * st->pitch;
+    h->dist_local_ranks = comm->loopback ? comm->nranks : 1;
+    *out = h;
+    return BMG_OK;
+}
+
+bmg_status_t bmg_local_rows(bmg_solver_t h, int *row0, int *nrows, int *ylo, int *yhi, int *kdist)
+{
+    if (!h)
+        return fail(BMG_EINVAL, "null handle");
+    if (h->dist) {
+        dist_local_rows(h->dist, row0, nrows, ylo, yhi, kdist);
+        return BMG_OK;
+    }
+    if (row0)
+        *row0 = 0;
+    if (nrows)
+        *nrows = h->lv[0].ny + 2;
+    if (ylo)
+        *ylo = 1;
+    if (yhi)
+        *yhi = h->lv[0].ny + 1;
+    if (kdist)
+        *kdist = 0;
+    return BMG_OK;
+}
+
 }  // extern "C"
+

@@ -20,16 +20,25 @@ enum { CI_LNE = 0, CI_LA = 1, CI_LNW = 2, CI_LR = 3, CI_LL = 4, CI_LSE = 5, CI_L
 enum { ERR_DIAG = 1, ERR_DEN = 2, ERR_PIVOT = 4 };
 
 // One level's operator (read-only view).  SW/NW are nullptr on 5-point levels.
+// Pointers are GLOBAL-row indexed: element (i, j) is at p[j*pitch + i] for the
+// global row j.  A single-GPU level stores all rows (roff = 0, nrows = ny+2);
+// a slab of a row-partitioned level (dist.cu) stores global rows
+// [roff, roff+nrows) and owns interior rows [ylo, yhi) -- its pointers are the
+// allocation shifted by -roff*pitch, so kernels index identically.
 struct Op {
-    int nx, ny, kind;
+    int nx, ny, kind;  // GLOBAL interior sizes
     long long pitch;
     const double *O, *W, *S, *SW, *NW;
+    int ylo, yhi;      // owned interior rows
+    int roff, nrows;   // stored rows
 };
 
-// Interpolation weights between a level (fine) and the next (coarse).
+// Interpolation weights between a level (fine) and the next (coarse); same
+// row convention on the coarse grid.
 struct CIv {
     long long pitch;  // coarse pitch
     const double *w[8];
+    int roff, nrows;  // stored coarse rows
 };
 
 // Full 9-entry row of the operator at an interior point, reconstructed from
@@ -59,10 +68,11 @@ __device__ __forceinline__ Row9 load_row9(const Op &A, long long p)
 
 // ---- launchers (kernels.cu) ----
 void launch_ingest(int nx, int ny, int kind, long long pitch, const double *const src[5], double *const dst[5],
-                   int *err, cudaStream_t s);
-void launch_setup_interp(const Op &A, double *const ci[8], long long cpitch, int *err, cudaStream_t s);
+                   int *err, cudaStream_t s, int j0, int j1);
+void launch_setup_interp(const Op &A, double *const ci[8], long long cpitch, int *err, cudaStream_t s, int J0,
+                         int J1);
 void launch_setup_rap(const Op &A, const CIv &ci, int ncx, int ncy, long long cpitch, double *const dst[5],
-                      cudaStream_t s);
+                      cudaStream_t s, int J0, int J1);
 void launch_assemble_dense(const Op &A, double *M, cudaStream_t s);
 void launch_chol_factor(int n, double *M, int *err, cudaStream_t s);
 void launch_coarse_solve(const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s);

@@ -49,7 +49,8 @@ bmg_status_t fused_plan_level(FusedPlan &fp, int l, int nx, int ny, long long pi
 bool fused_down(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const double *f, const double *uin,
                 double *uout, double *fc, double *uc, cudaStream_t s, int *nlaunch);
 // Up leg: uout = relax^nu2(uin + P ec).
+// ec: coarse correction, global-row indexed, stored rows [eroff, eroff+enrows).
 bool fused_up(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const double *f, const double *uin,
-              const double *ec, double *uout, cudaStream_t s, int *nlaunch);
+              const double *ec, int eroff, int enrows, double *uout, cudaStream_t s, int *nlaunch);
 
 }  // namespace bmg

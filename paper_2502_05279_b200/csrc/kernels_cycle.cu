@@ -219,7 +219,7 @@ __global__ void k_norm_partial(Op A, const double *__restrict__ f, const double 
 {
     double acc = 0.0;
     long long P = A.pitch;
-    for (int j = 1 + blockIdx.x; j <= A.ny; j += gridDim.x) {
+    for (int j = A.ylo + blockIdx.x; j < A.yhi; j += gridDim.x) {  // owned rows
         for (int i = 1 + threadIdx.x; i <= A.nx; i += blockDim.x) {
             long long p = j * P + i;
             double v;

@@ -136,6 +136,7 @@ struct FArgs {
     const double *f, *uin, *ec;
     double *uout, *fc, *uc;
     int nstrips, chunk, ncx, ncy;
+    int eroff;  // stored-row offset of the coarse correction e (up leg)
 };
 
 // TMA descriptors of one launch (kernel parameter, __grid_constant__):
@@ -331,10 +332,10 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT)
     const long long P = a.A.pitch, CP = a.ci.pitch;
     const int strip = blockIdx.x % a.nstrips, chunk = blockIdx.x / a.nstrips;
     const int x0 = strip * TX, xl = x0 - H;
-    const int ya = max(1, chunk * a.chunk), yb = min(ny + 1, (chunk + 1) * a.chunk);
+    const int ya = a.A.ylo + chunk * a.chunk, yb = min(a.A.yhi, ya + a.chunk);
     if (ya >= yb)
         return;
-    const int lo = max(ya - NS - 2, 0), hi = min(yb + NS + 1, ny + 1);
+    const int lo = max(ya - NS - 2, a.A.roff), hi = min(yb + NS + 1, a.A.roff + a.A.nrows - 1);
     const int cs = max(xl, 0), ce = min(xl + WD, (int)P);
     const uint32_t rowbytes = (uint32_t)(ce - cs) * 8u;
     const int soff = cs - xl;
@@ -365,9 +366,9 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT)
         if (BMG_EXP & 32)
             return;
         double *d = smS + slot * (NA * WD);
-        tma_2d(d + A_U * WD, &tmaps.u, xl, row, b);
-        tma_2d(d + A_F * WD, &tmaps.f, xl, row, b);
-        tma_3d(d + A_O * WD, &tmaps.a, xl, row, 0, b);
+        tma_2d(d + A_U * WD, &tmaps.u, xl, row - a.A.roff, b);
+        tma_2d(d + A_F * WD, &tmaps.f, xl, row - a.A.roff, b);
+        tma_3d(d + A_O * WD, &tmaps.a, xl, row - a.A.roff, 0, b);
     };
     auto issue_coarse = [&](int t) {
         while (Knext <= Kend) {
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT)
             const int slot = (Knext - Jlo) & 3;
             uint64_t *b = &bar[SD + slot];
             mbar_arrive_tx(b, (uint32_t)(8 * WC * 8));
-            tma_3d(sC + slot * 8 * WC, &tmaps.c, cxl, Knext, 0, b);
+            tma_3d(sC + slot * 8 * WC, &tmaps.c, cxl, Knext - a.ci.roff, 0, b);
             Knext++;
         }
     };
@@ -555,10 +556,10 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT)
     const long long P = a.A.pitch, CP = a.ci.pitch;
     const int strip = blockIdx.x % a.nstrips, chunk = blockIdx.x / a.nstrips;
     const int x0 = strip * TX, xl = x0 - H;
-    const int ya = max(1, chunk * a.chunk), yb = min(ny + 1, (chunk + 1) * a.chunk);
+    const int ya = a.A.ylo + chunk * a.chunk, yb = min(a.A.yhi, ya + a.chunk);
     if (ya >= yb)
         return;
-    const int lo = max(ya - NS, 0), hi = min(yb + NS - 1, ny + 1);
+    const int lo = max(ya - NS, a.A.roff), hi = min(yb + NS - 1, a.A.roff + a.A.nrows - 1);
     const int lo1 = max(lo, 1), hi1 = min(hi, ny);  // corrected rows
     const int cs = max(xl, 0), ce = min(xl + WD, (int)P);
     const uint32_t rowbytes = (uint32_t)(ce - cs) * 8u;
@@ -587,9 +588,9 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT)
         if (BMG_EXP & 32)
             return;
         double *d = smS + slot * (NA * WD);
-        tma_2d(d + A_U * WD, &tmaps.u, xl, row, b);
-        tma_2d(d + A_F * WD, &tmaps.f, xl, row, b);
-        tma_3d(d + A_O * WD, &tmaps.a, xl, row, 0, b);
+        tma_2d(d + A_U * WD, &tmaps.u, xl, row - a.A.roff, b);
+        tma_2d(d + A_F * WD, &tmaps.f, xl, row - a.A.roff, b);
+        tma_3d(d + A_O * WD, &tmaps.a, xl, row - a.A.roff, 0, b);
     };
     auto issue_coarse = [&](int t) {
         while (Knext <= Khi) {
@@ -599,8 +600,8 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT)
             const int slot = (Knext - Klo) & 3;
             uint64_t *b = &bar[SD + slot];
             mbar_arrive_tx(b, (uint32_t)(9 * WC * 8));
-            tma_2d(sE + slot * WC, &tmaps.e, cxl, Knext, b);
-            tma_3d(sC + slot * 8 * WC, &tmaps.c, cxl, Knext, 0, b);
+            tma_2d(sE + slot * WC, &tmaps.e, cxl, Knext - a.eroff, b);
+            tma_3d(sC + slot * 8 * WC, &tmaps.c, cxl, Knext - a.ci.roff, 0, b);
             Knext++;
         }
     };
@@ -923,25 +924,25 @@ static bool make_map(CUtensorMap *m, const double *base, long long width, long l
 
 // Maps of one fused launch: the planes and the weights must be contiguous blocks.
 static bool make_maps(TMaps &tm, const FusedGeom &g, const Op &A, const CIv &ci, const double *uin, const double *f,
-                      const double *ec)
+                      const double *ec, int eroff, int enrows)
 {
-    const long long np = (A.ny + 2) * A.pitch;
+    const long long np = (long long)A.nrows * A.pitch;  // plane stride of the (slab) block
     const int npl = A.kind == 9 ? 5 : 3;
     const double *pl[5] = {A.O, A.W, A.S, A.SW, A.NW};
     for (int k = 1; k < npl; k++)
         if (pl[k] != A.O + k * np)
             return false;
-    const int ncx = A.nx / 2, ncy = A.ny / 2;
-    const long long npc = (ncy + 2) * ci.pitch;
+    const int ncx = A.nx / 2;
+    const long long npc = (long long)ci.nrows * ci.pitch;
     for (int k = 1; k < 8; k++)
         if (ci.w[k] != ci.w[0] + k * npc)
             return false;
-    bool ok = make_map(&tm.u, uin, A.nx + 2, A.ny + 2, A.pitch, 0, 0, g.WD) &&
-              make_map(&tm.f, f, A.nx + 2, A.ny + 2, A.pitch, 0, 0, g.WD) &&
-              make_map(&tm.a, A.O, A.nx + 2, A.ny + 2, A.pitch, np, npl, g.WD) &&
-              make_map(&tm.c, ci.w[0], ncx + 2, ncy + 2, ci.pitch, npc, 8, g.WC);
+    bool ok = make_map(&tm.u, uin + A.roff * A.pitch, A.nx + 2, A.nrows, A.pitch, 0, 0, g.WD) &&
+              make_map(&tm.f, f + A.roff * A.pitch, A.nx + 2, A.nrows, A.pitch, 0, 0, g.WD) &&
+              make_map(&tm.a, A.O + A.roff * A.pitch, A.nx + 2, A.nrows, A.pitch, np, npl, g.WD) &&
+              make_map(&tm.c, ci.w[0] + ci.roff * ci.pitch, ncx + 2, ci.nrows, ci.pitch, npc, 8, g.WC);
     if (ok && ec)
-        ok = make_map(&tm.e, ec, ncx + 2, ncy + 2, ci.pitch, 0, 0, g.WC);
+        ok = make_map(&tm.e, ec + (long long)eroff * ci.pitch, ncx + 2, enrows, ci.pitch, 0, 0, g.WC);
     else
         tm.e = tm.c;
     return ok;
@@ -972,6 +973,7 @@ static FArgs make_args(const FusedGeom &g, const Op &A, const CIv &ci)
     a.chunk = g.chunk;
     a.ncx = A.nx / 2;
     a.ncy = A.ny / 2;
+    a.eroff = 0;
     return a;
 }
 
@@ -988,7 +990,7 @@ bool fused_down(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const do
     a.fc = fc;
     a.uc = uc;
     TMaps tm;
-    if (!make_maps(tm, g, A, ci, uin, f, nullptr))
+    if (!make_maps(tm, g, A, ci, uin, f, nullptr, 0, 0))
         return false;
     if (A.kind == 5)
         g.NS == 2 ? launch_down<5, 2>(g, a, tm, s) : launch_down<5, 4>(g, a, tm, s);
@@ -1000,7 +1002,7 @@ bool fused_down(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const do
 }
 
 bool fused_up(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const double *f, const double *uin,
-              const double *ec, double *uout, cudaStream_t s, int *nlaunch)
+              const double *ec, int eroff, int enrows, double *uout, cudaStream_t s, int *nlaunch)
 {
     if (l >= 32 || !fp.lv[l].up || !ptrs_ok(A, ci, {f, uin, uout, ec}))
         return false;
@@ -1011,7 +1013,8 @@ bool fused_up(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const doub
     a.ec = ec;
     a.uout = uout;
     TMaps tm;
-    if (!make_maps(tm, g, A, ci, uin, f, ec))
+    a.eroff = eroff;
+    if (!make_maps(tm, g, A, ci, uin, f, ec, eroff, enrows))
         return false;
     if (A.kind == 5)
         g.NS == 2 ? launch_up<5, 2>(g, a, tm, s) : launch_up<5, 4>(g, a, tm, s);

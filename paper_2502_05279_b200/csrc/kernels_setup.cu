@@ -16,10 +16,10 @@ namespace bmg {
 __global__ void k_ingest(int nx, int ny, int kind, long long pitch, const double *__restrict__ sO,
                          const double *__restrict__ sW, const double *__restrict__ sS,
                          const double *__restrict__ sSW, const double *__restrict__ sNW, double *dO, double *dW,
-                         double *dS, double *dSW, double *dNW, int *err)
+                         double *dS, double *dSW, double *dNW, int *err, int j0)
 {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    int j = blockIdx.y;
+    int j = blockIdx.y + j0;  // global row
     if (i >= pitch)
         return;
     long long p = j * pitch + i;
@@ -46,11 +46,13 @@ __global__ void k_ingest(int nx, int ny, int kind, long long pitch, const double
 }
 
 void launch_ingest(int nx, int ny, int kind, long long pitch, const double *const src[5], double *const dst[5],
-                   int *err, cudaStream_t st)
+                   int *err, cudaStream_t st, int j0, int j1)
 {
-    dim3 b(256), g((unsigned)((pitch + 255) / 256), ny + 2);
+    if (j1 <= j0)
+        return;
+    dim3 b(256), g((unsigned)((pitch + 255) / 256), j1 - j0);
     k_ingest<<<g, b, 0, st>>>(nx, ny, kind, pitch, src[0], src[1], src[2], src[3], src[4], dst[0], dst[1], dst[2],
-                              dst[3], dst[4], err);
+                              dst[3], dst[4], err, j0);
 }
 
 // ---------------------------------------------------------------- S1 interpolation
@@ -75,12 +77,12 @@ __device__ __forceinline__ Collapsed collapse(const Row9 &a)
 }
 
 // Phase 1: X points (2I-1,2J) -> LL, LR and Y points (2I,2J-1) -> LB, LA, all stored at (I,J).
-__global__ void k_interp_xy(Op A, CIv ci, double *cLL, double *cLR, double *cLB, double *cLA, int ncx, int ncy,
-                            int *err)
+__global__ void k_interp_xy(Op A, CIv ci, double *cLL, double *cLR, double *cLB, double *cLA, int ncx, int J0,
+                            int J1, int *err)
 {
     int I = blockIdx.x * blockDim.x + threadIdx.x + 1;
-    int J = blockIdx.y * blockDim.y + threadIdx.y + 1;
-    if (I > ncx + 1 || J > ncy + 1)
+    int J = blockIdx.y * blockDim.y + threadIdx.y + J0;
+    if (I > ncx + 1 || J > J1)
         return;
     long long q = J * ci.pitch + I;
     // X point
@@ -115,12 +117,12 @@ __global__ void k_interp_xy(Op A, CIv ci, double *cLL, double *cLR, double *cLB,
 
 // Phase 2: Z points (2I-1,2J-1) -> LNE, LNW, LSE, LSW at (I,J), from the
 // neighbouring edge weights X(I,J) north, X(I,J-1) south, Y(I,J) east, Y(I-1,J) west.
-__global__ void k_interp_z(Op A, CIv ci, double *cLNE, double *cLNW, double *cLSE, double *cLSW, int ncx, int ncy,
-                           int *err)
+__global__ void k_interp_z(Op A, CIv ci, double *cLNE, double *cLNW, double *cLSE, double *cLSW, int ncx, int J0,
+                           int J1, int *err)
 {
     int I = blockIdx.x * blockDim.x + threadIdx.x + 1;
-    int J = blockIdx.y * blockDim.y + threadIdx.y + 1;
-    if (I > ncx + 1 || J > ncy + 1)
+    int J = blockIdx.y * blockDim.y + threadIdx.y + J0;
+    if (I > ncx + 1 || J > J1)
         return;
     int i = 2 * I - 1, j = 2 * J - 1;
     if (i > A.nx || j > A.ny)
@@ -141,16 +143,21 @@ __global__ void k_interp_z(Op A, CIv ci, double *cLNE, double *cLNW, double *cLS
     cLSW[q] = __dadd_rn(__dadd_rn(-a.sw, -__dmul_rn(a.s, LLs)), -__dmul_rn(a.w, LBw)) / den;
 }
 
-void launch_setup_interp(const Op &A, double *const ci[8], long long cpitch, int *err, cudaStream_t s)
+// Coarse rows [J0, J1] (inclusive; single GPU: [1, ncy+1]).  The Z phase reads
+// edge weights of row J-1, so a slab computes phase 1 from one row lower.
+void launch_setup_interp(const Op &A, double *const ci[8], long long cpitch, int *err, cudaStream_t s, int J0, int J1)
 {
-    int ncx = A.nx / 2, ncy = A.ny / 2;
+    int ncx = A.nx / 2;
     CIv v;
     v.pitch = cpitch;
+    v.roff = 0;
+    v.nrows = 0;
     for (int k = 0; k < 8; k++)
         v.w[k] = ci[k];
-    dim3 b(32, 8), g((ncx + 1 + 31) / 32, (ncy + 1 + 7) / 8);
-    k_interp_xy<<<g, b, 0, s>>>(A, v, ci[CI_LL], ci[CI_LR], ci[CI_LB], ci[CI_LA], ncx, ncy, err);
-    k_interp_z<<<g, b, 0, s>>>(A, v, ci[CI_LNE], ci[CI_LNW], ci[CI_LSE], ci[CI_LSW], ncx, ncy, err);
+    dim3 b(32, 8);
+    dim3 g1((ncx + 1 + 31) / 32, (J1 - J0 + 1 + 7) / 8);
+    k_interp_xy<<<g1, b, 0, s>>>(A, v, ci[CI_LL], ci[CI_LR], ci[CI_LB], ci[CI_LA], ncx, J0, J1, err);
+    k_interp_z<<<g1, b, 0, s>>>(A, v, ci[CI_LNE], ci[CI_LNW], ci[CI_LSE], ci[CI_LSW], ncx, J0, J1, err);
 }
 
 // ---------------------------------------------------------------- S2 Galerkin RAP
@@ -186,11 +193,11 @@ __device__ __forceinline__ double pweight(const CIv &ci, int gx, int gy, int Dx,
 //   A_c(C,D) = sum_f P(f,C) sum_g A(f,g) P(g,D)   for D in {C, C-(1,0), C-(0,1), C-(1,1), C+(-1,1)}
 // over interior fine f in C's 3x3 window and interior g in f's 3x3 window.
 __global__ void k_rap(Op A, CIv ci, int ncx, int ncy, long long cpitch, double *cO, double *cW, double *cS,
-                      double *cSW, double *cNW)
+                      double *cSW, double *cNW, int J0, int J1)
 {
     int I = blockIdx.x * blockDim.x + threadIdx.x + 1;
-    int J = blockIdx.y * blockDim.y + threadIdx.y + 1;
-    if (I > ncx || J > ncy)
+    int J = blockIdx.y * blockDim.y + threadIdx.y + J0;
+    if (I > ncx || J > J1)
         return;
     const int tx[5] = {0, -1, 0, -1, -1};
     const int ty[5] = {0, 0, -1, -1, 1};
@@ -230,11 +237,14 @@ __global__ void k_rap(Op A, CIv ci, int ncx, int ncy, long long cpitch, double *
     cNW[q] = acc[4];
 }
 
+// Coarse rows [J0, J1] (inclusive; single GPU: [1, ncy]).
 void launch_setup_rap(const Op &A, const CIv &ci, int ncx, int ncy, long long cpitch, double *const dst[5],
-                      cudaStream_t s)
+                      cudaStream_t s, int J0, int J1)
 {
-    dim3 b(32, 4), g((ncx + 31) / 32, (ncy + 3) / 4);
-    k_rap<<<g, b, 0, s>>>(A, ci, ncx, ncy, cpitch, dst[0], dst[1], dst[2], dst[3], dst[4]);
+    if (J1 < J0)
+        return;
+    dim3 b(32, 4), g((ncx + 31) / 32, (J1 - J0 + 1 + 3) / 4);
+    k_rap<<<g, b, 0, s>>>(A, ci, ncx, ncy, cpitch, dst[0], dst[1], dst[2], dst[3], dst[4], J0, J1);
 }
 
 // ---------------------------------------------------------------- S3 coarsest factor
