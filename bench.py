@@ -25,6 +25,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "V(2,1) cycles/s and Munknowns/s at 8193^2; HBM GB/s vs peak; 1/2/4/8 GPU"
+CONFIG_KIND = {"aniso": 9}
 
 CONFIGS = {
     # name: (workload, nx, ny, description)
@@ -193,13 +194,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="one kernel per method step (debug/comparison)")
+    ap.add_argument("--dist", action="store_true", help="use the row-slab NCCL solver even on one GPU")
     ap.add_argument("--e2e-steps", type=int, default=5)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args, args.config)
 
-    import numpy as np
     import torch
 
     from paper_2502_05279_b200 import bmg, problems as P
@@ -218,15 +219,30 @@ def main():
     st = P.workload(wl, nx, ny)
     prm = bmg.bmg_params_default()
     prm.fused = 0 if args.unfused else 1
-    solver = bmg.Solver(st, prm)
+    distributed = world > 1 or args.dist
+    if distributed:
+        # strong scaling (BASELINE config 4): one global problem in row slabs, NCCL ghost rows
+        from paper_2502_05279_b200 import dist as D
+
+        comm = D.nccl_comm(world, rank)
+        solver = D.DistSolver(st, world, rank, comm, prm)
+        f = solver.local(P.rhs_const(nx, ny))
+        x = solver.local()
+        parallelism = (f"{world} row slabs (NCCL ghost-row exchange, coarse levels all-gathered below "
+                       f"level {solver.kdist})")
+        scaling = "strong"
+    else:
+        solver = bmg.Solver(st, prm)
+        f = solver.grid(P.rhs_const(nx, ny))
+        x = solver.grid()
+        parallelism = "single GPU"
+        scaling = "weak"
     del st
-    f = solver.grid(P.rhs_const(nx, ny))
-    x = solver.grid()
-    L = solver.L
-    kind = bmg.bmg_level_shape(solver.h, 0)[2]
+    L = bmg.bmg_num_levels(solver.h)
+    kind = CONFIG_KIND.get(wl, 5)
     stream = torch.cuda.current_stream()
 
-    # warm-up (untimed): builds and caches the CUDA graph
+    # warm-up (untimed): builds and caches the CUDA graph(s)
     solver.vcycle(f, x, args.warmup)
     torch.cuda.synchronize()
     kpc = bmg.bmg_cycle_kernel_count(solver.h)
@@ -253,29 +269,44 @@ def main():
         ms = float(t.item())
     clocks.stop()
     ms_per_step = ms / args.steps
-    cycles_per_s = world * args.steps / (ms / 1e3)
+    # whole-job throughput: V-cycles of the global problem per second (strong scaling)
+    cycles_per_s = args.steps / (ms / 1e3)
 
-    # roofline: the dominant kernel group = level-0 down leg (smooth+residual+restrict),
-    # launched alone through the ABI step call, CUDA events on its stream.
     peak, peak_src = measured_peaks()
-    rl = roofline(solver, bmg, torch, f, x, nx, ny, kind, peak, peak_src, ms_per_step, args)
+    rl = None
+    if not distributed:
+        # roofline: the dominant kernel = level-0 down leg, launched alone through the ABI
+        rl = roofline(solver, bmg, torch, f, x, nx, ny, kind, peak, peak_src, ms_per_step, args)
 
-    # convergence sanity of the timed run (residual keeps falling / at rounding floor)
+    # convergence sanity of the timed run (residual at the rounding floor after many cycles)
     rnorm = solver.residual_norm(f, x)
-    fnorm = float(torch.linalg.vector_norm(f))
+    fnorm = P.h_of(max(nx, ny)) ** 2 * (float(nx) * ny) ** 0.5
 
-    # e2e: same metric through the public API with HOST buffers (pinned), copies inside the timed region
+    # e2e: the same metric through the public API with HOST buffers (pinned): per step
+    # H2D of rhs and x, one V(2,1) cycle, D2H of x; host wall clock, max over ranks
     e2e = None
     if args.e2e_steps > 0:
         fh = f.cpu().pin_memory()
         xh = torch.zeros_like(fh).pin_memory()
-        bmg.bmg_vcycle_host(solver.h, fh, xh, 1)
+
+        def e2e_step():
+            if distributed:
+                fd, xd = f, x
+                fd.copy_(fh, non_blocking=True)
+                xd.copy_(xh, non_blocking=True)
+                solver.vcycle(fd, xd, 1)
+                xh.copy_(xd, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+            else:
+                bmg.bmg_vcycle_host(solver.h, fh, xh, 1)
+
+        e2e_step()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            bmg.bmg_vcycle_host(solver.h, fh, xh, 1)
+            e2e_step()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if dist:
@@ -283,9 +314,10 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         nbytes = fh.numel() * 8
-        e2e = {"value": world * args.e2e_steps / dt, "unit": "cycles/s", "h2d_bytes_per_step": 2 * nbytes,
-               "d2h_bytes_per_step": nbytes,
-               "note": "bmg_vcycle_host: H2D rhs+x (pinned), 1 V(2,1) cycle, D2H x, per step; host wall clock"}
+        e2e = {"value": args.e2e_steps / dt, "unit": "cycles/s", "h2d_bytes_per_step": 2 * nbytes * world,
+               "d2h_bytes_per_step": nbytes * world,
+               "note": ("per step: H2D rhs+x (pinned), 1 V(2,1) cycle, D2H x (bmg_vcycle_host on 1 GPU; "
+                        "torch copies + bmg_vcycle on the rank-local slabs otherwise); host wall clock")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -305,18 +337,18 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling,
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": desc, "nx": nx, "ny": ny, "levels": L, "cycle": "V(2,1)",
-                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (one problem per GPU)",
+                   "parallelism": parallelism,
                    "l2": "inputs > L2 (level-0 arrays 537 MB each); no flush needed",
                    "fused": bool(prm.fused)},
         "munknowns_per_s": cycles_per_s * nx * ny / 1e6,
         "model_B_GBps": B / (ms_per_step / 1e3) / 1e9,
-        "model_B_frac": B / (ms_per_step / 1e3) / 1e9 / peak,
-        "model_A_frac": A / (ms_per_step / 1e3) / 1e9 / peak,
+        "model_B_frac": B / (ms_per_step / 1e3) / 1e9 / (peak * world),
+        "model_A_frac": A / (ms_per_step / 1e3) / 1e9 / (peak * world),
         "final_rel_residual": rnorm / fnorm,
         "gpu_launches": kpc * args.steps,
         "kernels_per_cycle": kpc,

@@ -93,3 +93,30 @@ def test_den_nonpositive_rejected_like_oracle(orc):
     with pytest.raises(bmg.BmgError) as ei:
         bmg.Solver(st)
     assert ei.value.status == bmg.BMG_EINVAL
+
+
+def test_nccl_mode_single_rank():
+    """The NCCL transport path (dlopen'ed libnccl, rank-local arrays, grouped
+    send/recv + all-gather code) with a 1-rank communicator: bitwise equal to
+    the single-GPU solver; the partition-derived local layout matches the ABI."""
+    from paper_2502_05279_b200 import dist as D
+
+    n = 511
+    st = P.workload("checker", n, n)
+    prm = bmg.bmg_params_default()
+    single = bmg.Solver(st, prm)
+    comm = D.nccl_comm(1, 0)
+    ds = D.DistSolver(st, 1, 0, comm, prm, pitch=single.pitch)
+    assert bmg.bmg_local_rows(ds.h) == D.local_layout(n, n, 1, 0, prm)
+    f = P.field_uniform(n, n, seed=61)
+    x0 = P.field_uniform(n, n, seed=62)
+    xs = single.grid(x0)
+    single.vcycle(single.grid(f), xs, 2)
+    fl, xl = ds.local(f), ds.local(x0)
+    ds.vcycle(fl, xl, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(xs[1:-1], xl[1:-1])
+    assert abs(ds.residual_norm(fl, xl) - single.residual_norm(single.grid(f), xs)) <= 1e-12 * single.residual_norm(
+        single.grid(f), xs)
+    ds.close()
+    single.close()
