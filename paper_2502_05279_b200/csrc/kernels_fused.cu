@@ -9,13 +9,15 @@
 // Up leg in ONE pass:
 //   split of row t; interpolation + correction (c7) on row t-1; stage k on
 //   row t-1-2k; store of row t-2NS-2.
-// Stages 2 rows apart never touch each other's rows within a row step, so one
-// __syncthreads per step orders everything (two on 9-point levels, whose row
-// stage is two colour phases: even columns, then odd columns).
+// Each task runs in its own warp group; groups are decoupled: a group waits only
+// on the step-completion mbarriers of the groups it reads from (or whose ring
+// slots it overwrites), so a slow task delays its consumers, not the whole CTA.
+// A 9-point row stage is two colour phases (even columns, then odd columns)
+// ordered by a barrier over its group only.
 //
-// Memory path: rows of u_in, f and the operator planes arrive by 1-D TMA bulk
-// copies (cp.async.bulk.shared::cluster.global + mbarrier complete_tx) into a
-// staging ring D rows ahead, in natural order.  A split task de-interleaves
+// Memory path: rows of u_in, f and the operator planes arrive by tensor TMA
+// (one 2-D box for u and f each, one 3-D box for the plane block; mbarrier
+// complete_tx) into a staging ring D rows ahead, in natural order.  A split task de-interleaves
 // each row into [even columns | odd columns] halves of the main ring, so every
 // compute access -- a colour pass touches every other column -- is a run of
 // consecutive doubles across a warp (no shared-memory bank conflicts).  Coarse
@@ -65,12 +67,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity)
         : "memory");
 }
 
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *b)
+__device__ __forceinline__ void mbar_arrive(uint64_t *b)
 {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(b))
-                 : "memory");
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+// barrier among the `n` threads (whole warps) of one task group
+__device__ __forceinline__ void group_sync(int id, int n)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 // Tiled tensor TMA: one box (out-of-bounds elements zero-filled) into smem.
@@ -92,15 +97,12 @@ __device__ __forceinline__ void tma_3d(void *dst, const CUtensorMap *m, int x, i
         : "memory");
 }
 
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
 // ------------------------------------------------------------------ configuration
-#ifndef BMG_EXP
-#define BMG_EXP 0  // timing-study mask: skip 1 stages, 2 residual, 4 restriction, 8 split, 16 store, 32 TMA
-#endif
 constexpr int DC = 4;  // coarse-row prefetch distance (row steps); < 6 for safe ring reuse
 constexpr int CH = 4;  // coarse halo columns on each side of a strip
+constexpr int NSLOT = 32;  // slots of each task group's step-completion ring
 
 // streamed arrays: index into the shared-memory array blocks
 enum { A_U = 0, A_F = 1, A_O = 2, A_W = 3, A_S = 4, A_SW = 5, A_NW = 6 };
@@ -125,9 +127,31 @@ struct Cfg {
     static constexpr int NT = NTW + 32;                        // + one TMA producer warp
     static constexpr size_t SMEM_DBL =
         (size_t)NA * (AM + AS) + (UP ? 4 * (size_t)WC : 4 * (size_t)WD) + 32 * (size_t)WC;
-    static constexpr size_t SMEM = SMEM_DBL * 8 + (SD + 4) * 8;
+    static constexpr size_t SMEM = SMEM_DBL * 8 + (SD + 4 + (size_t)NG * NSLOT) * 8;
     static_assert(TX % 4 == 0 && TX > 0, "strip width");
     static_assert(NPG % 32 == 0, "task groups must be whole warps");
+};
+
+// Step-completion rings: group g arrives (one arrival per warp) on slot t mod
+// NSLOT after finishing row step t; a consumer waits on the producer's step.
+// Every dependency cycle of the pipeline spans fewer than NSLOT steps, so no
+// warp is ever NSLOT steps ahead of a waiter or of the slowest warp of its group.
+struct DoneRing {
+    uint64_t *b;
+    int lo;
+    __device__ __forceinline__ void arrive(int g, int t) const
+    {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0)
+            mbar_arrive(&b[g * NSLOT + ((t - lo) & (NSLOT - 1))]);
+    }
+    __device__ __forceinline__ void wait(int g, int t) const
+    {
+        if (t < lo)
+            return;
+        const int s = t - lo;
+        mbar_wait(&b[g * NSLOT + (s & (NSLOT - 1))], (s / NSLOT) & 1);
+    }
 };
 
 struct FArgs {
@@ -336,22 +360,19 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT)
     if (ya >= yb)
         return;
     const int lo = max(ya - NS - 2, a.A.roff), hi = min(yb + NS + 1, a.A.roff + a.A.nrows - 1);
-    const int cs = max(xl, 0), ce = min(xl + WD, (int)P);
-    const uint32_t rowbytes = (uint32_t)(ce - cs) * 8u;
-    const int soff = cs - xl;
     const int cxl = x0 / 2 - CH;
-    const int ccs = max(cxl, 0), cce = min(cxl + WC, (int)CP);
-    const uint32_t crowbytes = (uint32_t)(cce - ccs) * 8u;
-    const int csoff = ccs - cxl;
     const int Jlo = (ya + 1) / 2, Jhi = min((yb - 1) / 2, a.ncy);  // restricted rows: 2J in [ya, yb)
     const int Kend = Jhi >= Jlo ? Jhi + 1 : Jlo - 1;
 
     const int tid = threadIdx.x, grp = tid / NPG, m = tid % NPG;
     const bool producer = tid == C::NTW;  // lane 0 of the producer warp issues every TMA copy
+    const DoneRing dn{bar + SD + 4, lo};
 
     if (tid == 0) {
         for (int i = 0; i < SD + 4; i++)
             mbar_init(&bar[i], 1);
+        for (int i = 0; i < C::NG * NSLOT; i++)
+            mbar_init(&dn.b[i], NPG / 32);
         fence_mbar_init();
     }
     __syncthreads();
@@ -362,9 +383,7 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT)
     auto issue_row = [&](int row) {
         const int slot = (row - lo) % SD;
         uint64_t *b = &bar[slot];
-        mbar_arrive_tx(b, (BMG_EXP & 32) ? 0u : (uint32_t)(NA * WD * 8));
-        if (BMG_EXP & 32)
-            return;
+        mbar_arrive_tx(b, (uint32_t)(NA * WD * 8));
         double *d = smS + slot * (NA * WD);
         tma_2d(d + A_U * WD, &tmaps.u, xl, row - a.A.roff, b);
         tma_2d(d + A_F * WD, &tmaps.f, xl, row - a.A.roff, b);
@@ -464,77 +483,100 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT)
         }
     };
 
-    // Task groups (warp-aligned, one task per step):
+    // Task groups (warp-aligned, one task per row step), decoupled: a group
+    // waits only on the step-completion rings of the groups whose results (RAW)
+    // or ring slots (WAR) it touches, so stages overlap instead of meeting at a
+    // CTA-wide barrier every step.
     //  5-point: 0..NS-1 colour stage k = grp+1; NS, NS+1 residual of even/odd columns;
     //           NS+2 store; NS+3 restriction; NS+4, NS+5 split.
     //  9-point: 0,1 the two active row stages (phase A even columns, phase B odd);
     //           2,3 residual; 4 store; 5 restriction; 6,7 split.
-    constexpr int G_SPLIT = KIND == 5 ? NS + 4 : 6;
+    // Dependencies at step t (all on step t-1 unless noted):
+    //  split    <- residual (reads the slot's old row t-RM), store; TMA of row t
+    //  stage 1  <- split (row t-1 = r+1);  stage k <- stage k-1 (row r+1)
+    //  9-point: group 0 <- split, group 1 <- group 0 (stage k-1 ran in group 0
+    //           or in the same group; phases ordered by the group barrier)
+    //  residual <- last stage (row rr+1), restriction (residual ring slot)
+    //  store    <- last stage at t-3;  restriction <- residual; weights TMA
+    //  producer <- split (staging slot of row t-1), restriction (weight slot)
+    constexpr int NSG = KIND == 5 ? NS : 2;  // colour-stage groups
+    constexpr int G_RES = NSG, G_STORE = NSG + 2, G_RESTR = NSG + 3, G_SPLIT = NSG + 4;
     constexpr int QSPLIT = KIND == 5 ? 3 : 4;  // arrays [0,QSPLIT) by the first split group
     const int tend = yb + 2 * NS + 3;
-    int tm = 0, tsd = 0;  // main / staging ring slots of row t
-    for (int t = lo; t <= tend; t++, tm = (tm + 1 == RM) ? 0 : tm + 1, tsd = (tsd + 1 == SD) ? 0 : tsd + 1) {
-        if (producer) {
-            // No proxy fence: staging slots are only READ by generic-proxy code before the
-            // TMA (async proxy) overwrites them, and the step barrier orders that WAR.
+    if (grp >= C::NG) {
+        if (!producer)
+            return;
+        for (int t = lo; t <= tend; t++) {
+            dn.wait(G_SPLIT, t - 1);
+            dn.wait(G_SPLIT + 1, t - 1);
+            dn.wait(G_RESTR, t - 1);
+            // No proxy fence: staging slots are only READ by generic-proxy code before
+            // the TMA (async proxy) overwrites them, ordered by the mbarrier wait above.
             if (t + D <= hi)
                 issue_row(t + D);
-            if (!(BMG_EXP & 64))
-                issue_coarse(t);
+            issue_coarse(t);
         }
-        const int jr = t - 2 * NS - 4;
-        const int J = jr >> 1;
-        const bool restr = jr >= 0 && !(jr & 1) && J >= Jlo && J <= Jhi;
-        if (grp >= C::NG) {
-            // producer warp: no compute task
-        } else if (grp >= G_SPLIT) {
+        return;
+    }
+    int tm = 0, tsd = 0;  // main / staging ring slots of row t
+    for (int t = lo; t <= tend; t++, tm = (tm + 1 == RM) ? 0 : tm + 1, tsd = (tsd + 1 == SD) ? 0 : tsd + 1) {
+        if (grp >= G_SPLIT) {
+            dn.wait(G_RES, t - 1);
+            dn.wait(G_RES + 1, t - 1);
+            dn.wait(G_STORE, t - 1);
             if (t <= hi) {
                 mbar_wait(&bar[tsd], ((t - lo) / SD) & 1);
-                if (BMG_EXP & 8) {
-                } else if (grp == G_SPLIT)
+                if (grp == G_SPLIT)
                     split_row<NA, AM, WD, PPT, NPG>(sm, smS, tsd, tm, 0, QSPLIT, m);
                 else
                     split_row<NA, AM, WD, PPT, NPG>(sm, smS, tsd, tm, QSPLIT, NA, m);
             }
-        } else if (KIND == 5) {
-            if (grp < NS) {
+        } else if (grp < NSG) {
+            if (grp == 0) {
+                dn.wait(G_SPLIT, t - 1);
+                dn.wait(G_SPLIT + 1, t - 1);
+            } else {
+                dn.wait(grp - 1, t - 1);
+            }
+            if (KIND == 5) {
                 const int k = grp + 1, d = 2 * k, r = t - d;
-                if (!(BMG_EXP & 1) && r > lo && r < hi && r >= 1 && r <= ny)
-                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1),
-                                                        back<RM>(tm, d - 1), (((k - 1) & 1) - r) & 1, kc);
-            } else if (grp <= NS + 1) {
-                const int d = 2 * NS + 2;
-                if (!(BMG_EXP & 2))
-                    resid_task(t - d, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), grp - NS);
-            } else if (grp == NS + 2) {
-                if (!(BMG_EXP & 16))
-                    store_task(t - 2 * NS - 3, back<RM>(tm, 2 * NS + 3));
-            } else if (restr && !(BMG_EXP & 4)) {
-                restrict_task(J);
+                if (r > lo && r < hi && r >= 1 && r <= ny)
+                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1),
+                                                   (((k - 1) & 1) - r) & 1, kc);
+            } else {
+                // active 9-point row stages at step t: k with (t - 2k) & 1 == (k - 1) & 1, i.e. (t + k) odd
+                const int k = ((t & 1) ? 2 : 1) + 2 * grp, d = 2 * k, r = t - d;
+                const bool act = k <= NS && r > lo && r < hi && r >= 1 && r <= ny;
+                if (act)
+                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), 0,
+                                                   kc);
+                group_sync(1 + grp, NPG);
+                if (act)
+                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), 1,
+                                                   kc);
+                group_sync(1 + grp, NPG);
             }
+        } else if (grp < G_STORE) {
+            dn.wait(NSG - 1, t - 1);
+            if (KIND == 9)
+                dn.wait(0, t - 1);
+            dn.wait(G_RESTR, t - 1);
+            const int d = 2 * NS + 2;
+            resid_task(t - d, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), grp - G_RES);
+        } else if (grp == G_STORE) {
+            dn.wait(NSG - 1, t - 3);
+            if (KIND == 9)
+                dn.wait(0, t - 3);
+            store_task(t - 2 * NS - 3, back<RM>(tm, 2 * NS + 3));
         } else {
-            // active 9-point row stages at step t: k with (t - 2k) & 1 == (k - 1) & 1, i.e. (t + k) odd
-            const int k = ((t & 1) ? 2 : 1) + 2 * grp, d = 2 * k, r = t - d;
-            if (grp < 2) {
-                if (k <= NS && r > lo && r < hi && r >= 1 && r <= ny)
-                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1),
-                                                        back<RM>(tm, d - 1), 0, kc);
-            } else if (grp < 4) {
-                const int dr = 2 * NS + 2;
-                resid_task(t - dr, back<RM>(tm, dr), back<RM>(tm, dr + 1), back<RM>(tm, dr - 1), grp - 2);
-            } else if (grp == 4) {
-                store_task(t - 2 * NS - 3, back<RM>(tm, 2 * NS + 3));
-            } else if (restr) {
+            dn.wait(G_RES, t - 1);
+            dn.wait(G_RES + 1, t - 1);
+            const int jr = t - 2 * NS - 4;
+            const int J = jr >> 1;
+            if (jr >= 0 && !(jr & 1) && J >= Jlo && J <= Jhi)
                 restrict_task(J);
-            }
         }
-        __syncthreads();
-        if (KIND == 9) {
-            const int k = ((t & 1) ? 2 : 1) + 2 * grp, d = 2 * k, r = t - d;
-            if (grp < 2 && k <= NS && r > lo && r < hi && r >= 1 && r <= ny)
-                colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), 1, kc);
-            __syncthreads();
-        }
+        dn.arrive(grp, t);
     }
 }
 
@@ -553,7 +595,7 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT)
     uint64_t *bar = (uint64_t *)(sC + 32 * WC);
 
     const int nx = a.A.nx, ny = a.A.ny;
-    const long long P = a.A.pitch, CP = a.ci.pitch;
+    const long long P = a.A.pitch;
     const int strip = blockIdx.x % a.nstrips, chunk = blockIdx.x / a.nstrips;
     const int x0 = strip * TX, xl = x0 - H;
     const int ya = a.A.ylo + chunk * a.chunk, yb = min(a.A.yhi, ya + a.chunk);
@@ -561,21 +603,18 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT)
         return;
     const int lo = max(ya - NS, a.A.roff), hi = min(yb + NS - 1, a.A.roff + a.A.nrows - 1);
     const int lo1 = max(lo, 1), hi1 = min(hi, ny);  // corrected rows
-    const int cs = max(xl, 0), ce = min(xl + WD, (int)P);
-    const uint32_t rowbytes = (uint32_t)(ce - cs) * 8u;
-    const int soff = cs - xl;
     const int cxl = x0 / 2 - CH;
-    const int ccs = max(cxl, 0), cce = min(cxl + WC, (int)CP);
-    const uint32_t crowbytes = (uint32_t)(cce - ccs) * 8u;
-    const int csoff = ccs - cxl;
     const int Klo = lo1 / 2, Khi = (hi1 + 1) / 2;
 
     const int tid = threadIdx.x, grp = tid / NPG, m = tid % NPG;
     const bool producer = tid == C::NTW;  // lane 0 of the producer warp issues every TMA copy
+    const DoneRing dn{bar + SD + 4, lo};
 
     if (tid == 0) {
         for (int i = 0; i < SD + 4; i++)
             mbar_init(&bar[i], 1);
+        for (int i = 0; i < C::NG * NSLOT; i++)
+            mbar_init(&dn.b[i], NPG / 32);
         fence_mbar_init();
     }
     __syncthreads();
@@ -584,9 +623,7 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT)
     auto issue_row = [&](int row) {
         const int slot = (row - lo) % SD;
         uint64_t *b = &bar[slot];
-        mbar_arrive_tx(b, (BMG_EXP & 32) ? 0u : (uint32_t)(NA * WD * 8));
-        if (BMG_EXP & 32)
-            return;
+        mbar_arrive_tx(b, (uint32_t)(NA * WD * 8));
         double *d = smS + slot * (NA * WD);
         tma_2d(d + A_U * WD, &tmaps.u, xl, row - a.A.roff, b);
         tma_2d(d + A_F * WD, &tmaps.f, xl, row - a.A.roff, b);
@@ -675,26 +712,43 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT)
 
     const Cols<PPT> kc = make_cols<WD, PPT, NPG>(m, xl, nx);
 
-    // Task groups: 5-point: 0,1 correction of even/odd columns; 2..NS+1 stage k = grp-1;
-    //              NS+2 store; NS+3, NS+4 split.
-    //              9-point: 0,1 active row stage(s) (phase A, B); 2,3 correction;
-    //              4 store; 5, 6 split.
-    constexpr int G_SPLIT = KIND == 5 ? NS + 3 : 5;
+    // Task groups (decoupled as in the down leg):
+    //  5-point: 0,1 correction of even/odd columns; 2..NS+1 stage k = grp-1;
+    //           NS+2 store; NS+3, NS+4 split.
+    //  9-point: 0,1 active row stage(s) (phase A, B); 2,3 correction; 4 store; 5, 6 split.
+    // Dependencies at step t (on step t-1):
+    //  split      <- last stage (reads the slot's old row t-RM), store; TMA of row t
+    //  correction <- split (row t-1); coarse TMA
+    //  stage 1    <- correction (row r+1 = t-2);  stage k <- stage k-1
+    //  9-point: group 0 <- correction, group 1 <- group 0
+    //  store      <- last stage;  producer <- split, correction (coarse slots)
+    constexpr int NSG = KIND == 5 ? NS : 2;
+    constexpr int G_ST0 = KIND == 5 ? 2 : 0, G_CORR = KIND == 5 ? 0 : 2;
+    constexpr int G_LAST = G_ST0 + NSG - 1;
+    constexpr int G_STORE = NSG + 2, G_SPLIT = NSG + 3;
     constexpr int QSPLIT = KIND == 5 ? 3 : 4;
     const int tend = yb + 2 * NS + 1;
-    int tm = 0, tsd = 0;
-    for (int t = lo; t <= tend; t++, tm = (tm + 1 == RM) ? 0 : tm + 1, tsd = (tsd + 1 == SD) ? 0 : tsd + 1) {
-        if (producer) {
-            // No proxy fence: staging slots are only READ by generic-proxy code before the
-            // TMA (async proxy) overwrites them, and the step barrier orders that WAR.
+    if (grp >= C::NG) {
+        if (!producer)
+            return;
+        for (int t = lo; t <= tend; t++) {
+            dn.wait(G_SPLIT, t - 1);
+            dn.wait(G_SPLIT + 1, t - 1);
+            dn.wait(G_CORR, t - 1);
+            dn.wait(G_CORR + 1, t - 1);
             if (t + D <= hi)
                 issue_row(t + D);
-            if (!(BMG_EXP & 64))
-                issue_coarse(t);
+            issue_coarse(t);
         }
-        if (grp >= C::NG) {
-            // producer warp: no compute task
-        } else if (grp >= G_SPLIT) {
+        return;
+    }
+    int tm = 0, tsd = 0;
+    for (int t = lo; t <= tend; t++, tm = (tm + 1 == RM) ? 0 : tm + 1, tsd = (tsd + 1 == SD) ? 0 : tsd + 1) {
+        if (grp >= G_SPLIT) {
+            dn.wait(G_LAST, t - 1);
+            if (KIND == 9)
+                dn.wait(G_ST0, t - 1);
+            dn.wait(G_STORE, t - 1);
             if (t <= hi) {
                 mbar_wait(&bar[tsd], ((t - lo) / SD) & 1);
                 if (grp == G_SPLIT)
@@ -702,37 +756,42 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT)
                 else
                     split_row<NA, AM, WD, PPT, NPG>(sm, smS, tsd, tm, QSPLIT, NA, m);
             }
-        } else if (KIND == 5) {
-            if (grp < 2) {
-                correct_task(t - 1, back<RM>(tm, 1), grp);
-            } else if (grp < NS + 2) {
-                const int k = grp - 1, d = 2 * k + 1, r = t - d;
-                if (r > lo && r < hi && r >= 1 && r <= ny)
-                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1),
-                                                        back<RM>(tm, d - 1), (((k - 1) & 1) - r) & 1, kc);
+        } else if (grp == G_CORR || grp == G_CORR + 1) {
+            dn.wait(G_SPLIT, t - 1);
+            dn.wait(G_SPLIT + 1, t - 1);
+            correct_task(t - 1, back<RM>(tm, 1), grp - G_CORR);
+        } else if (grp < G_ST0 + NSG) {
+            if (grp == G_ST0) {
+                dn.wait(G_CORR, t - 1);
+                dn.wait(G_CORR + 1, t - 1);
             } else {
-                store_task(t - 2 * NS - 2, back<RM>(tm, 2 * NS + 2));
+                dn.wait(grp - 1, t - 1);
+            }
+            if (KIND == 5) {
+                const int k = grp - G_ST0 + 1, d = 2 * k + 1, r = t - d;
+                if (r > lo && r < hi && r >= 1 && r <= ny)
+                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1),
+                                                   (((k - 1) & 1) - r) & 1, kc);
+            } else {
+                // active 9-point row stage(s): k with (t-1-2k) & 1 == (k-1) & 1, i.e. (t + k) even
+                const int k = ((t & 1) ? 1 : 2) + 2 * grp, d = 2 * k + 1, r = t - d;
+                const bool act = k <= NS && r > lo && r < hi && r >= 1 && r <= ny;
+                if (act)
+                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), 0,
+                                                   kc);
+                group_sync(1 + grp, NPG);
+                if (act)
+                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), 1,
+                                                   kc);
+                group_sync(1 + grp, NPG);
             }
         } else {
-            // active 9-point row stage(s): k with (t-1-2k) & 1 == (k-1) & 1, i.e. (t + k) even
-            const int k = ((t & 1) ? 1 : 2) + 2 * grp, d = 2 * k + 1, r = t - d;
-            if (grp < 2) {
-                if (k <= NS && r > lo && r < hi && r >= 1 && r <= ny)
-                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1),
-                                                        back<RM>(tm, d - 1), 0, kc);
-            } else if (grp < 4) {
-                correct_task(t - 1, back<RM>(tm, 1), grp - 2);
-            } else {
-                store_task(t - 2 * NS - 2, back<RM>(tm, 2 * NS + 2));
-            }
+            dn.wait(G_LAST, t - 1);
+            if (KIND == 9)
+                dn.wait(G_ST0, t - 1);
+            store_task(t - 2 * NS - 2, back<RM>(tm, 2 * NS + 2));
         }
-        __syncthreads();
-        if (KIND == 9) {
-            const int k = ((t & 1) ? 1 : 2) + 2 * grp, d = 2 * k + 1, r = t - d;
-            if (grp < 2 && k <= NS && r > lo && r < hi && r >= 1 && r <= ny)
-                colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), 1, kc);
-            __syncthreads();
-        }
+        dn.arrive(grp, t);
     }
 }
 
