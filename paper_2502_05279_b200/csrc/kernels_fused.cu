@@ -132,25 +132,50 @@ struct Cfg {
     static_assert(NPG % 32 == 0, "task groups must be whole warps");
 };
 
-// Step-completion rings: group g arrives (one arrival per warp) on slot t mod
-// NSLOT after finishing row step t; a consumer waits on the producer's step.
-// Every dependency cycle of the pipeline spans fewer than NSLOT steps, so no
-// warp is ever NSLOT steps ahead of a waiter or of the slowest warp of its group.
-struct DoneRing {
-    uint64_t *b;
-    int lo;
-    __device__ __forceinline__ void arrive(int g, int t) const
+// Step-completion rings, one per waiting task: ring r slot (t mod NSLOT)
+// completes when every warp of the groups that task depends on has finished
+// row step t (each warp arrives once, after __syncwarp).  A task therefore waits
+// on exactly one mbarrier per step.  Every dependency cycle of the pipeline
+// spans fewer than NSLOT steps, so no warp is ever NSLOT steps ahead of a waiter
+// or of another warp arriving on the same ring.
+struct Rings {
+    uint32_t base;  // shared-memory address of ring 0, slot 0
+    int lo;         // first row step
+    __device__ __forceinline__ uint32_t at(int r, int t) const
     {
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0)
-            mbar_arrive(&b[g * NSLOT + ((t - lo) & (NSLOT - 1))]);
+        return base + 8u * (uint32_t)(r * NSLOT + ((t - lo) & (NSLOT - 1)));
     }
-    __device__ __forceinline__ void wait(int g, int t) const
+    __device__ __forceinline__ void arrive(int r, int t) const
+    {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(at(r, t)) : "memory");
+    }
+    __device__ __forceinline__ void wait(int r, int t) const
     {
         if (t < lo)
             return;
-        const int s = t - lo;
-        mbar_wait(&b[g * NSLOT + (s & (NSLOT - 1))], (s / NSLOT) & 1);
+        const uint32_t par = ((t - lo) / NSLOT) & 1;
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "RWAIT:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+            "@!P1 bra RWAIT;\n"
+            "}\n" ::"r"(at(r, t)),
+            "r"(par)
+            : "memory");
+    }
+    // end of step t for one warp: arrive on rings a, b, c (-1: none)
+    __device__ __forceinline__ void done(int t, int a, int b, int c) const
+    {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+            if (a >= 0)
+                arrive(a, t);
+            if (b >= 0)
+                arrive(b, t);
+            if (c >= 0)
+                arrive(c, t);
+        }
     }
 };
 
@@ -340,7 +365,7 @@ __device__ __forceinline__ void split_row(double *smM, const double *smS, int ss
 
 // ------------------------------------------------------------------ down kernel
 template <int KIND, int NS, int WD, int D, int PPT>
-__global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT)
+__global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT, 1)
     k_fused_down(FArgs a, const __grid_constant__ TMaps tmaps)
 {
     using C = Cfg<KIND, NS, WD, D, false, PPT>;
@@ -366,13 +391,37 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT)
 
     const int tid = threadIdx.x, grp = tid / NPG, m = tid % NPG;
     const bool producer = tid == C::NTW;  // lane 0 of the producer warp issues every TMA copy
-    const DoneRing dn{bar + SD + 4, lo};
+    // Task groups (warp-aligned, one task per row step):
+    //  5-point: 0..NS-1 colour stage k = grp+1; NS, NS+1 residual of even/odd columns;
+    //           NS+2 store; NS+3 restriction; NS+4, NS+5 split.
+    //  9-point: 0,1 the two active row stages (phase A even columns, phase B odd);
+    //           2,3 residual; 4 store; 5 restriction; 6,7 split.
+    constexpr int NSG = KIND == 5 ? NS : 2;  // colour-stage groups
+    constexpr int G_RES = NSG, G_STORE = NSG + 2, G_SPLIT = NSG + 4;  // restriction: NSG + 3
+    // Rings (waiter <- groups it depends on, at step t-1 unless noted):
+    //  g < NSG  stage group g <- split (g = 0) or stage group g-1: row r+1 = t-2k+1
+    //  R_RES    residual <- last stage group(s) (row rr+1), restriction (residual-ring slot)
+    //  R_STORE  store <- last stage group(s), at step t-3
+    //  R_RESTR  restriction <- residual groups
+    //  R_SPLIT  split <- residual groups, store (the main slot's old row t-RM)
+    //  R_PROD   producer <- split groups (staging slot of row t-1), restriction (weight slot)
+    constexpr int W = NPG / 32;
+    constexpr int R_RES = NSG, R_STORE = NSG + 1, R_RESTR = NSG + 2, R_SPLIT = NSG + 3, R_PROD = NSG + 4;
+    constexpr int NR = NSG + 5;
+    static_assert(NR <= C::NG, "ring space");
+    const Rings rg{smem_u32(bar + SD + 4), lo};
 
     if (tid == 0) {
         for (int i = 0; i < SD + 4; i++)
             mbar_init(&bar[i], 1);
-        for (int i = 0; i < C::NG * NSLOT; i++)
-            mbar_init(&dn.b[i], NPG / 32);
+        for (int r = 0; r < NR; r++) {
+            const int cnt = r < NSG ? (r == 0 ? 2 * W : W)
+                            : r == R_RES ? (KIND == 5 ? 2 : 3) * W
+                            : r == R_STORE ? (KIND == 5 ? 1 : 2) * W
+                            : r == R_RESTR ? 2 * W : 3 * W;
+            for (int q = 0; q < NSLOT; q++)
+                mbar_init(bar + SD + 4 + r * NSLOT + q, cnt);
+        }
         fence_mbar_init();
     }
     __syncthreads();
@@ -483,33 +532,16 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT)
         }
     };
 
-    // Task groups (warp-aligned, one task per row step), decoupled: a group
-    // waits only on the step-completion rings of the groups whose results (RAW)
-    // or ring slots (WAR) it touches, so stages overlap instead of meeting at a
-    // CTA-wide barrier every step.
-    //  5-point: 0..NS-1 colour stage k = grp+1; NS, NS+1 residual of even/odd columns;
-    //           NS+2 store; NS+3 restriction; NS+4, NS+5 split.
-    //  9-point: 0,1 the two active row stages (phase A even columns, phase B odd);
-    //           2,3 residual; 4 store; 5 restriction; 6,7 split.
-    // Dependencies at step t (all on step t-1 unless noted):
-    //  split    <- residual (reads the slot's old row t-RM), store; TMA of row t
-    //  stage 1  <- split (row t-1 = r+1);  stage k <- stage k-1 (row r+1)
-    //  9-point: group 0 <- split, group 1 <- group 0 (stage k-1 ran in group 0
-    //           or in the same group; phases ordered by the group barrier)
-    //  residual <- last stage (row rr+1), restriction (residual ring slot)
-    //  store    <- last stage at t-3;  restriction <- residual; weights TMA
-    //  producer <- split (staging slot of row t-1), restriction (weight slot)
-    constexpr int NSG = KIND == 5 ? NS : 2;  // colour-stage groups
-    constexpr int G_RES = NSG, G_STORE = NSG + 2, G_RESTR = NSG + 3, G_SPLIT = NSG + 4;
+    // Decoupled pipeline: each group waits only on its own ring, i.e. on the
+    // groups whose results (RAW) or ring slots (WAR) it touches, so stages
+    // overlap instead of meeting at a CTA-wide barrier every step.
     constexpr int QSPLIT = KIND == 5 ? 3 : 4;  // arrays [0,QSPLIT) by the first split group
     const int tend = yb + 2 * NS + 3;
     if (grp >= C::NG) {
         if (!producer)
             return;
         for (int t = lo; t <= tend; t++) {
-            dn.wait(G_SPLIT, t - 1);
-            dn.wait(G_SPLIT + 1, t - 1);
-            dn.wait(G_RESTR, t - 1);
+            rg.wait(R_PROD, t - 1);
             // No proxy fence: staging slots are only READ by generic-proxy code before
             // the TMA (async proxy) overwrites them, ordered by the mbarrier wait above.
             if (t + D <= hi)
@@ -518,12 +550,26 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT)
         }
         return;
     }
+    // rings this group arrives on after each step
+    int a0 = -1, a1 = -1, a2 = -1;
+    if (grp >= G_SPLIT) {
+        a0 = 0, a1 = R_PROD;
+    } else if (grp < NSG) {
+        if (grp + 1 < NSG)
+            a0 = grp + 1;
+        if (KIND == 9 || grp == NSG - 1)
+            a1 = R_RES, a2 = R_STORE;
+    } else if (grp < G_STORE) {
+        a0 = R_SPLIT, a1 = R_RESTR;
+    } else if (grp == G_STORE) {
+        a0 = R_SPLIT;
+    } else {
+        a0 = R_RES, a1 = R_PROD;
+    }
     int tm = 0, tsd = 0;  // main / staging ring slots of row t
     for (int t = lo; t <= tend; t++, tm = (tm + 1 == RM) ? 0 : tm + 1, tsd = (tsd + 1 == SD) ? 0 : tsd + 1) {
         if (grp >= G_SPLIT) {
-            dn.wait(G_RES, t - 1);
-            dn.wait(G_RES + 1, t - 1);
-            dn.wait(G_STORE, t - 1);
+            rg.wait(R_SPLIT, t - 1);
             if (t <= hi) {
                 mbar_wait(&bar[tsd], ((t - lo) / SD) & 1);
                 if (grp == G_SPLIT)
@@ -532,12 +578,7 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT)
                     split_row<NA, AM, WD, PPT, NPG>(sm, smS, tsd, tm, QSPLIT, NA, m);
             }
         } else if (grp < NSG) {
-            if (grp == 0) {
-                dn.wait(G_SPLIT, t - 1);
-                dn.wait(G_SPLIT + 1, t - 1);
-            } else {
-                dn.wait(grp - 1, t - 1);
-            }
+            rg.wait(grp, t - 1);
             if (KIND == 5) {
                 const int k = grp + 1, d = 2 * k, r = t - d;
                 if (r > lo && r < hi && r >= 1 && r <= ny)
@@ -557,32 +598,26 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT)
                 group_sync(1 + grp, NPG);
             }
         } else if (grp < G_STORE) {
-            dn.wait(NSG - 1, t - 1);
-            if (KIND == 9)
-                dn.wait(0, t - 1);
-            dn.wait(G_RESTR, t - 1);
+            rg.wait(R_RES, t - 1);
             const int d = 2 * NS + 2;
             resid_task(t - d, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), grp - G_RES);
         } else if (grp == G_STORE) {
-            dn.wait(NSG - 1, t - 3);
-            if (KIND == 9)
-                dn.wait(0, t - 3);
+            rg.wait(R_STORE, t - 3);
             store_task(t - 2 * NS - 3, back<RM>(tm, 2 * NS + 3));
         } else {
-            dn.wait(G_RES, t - 1);
-            dn.wait(G_RES + 1, t - 1);
+            rg.wait(R_RESTR, t - 1);
             const int jr = t - 2 * NS - 4;
             const int J = jr >> 1;
             if (jr >= 0 && !(jr & 1) && J >= Jlo && J <= Jhi)
                 restrict_task(J);
         }
-        dn.arrive(grp, t);
+        rg.done(t, a0, a1, a2);
     }
 }
 
 // ------------------------------------------------------------------ up kernel
 template <int KIND, int NS, int WD, int D, int PPT>
-__global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT)
+__global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT, 1)
     k_fused_up(FArgs a, const __grid_constant__ TMaps tmaps)
 {
     using C = Cfg<KIND, NS, WD, D, true, PPT>;
@@ -608,13 +643,35 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT)
 
     const int tid = threadIdx.x, grp = tid / NPG, m = tid % NPG;
     const bool producer = tid == C::NTW;  // lane 0 of the producer warp issues every TMA copy
-    const DoneRing dn{bar + SD + 4, lo};
+    // Task groups:
+    //  5-point: 0,1 correction of even/odd columns; 2..NS+1 stage k = grp-1;
+    //           NS+2 store; NS+3, NS+4 split.
+    //  9-point: 0,1 active row stage(s) (phase A, B); 2,3 correction; 4 store; 5, 6 split.
+    constexpr int NSG = KIND == 5 ? NS : 2;
+    constexpr int G_ST0 = KIND == 5 ? 2 : 0, G_CORR = KIND == 5 ? 0 : 2;
+    constexpr int G_SPLIT = NSG + 3;  // store: NSG + 2
+    // Rings (waiter <- groups it depends on, at step t-1):
+    //  g < NSG  stage group g <- correction groups (g = 0: row r+1 = t-2) or stage group g-1
+    //  R_CORR   correction <- split groups (row t-1)
+    //  R_STORE  store <- last stage group(s)
+    //  R_SPLIT  split <- last stage group(s) (reads the slot's old row t-RM), store
+    //  R_PROD   producer <- split groups (staging slot), correction groups (coarse slots)
+    constexpr int W = NPG / 32;
+    constexpr int R_CORR = NSG, R_STORE = NSG + 1, R_SPLIT = NSG + 2, R_PROD = NSG + 3, NR = NSG + 4;
+    static_assert(NR <= C::NG, "ring space");
+    const Rings rg{smem_u32(bar + SD + 4), lo};
 
     if (tid == 0) {
         for (int i = 0; i < SD + 4; i++)
             mbar_init(&bar[i], 1);
-        for (int i = 0; i < C::NG * NSLOT; i++)
-            mbar_init(&dn.b[i], NPG / 32);
+        for (int r = 0; r < NR; r++) {
+            const int cnt = r < NSG ? (r == 0 ? 2 * W : W)
+                            : r == R_CORR ? 2 * W
+                            : r == R_STORE ? (KIND == 5 ? 1 : 2) * W
+                            : r == R_SPLIT ? (KIND == 5 ? 2 : 3) * W : 4 * W;
+            for (int q = 0; q < NSLOT; q++)
+                mbar_init(bar + SD + 4 + r * NSLOT + q, cnt);
+        }
         fence_mbar_init();
     }
     __syncthreads();
@@ -712,43 +769,37 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT)
 
     const Cols<PPT> kc = make_cols<WD, PPT, NPG>(m, xl, nx);
 
-    // Task groups (decoupled as in the down leg):
-    //  5-point: 0,1 correction of even/odd columns; 2..NS+1 stage k = grp-1;
-    //           NS+2 store; NS+3, NS+4 split.
-    //  9-point: 0,1 active row stage(s) (phase A, B); 2,3 correction; 4 store; 5, 6 split.
-    // Dependencies at step t (on step t-1):
-    //  split      <- last stage (reads the slot's old row t-RM), store; TMA of row t
-    //  correction <- split (row t-1); coarse TMA
-    //  stage 1    <- correction (row r+1 = t-2);  stage k <- stage k-1
-    //  9-point: group 0 <- correction, group 1 <- group 0
-    //  store      <- last stage;  producer <- split, correction (coarse slots)
-    constexpr int NSG = KIND == 5 ? NS : 2;
-    constexpr int G_ST0 = KIND == 5 ? 2 : 0, G_CORR = KIND == 5 ? 0 : 2;
-    constexpr int G_LAST = G_ST0 + NSG - 1;
-    constexpr int G_STORE = NSG + 2, G_SPLIT = NSG + 3;
     constexpr int QSPLIT = KIND == 5 ? 3 : 4;
     const int tend = yb + 2 * NS + 1;
     if (grp >= C::NG) {
         if (!producer)
             return;
         for (int t = lo; t <= tend; t++) {
-            dn.wait(G_SPLIT, t - 1);
-            dn.wait(G_SPLIT + 1, t - 1);
-            dn.wait(G_CORR, t - 1);
-            dn.wait(G_CORR + 1, t - 1);
+            rg.wait(R_PROD, t - 1);
             if (t + D <= hi)
                 issue_row(t + D);
             issue_coarse(t);
         }
         return;
     }
+    int a0 = -1, a1 = -1, a2 = -1;
+    if (grp >= G_SPLIT) {
+        a0 = R_CORR, a1 = R_PROD;
+    } else if (grp == G_CORR || grp == G_CORR + 1) {
+        a0 = 0, a1 = R_PROD;
+    } else if (grp < G_ST0 + NSG) {
+        const int g = grp - G_ST0;
+        if (g + 1 < NSG)
+            a0 = g + 1;
+        if (KIND == 9 || g == NSG - 1)
+            a1 = R_SPLIT, a2 = R_STORE;
+    } else {
+        a0 = R_SPLIT;
+    }
     int tm = 0, tsd = 0;
     for (int t = lo; t <= tend; t++, tm = (tm + 1 == RM) ? 0 : tm + 1, tsd = (tsd + 1 == SD) ? 0 : tsd + 1) {
         if (grp >= G_SPLIT) {
-            dn.wait(G_LAST, t - 1);
-            if (KIND == 9)
-                dn.wait(G_ST0, t - 1);
-            dn.wait(G_STORE, t - 1);
+            rg.wait(R_SPLIT, t - 1);
             if (t <= hi) {
                 mbar_wait(&bar[tsd], ((t - lo) / SD) & 1);
                 if (grp == G_SPLIT)
@@ -757,16 +808,10 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT)
                     split_row<NA, AM, WD, PPT, NPG>(sm, smS, tsd, tm, QSPLIT, NA, m);
             }
         } else if (grp == G_CORR || grp == G_CORR + 1) {
-            dn.wait(G_SPLIT, t - 1);
-            dn.wait(G_SPLIT + 1, t - 1);
+            rg.wait(R_CORR, t - 1);
             correct_task(t - 1, back<RM>(tm, 1), grp - G_CORR);
         } else if (grp < G_ST0 + NSG) {
-            if (grp == G_ST0) {
-                dn.wait(G_CORR, t - 1);
-                dn.wait(G_CORR + 1, t - 1);
-            } else {
-                dn.wait(grp - 1, t - 1);
-            }
+            rg.wait(grp - G_ST0, t - 1);
             if (KIND == 5) {
                 const int k = grp - G_ST0 + 1, d = 2 * k + 1, r = t - d;
                 if (r > lo && r < hi && r >= 1 && r <= ny)
@@ -786,12 +831,10 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT)
                 group_sync(1 + grp, NPG);
             }
         } else {
-            dn.wait(G_LAST, t - 1);
-            if (KIND == 9)
-                dn.wait(G_ST0, t - 1);
+            rg.wait(R_STORE, t - 1);
             store_task(t - 2 * NS - 2, back<RM>(tm, 2 * NS + 2));
         }
-        dn.arrive(grp, t);
+        rg.done(t, a0, a1, a2);
     }
 }
 
