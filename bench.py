@@ -236,7 +236,7 @@ def main():
         f = solver.grid(P.rhs_const(nx, ny))
         x = solver.grid()
         parallelism = "single GPU"
-        scaling = "weak"
+        scaling = "strong"  # the global problem is fixed; N GPUs split it
     del st
     L = bmg.bmg_num_levels(solver.h)
     kind = CONFIG_KIND.get(wl, 5)
@@ -255,11 +255,19 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     clocks.mark("t0")
+    if not distributed:
+        # the timed cycles launch their kernels directly with a CUDA event pair around
+        # every level-0 down leg (the roofline kernel) on this stream
+        bmg.bmg_timing(solver.h, True)
     ev0.record(stream)
     solver.vcycle(f, x, args.steps)
     ev1.record(stream)
     torch.cuda.synchronize()
     clocks.mark("t1")
+    leg = None
+    if not distributed:
+        leg = bmg.bmg_timing_read(solver.h)
+        bmg.bmg_timing(solver.h, False)
     if dist:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
@@ -276,7 +284,16 @@ def main():
     rl = None
     if not distributed:
         # roofline: the dominant kernel = level-0 down leg, launched alone through the ABI
-        rl = roofline(solver, bmg, torch, f, x, nx, ny, kind, peak, peak_src, ms_per_step, args)
+        rl = roofline(leg, nx, ny, kind, peak, peak_src, ms_per_step, args)
+        # for reference: the same cycles replayed as one CUDA graph each
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ng = max(10, args.steps // 4)
+        torch.cuda.synchronize()
+        g0.record(stream)
+        solver.vcycle(f, x, ng)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        rl["graph_replay_ms_per_step"] = g0.elapsed_time(g1) / ng
 
     # convergence sanity of the timed run (residual at the rounding floor after many cycles)
     rnorm = solver.residual_norm(f, x)
@@ -365,36 +382,40 @@ def main():
         dist.destroy_process_group()
 
 
-def roofline(solver, bmg, torch, f, x, nx, ny, kind, peak, peak_src, ms_per_step, args):
-    """Dominant kernel: the level-0 down leg.  Algorithmic bytes per launch =
+def traffic_per_launch(kernel: str, nx: int, ny: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel` at this
+    size, from the committed ncu --set full summary (profiles/traffic.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            rows = json.load(fh)["launches"]
+    except (OSError, ValueError, KeyError):
+        return None
+    for r in rows:
+        if r.get("kernel") == kernel and r.get("nx") == nx and r.get("ny") == ny:
+            return r["dram_bytes_read"] + r["dram_bytes_write"]
+    return None
+
+
+def roofline(leg, nx, ny, kind, peak, peak_src, ms_per_step, args):
+    """Dominant kernel: the level-0 down leg (one fused launch per cycle), timed by the
+    library's event pairs inside the timed region.  Algorithmic bytes per launch =
     per-fine-unknown bytes x nx*ny."""
-    stream = torch.cuda.current_stream()
-    fc = solver.level_grid(1)
-    uc = solver.level_grid(1)
-    u = x.clone()
-    u2 = torch.zeros_like(u)
-    nrep = 20
-    for _ in range(3):
-        bmg.bmg_smooth_restrict(solver.h, 0, f, u, u2, fc, uc)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    for _ in range(nrep):
-        bmg.bmg_smooth_restrict(solver.h, 0, f, u, u2, fc, uc)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    dur_ms = ev0.elapsed_time(ev1) / nrep
+    ms_total, launches = leg
+    dur_ms = ms_total / max(launches, 1)
     s_planes = 3 if kind == 5 else 5
     # compulsory bytes of the down leg per fine unknown (DESIGN §6): read u, f and the
     # s operator planes, write u, read the 2N-double CI planes, write f_c and zero u_c (N/4 each)
     per_unk = 8.0 * (s_planes + 2 + 1 + 2 + 0.25 + 0.25)
     algo = per_unk * nx * ny
     achieved = algo / (dur_ms / 1e3) / 1e9
+    kname = f"k_fused_down<{kind}, 4>" if not args.unfused else None
+    traffic = traffic_per_launch(kname, nx, ny) if kname else None
     return {"bound": "hbm", "kernel": "level-0 down leg (bmg_smooth_restrict: nu1 GS sweeps + residual + "
                                       "restriction)", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-            "algorithmic_bytes_per_unknown": per_unk, "launch_ms": dur_ms,
-            "share_of_step": dur_ms / ms_per_step}
+            "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": algo, "algorithmic_bytes_per_unknown": per_unk,
+            "launch_ms": dur_ms, "launches_timed": launches, "share_of_step": dur_ms / ms_per_step}
 
 
 if __name__ == "__main__":

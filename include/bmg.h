@@ -173,6 +173,17 @@ bmg_status_t bmg_correct_smooth(bmg_solver_t h, int level, const double *f, cons
 /* Number of kernels one bmg_vcycle cycle launches (the captured graph's kernel nodes). */
 bmg_status_t bmg_cycle_kernel_count(bmg_solver_t h, int *count);
 
+/* Measurement hook (bench.py's roofline figure).  enable != 0: subsequent
+ * bmg_vcycle calls on this single-GPU handle replay a variant of the cycle's
+ * graph with two event-record nodes around the level-0 down-leg launch, each
+ * launch re-pointed at a fresh CUDA event pair (timed on the caller's stream);
+ * enable == 0 returns to the plain graph.  Either call clears the records.
+ * bmg_timing_read waits for the recorded events and returns the summed
+ * duration (ms) and number of those launches since the last clear.
+ * EINVAL on a distributed handle. */
+bmg_status_t bmg_timing(bmg_solver_t h, int enable);
+bmg_status_t bmg_timing_read(bmg_solver_t h, double *ms_total, int *launches);
+
 /* ---------------------------------------------------------------------------
  * Multi-GPU: row-slab domain decomposition.
  *

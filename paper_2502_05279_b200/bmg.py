@@ -22,7 +22,8 @@ BMG_OK, BMG_EINVAL, BMG_ENOMEM, BMG_ECUDA, BMG_ENCCL, BMG_ENOTSPD, BMG_ENOTCONV 
 EXPORTS = (
     "bmg_params_default", "bmg_setup", "bmg_vcycle", "bmg_vcycle_host", "bmg_solve", "bmg_residual_norm",
     "bmg_num_levels", "bmg_level_shape", "bmg_level_pitch", "bmg_export_level", "bmg_relax", "bmg_residual",
-    "bmg_restrict", "bmg_interp_add", "bmg_smooth_restrict", "bmg_correct_smooth", "bmg_cycle_kernel_count", "bmg_destroy", "bmg_strerror",
+    "bmg_restrict", "bmg_interp_add", "bmg_smooth_restrict", "bmg_correct_smooth", "bmg_cycle_kernel_count", "bmg_timing",
+    "bmg_timing_read", "bmg_destroy", "bmg_strerror",
     "bmg_last_error_detail", "bmg_partition", "bmg_setup_dist", "bmg_local_rows",
 )
 
@@ -226,6 +227,18 @@ def bmg_cycle_kernel_count(h) -> int:
     c = ctypes.c_int()
     _check(lib().bmg_cycle_kernel_count(h, ctypes.byref(c)), "bmg_cycle_kernel_count")
     return c.value
+
+
+def bmg_timing(h, enable: bool) -> None:
+    _check(lib().bmg_timing(h, 1 if enable else 0), "bmg_timing")
+
+
+def bmg_timing_read(h):
+    """(summed ms, launches) of the level-0 down legs recorded since the last clear."""
+    ms = ctypes.c_double()
+    n = ctypes.c_int()
+    _check(lib().bmg_timing_read(h, ctypes.byref(ms), ctypes.byref(n)), "bmg_timing_read")
+    return ms.value, n.value
 
 
 def bmg_partition(nx: int, ny: int, nranks: int, params: bmg_params_t | None = None):

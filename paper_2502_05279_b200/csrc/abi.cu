@@ -65,6 +65,19 @@ long long round_pitch(int nx) { return ((long long)nx + 2 + 31) / 32 * 32; }
 
 }  // namespace
 
+struct GraphRec {
+    cudaGraphExec_t ex = nullptr;
+    cudaGraph_t g = nullptr;                         // kept for the timed variant's node handles
+    cudaGraphNode_t ev_node[2] = {nullptr, nullptr};  // event-record nodes (timed variant)
+    void destroy()
+    {
+        if (ex)
+            cudaGraphExecDestroy(ex);
+        if (g)
+            cudaGraphDestroy(g);
+    }
+};
+
 struct bmg_solver {
     bmg_params_t prm;
     int L = 0;
@@ -76,13 +89,17 @@ struct bmg_solver {
     double *partials = nullptr, *d_norm = nullptr, *h_norm = nullptr;  // h_norm pinned
     double *stage_f = nullptr, *stage_x = nullptr;                     // bmg_vcycle_host staging
     cudaStream_t cap = nullptr;                                        // capture stream
-    std::map<std::pair<const void *, const void *>, cudaGraphExec_t> graphs;
+    std::map<std::pair<const void *, const void *>, GraphRec> graphs, tgraphs;  // plain / timed
+    cudaEvent_t cev[2] = {nullptr, nullptr};  // placeholders captured into timed graphs
     int kernels_per_cycle = 0;
     FusedPlan fplan;
     DistSolver *dist = nullptr;  // row-slab distributed solver (bmg_setup_dist)
     bmg_solver_t dist_inner = nullptr;  // its replicated coarse solver (owned by dist)
     long long dist_rows_total = 0;      // doubles of a level-0 rhs/x array of this handle
     int dist_local_ranks = 1;
+    bool timing = false;              // bmg_timing: timed graph variant, event pair per launch
+    std::vector<cudaEvent_t> tev;     // event pairs (start, end) per recorded launch
+    size_t tev_used = 0;
 
     CIv civ(int l) const
     {
@@ -154,7 +171,14 @@ bmg_status_t bmg_destroy(bmg_solver_t h)
     }
     cudaDeviceSynchronize();
     for (auto &kv : h->graphs)
-        cudaGraphExecDestroy(kv.second);
+        kv.second.destroy();
+    for (auto &kv : h->tgraphs)
+        kv.second.destroy();
+    for (cudaEvent_t e : h->tev)
+        cudaEventDestroy(e);
+    for (cudaEvent_t e : h->cev)
+        if (e)
+            cudaEventDestroy(e);
     for (void *p : h->allocs)
         cudaFree(p);
     if (h->h_norm)
@@ -358,7 +382,25 @@ static void enqueue_up(bmg_solver *h, int l, bool fused, const double *f, const 
 
 // Enqueue one V(nu1,nu2) cycle (fig:vcycle_flowchart; DESIGN §3 c9) on s.
 // A fused level's iterate goes U -> T on the down leg and T -> U on the up leg.
-static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream_t s)
+// bmg_timing: the next free (start, end) event pair
+static bool next_events(bmg_solver *h, cudaEvent_t *e)
+{
+    while (h->tev.size() < h->tev_used + 2) {
+        cudaEvent_t ev;
+        if (cudaEventCreate(&ev) != cudaSuccess)
+            return false;
+        h->tev.push_back(ev);
+    }
+    e[0] = h->tev[h->tev_used];
+    e[1] = h->tev[h->tev_used + 1];
+    h->tev_used += 2;
+    return true;
+}
+
+// rec (bmg_timing): an event pair recorded around the level-0 down leg (external
+// event-record nodes when captured)
+static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream_t s,
+                         const cudaEvent_t *rec = nullptr)
 {
     int n = 0;
     const int L = h->L;
@@ -368,7 +410,11 @@ static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream
     for (int l = 0; l + 1 < L; l++) {
         double *T = l < 32 ? h->fplan.tmp[l] : nullptr;
         fz[l] = T && use_fused(h, l, F(l), U(l), T);
+        if (rec && l == 0)
+            cudaEventRecordWithFlags(rec[0], s, cudaEventRecordExternal);
         enqueue_down(h, l, fz[l], F(l), U(l), fz[l] ? T : U(l), h->lv[l + 1].f, h->lv[l + 1].u, s, &n);
+        if (rec && l == 0)
+            cudaEventRecordWithFlags(rec[1], s, cudaEventRecordExternal);
     }
     {
         Level &c = h->lv[L - 1];
@@ -380,31 +426,61 @@ static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream
     return n;
 }
 
-static bmg_status_t get_graph(bmg_solver *h, const double *f, double *x, cudaGraphExec_t *out)
+// The cycle's graph for (f, x).  timed: the variant with the two event-record
+// nodes of bmg_timing (their events are re-pointed before every launch).
+static bmg_status_t get_graph(bmg_solver *h, const double *f, double *x, bool timed, cudaGraphExec_t *out)
 {
     auto key = std::make_pair((const void *)f, (const void *)x);
-    auto it = h->graphs.find(key);
-    if (it != h->graphs.end()) {
-        *out = it->second;
+    auto &cache = timed ? h->tgraphs : h->graphs;
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *out = it->second.ex;
         return BMG_OK;
+    }
+    if (timed && !h->cev[0]) {
+        CK(cudaEventCreate(&h->cev[0]));
+        CK(cudaEventCreate(&h->cev[1]));
     }
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
-    int n = enqueue_cycle(h, f, x, h->cap);
+    int n = enqueue_cycle(h, f, x, h->cap, timed ? h->cev : nullptr);
     cudaError_t e = cudaStreamEndCapture(h->cap, &g);
     if (e != cudaSuccess)
         return fail(BMG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-    cudaGraphExec_t ex;
-    CK(cudaGraphInstantiate(&ex, g, 0));
-    cudaGraphDestroy(g);
-    h->kernels_per_cycle = n;
-    if (h->graphs.size() > 16) {  // bound the cache
-        for (auto &kv : h->graphs)
-            cudaGraphExecDestroy(kv.second);
-        h->graphs.clear();
+    GraphRec gr;
+    gr.g = g;
+    if (timed) {
+        size_t nn = 0;
+        CK(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType ty;
+            CK(cudaGraphNodeGetType(nd, &ty));
+            if (ty != cudaGraphNodeTypeEventRecord)
+                continue;
+            cudaEvent_t ev;
+            CK(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+            for (int k = 0; k < 2; k++)
+                if (ev == h->cev[k])
+                    gr.ev_node[k] = nd;
+        }
+        if (!gr.ev_node[0] || !gr.ev_node[1])
+            return fail(BMG_ECUDA, "timed graph: event-record nodes not found");
     }
-    h->graphs[key] = ex;
-    *out = ex;
+    CK(cudaGraphInstantiate(&gr.ex, g, 0));
+    if (!timed) {
+        cudaGraphDestroy(g);
+        gr.g = nullptr;
+    }
+    h->kernels_per_cycle = n;
+    if (cache.size() > 16) {  // bound the cache
+        for (auto &kv : cache)
+            kv.second.destroy();
+        cache.clear();
+    }
+    cache[key] = gr;
+    *out = gr.ex;
     return BMG_OK;
 }
 
@@ -420,9 +496,44 @@ bmg_status_t bmg_vcycle(bmg_solver_t h, const double *rhs, double *x, int ncycle
         return rc == BMG_OK ? rc : fail(rc, err);
     }
     cudaGraphExec_t ex;
-    TRY(get_graph(h, rhs, x, &ex));
-    for (int k = 0; k < ncycles; k++)
+    TRY(get_graph(h, rhs, x, h->timing, &ex));
+    const GraphRec &gr = (h->timing ? h->tgraphs : h->graphs)[std::make_pair((const void *)rhs, (const void *)x)];
+    for (int k = 0; k < ncycles; k++) {
+        if (h->timing) {  // a fresh event pair for this launch's level-0 down leg
+            cudaEvent_t ev[2];
+            if (!next_events(h, ev))
+                return fail(BMG_ECUDA, "bmg_timing: cudaEventCreate failed");
+            CK(cudaGraphExecEventRecordNodeSetEvent(ex, gr.ev_node[0], ev[0]));
+            CK(cudaGraphExecEventRecordNodeSetEvent(ex, gr.ev_node[1], ev[1]));
+        }
         CK(cudaGraphLaunch(ex, (cudaStream_t)cuda_stream));
+    }
+    return BMG_OK;
+}
+
+bmg_status_t bmg_timing(bmg_solver_t h, int enable)
+{
+    if (!h || h->dist)
+        return fail(BMG_EINVAL, "bmg_timing: null or distributed handle");
+    h->timing = enable != 0;
+    h->tev_used = 0;
+    return BMG_OK;
+}
+
+bmg_status_t bmg_timing_read(bmg_solver_t h, double *ms_total, int *launches)
+{
+    if (!h || h->dist || !ms_total || !launches)
+        return fail(BMG_EINVAL, "bmg_timing_read: bad arguments");
+    double tot = 0.0;
+    for (size_t i = 0; i + 1 < h->tev_used; i += 2) {
+        CK(cudaEventSynchronize(h->tev[i + 1]));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->tev[i], h->tev[i + 1]));
+        tot += ms;
+    }
+    *ms_total = tot;
+    *launches = (int)(h->tev_used / 2);
+    h->tev_used = 0;
     return BMG_OK;
 }
 

@@ -201,6 +201,27 @@ def test_determinism_and_graph_reuse():
     s.close()
 
 
+def test_timing_hook_same_iterate():
+    """bmg_timing (bench.py's roofline timing) replays the same cycle: bitwise the
+    same iterate as the plain graph, one recorded level-0 down launch per cycle."""
+    n = 255
+    s = bmg.Solver(P.workload("checker", n, n))
+    f = s.grid(P.field_uniform(n, n, seed=3))
+    x0 = P.field_uniform(n, n, seed=4)
+    xa, xb = s.grid(x0), s.grid(x0)
+    s.vcycle(f, xa, 4)
+    bmg.bmg_timing(s.h, True)
+    s.vcycle(f, xb, 4)
+    ms, nl = bmg.bmg_timing_read(s.h)
+    assert nl == 4 and ms > 0.0
+    s.vcycle(f, xb, 0)
+    assert bmg.bmg_timing_read(s.h) == (0.0, 0)
+    bmg.bmg_timing(s.h, False)
+    torch.cuda.synchronize()
+    assert torch.equal(xa, xb)
+    s.close()
+
+
 def test_vcycle_host_matches_device():
     n = 63
     st = P.workload("lognormal", n, n)
