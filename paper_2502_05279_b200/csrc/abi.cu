@@ -3,6 +3,7 @@
 // single-step entry points used by the parity tests.
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <map>
@@ -63,6 +64,10 @@ struct Level {
 
 long long round_pitch(int nx) { return ((long long)nx + 2 + 31) / 32 * 32; }
 
+// Levels with at most this many unknowns (and all coarser ones) run in the
+// single-CTA tail kernel in fused mode.
+constexpr long long TAIL_POINTS = 4096;
+
 }  // namespace
 
 struct GraphRec {
@@ -97,6 +102,8 @@ struct bmg_solver {
     bmg_solver_t dist_inner = nullptr;  // its replicated coarse solver (owned by dist)
     long long dist_rows_total = 0;      // doubles of a level-0 rhs/x array of this handle
     int dist_local_ranks = 1;
+    int tail_l0 = 1 << 30;            // first level of the tail kernel (none: > L)
+    TailPlan *tail = nullptr;         // its device-side plan
     bool timing = false;              // bmg_timing: timed graph variant, event pair per launch
     std::vector<cudaEvent_t> tev;     // event pairs (start, end) per recorded launch
     size_t tev_used = 0;
@@ -283,8 +290,39 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
     if (herr & ERR_PIVOT)
         return fail(BMG_ENOTSPD, "coarsest-level Cholesky pivot <= 0");
     CK(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
-    // fused streaming plan + ping-pong partner of u for every fused level
-    for (int l = 0; l + 1 < h->L && l < 32; l++) {
+    // tail kernel: levels from the first with <= TAIL_POINTS unknowns down to the coarsest
+    if (h->prm.fused && h->L >= 2 && h->L <= 32) {
+        long long lim = TAIL_POINTS;
+        if (const char *e = getenv("BMG_TAIL_POINTS"))  // tuning knob (bench sweeps)
+            lim = atoll(e);
+        int l0 = h->L - 1;
+        while (l0 > 0 && (long long)h->lv[l0 - 1].nx * h->lv[l0 - 1].ny <= lim)
+            l0--;
+        if (l0 <= h->L - 2) {
+            TailPlan tp;
+            memset(&tp, 0, sizeof(tp));
+            tp.l0 = l0;
+            tp.L = h->L;
+            tp.nu1 = h->prm.nu1;
+            tp.nu2 = h->prm.nu2;
+            tp.chol = h->chol;
+            for (int l = l0; l < h->L; l++) {
+                tp.lv[l].A = h->lv[l].op();
+                if (l + 1 < h->L)
+                    tp.lv[l].ci = h->civ(l);
+                tp.lv[l].f = h->lv[l].f;
+                tp.lv[l].u = h->lv[l].u;
+                tp.lv[l].r = h->lv[l].r;
+            }
+            double *d = nullptr;
+            TRY(dalloc(h, &d, sizeof(TailPlan) / sizeof(double) + 1));
+            CK(cudaMemcpyAsync(d, &tp, sizeof(TailPlan), cudaMemcpyHostToDevice, s));
+            h->tail = (TailPlan *)d;
+            h->tail_l0 = l0;
+        }
+    }
+    // fused streaming plan + ping-pong partner of u for every fused level above the tail
+    for (int l = 0; l + 1 < h->L && l < 32 && l < h->tail_l0; l++) {
         Level &v = h->lv[l];
         if (!h->prm.fused)
             break;
@@ -407,7 +445,8 @@ static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream
     auto F = [&](int l) { return l == 0 ? f0 : (const double *)h->lv[l].f; };
     auto U = [&](int l) { return l == 0 ? u0 : h->lv[l].u; };
     bool fz[64];
-    for (int l = 0; l + 1 < L; l++) {
+    const int lt = h->tail_l0 < L ? h->tail_l0 : L - 1;  // levels >= lt: tail kernel / coarse solve
+    for (int l = 0; l < lt; l++) {
         double *T = l < 32 ? h->fplan.tmp[l] : nullptr;
         fz[l] = T && use_fused(h, l, F(l), U(l), T);
         if (rec && l == 0)
@@ -416,12 +455,15 @@ static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream
         if (rec && l == 0)
             cudaEventRecordWithFlags(rec[1], s, cudaEventRecordExternal);
     }
-    {
+    if (h->tail) {
+        launch_tail(h->tail, h->nco, F(0), U(0), s);
+        n += 1;
+    } else {
         Level &c = h->lv[L - 1];
         launch_coarse_solve(c.op(), h->chol, F(L - 1), U(L - 1), s);
         n += 1;
     }
-    for (int l = L - 2; l >= 0; l--)
+    for (int l = lt - 1; l >= 0; l--)
         enqueue_up(h, l, fz[l], F(l), fz[l] ? h->fplan.tmp[l] : U(l), h->lv[l + 1].u, U(l), s, &n);
     return n;
 }

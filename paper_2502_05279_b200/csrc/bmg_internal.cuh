@@ -66,6 +66,22 @@ __device__ __forceinline__ Row9 load_row9(const Op &A, long long p)
     return a;
 }
 
+// 1/b for b > 0 normal, entirely on the FP64 FMA pipe (no MUFU.RCP64H on the
+// XU pipe, whose throughput bounded the streaming kernels).  Seed: exponent/
+// mantissa reflection 0x7FE0...0 - bits(b), relative error <= 1/8; six Newton
+// steps (2^-3 -> 2^-96, then a final one to settle rounding) give 1/b within
+// 1 ulp.  Every GPU relaxation (per-step, tail and fused kernels) forms
+// u = (f - sum) * rcp_pos(a_pp), so all paths agree bitwise; the oracle divides
+// (difference <= ~2 ulp per update, inside the DESIGN §7 tolerances).
+__device__ __forceinline__ double rcp_pos(double b)
+{
+    double r = __longlong_as_double(0x7FE0000000000000LL - __double_as_longlong(b));
+#pragma unroll
+    for (int i = 0; i < 5; i++)
+        r = fma(r, fma(-b, r, 1.0), r);
+    return fma(r, fma(-b, r, 1.0), r);
+}
+
 // ---- launchers (kernels.cu) ----
 void launch_ingest(int nx, int ny, int kind, long long pitch, const double *const src[5], double *const dst[5],
                    int *err, cudaStream_t s, int j0, int j1);
@@ -85,6 +101,20 @@ void launch_resid_norm(const Op &A, const double *f, const double *u, double *r_
                        double *result, cudaStream_t s);
 void launch_norm(const Op &A, const double *g, double *partials, double *result, cudaStream_t s);
 void launch_zero_interior(const Op &A, double *x, cudaStream_t s);
+
+// Small levels l0..L-1 of the cycle in one single-CTA launch (k_tail).  Lives in
+// device memory (filled once at setup); level 0's f/u are launch arguments.
+struct TailLevel {
+    Op A;
+    CIv ci;                // weights to level l+1 (unused on L-1)
+    double *f, *u, *r;     // level arrays (l > 0); r: residual scratch
+};
+struct TailPlan {
+    int l0, L, nu1, nu2;
+    const double *chol;    // coarsest Cholesky factor
+    TailLevel lv[32];
+};
+void launch_tail(const TailPlan *tp_dev, int ncoarse, const double *f0, double *u0, cudaStream_t s);
 
 constexpr int NORM_BLOCKS = 592;  // 4 x 148 SMs; fixed so the reduction tree is fixed
 

@@ -24,8 +24,38 @@ __device__ __forceinline__ double offdiag(const Row9 &a, const double *__restric
     return s;
 }
 
-// 5-point levels: colour (i+j)&1; updates u_p <- (f_p - sum_{q!=p} a_pq u_q)/a_pp
-// One thread per point of the colour (DESIGN §3 c6).
+// Per-point bodies, shared by the per-step kernels below and the tail kernel.
+// 5-point levels: colour (i+j)&1; updates u_p <- (f_p - sum_{q!=p} a_pq u_q)/a_pp (DESIGN §3 c6).
+__device__ __forceinline__ void relax5_pt(const Op &A, const double *__restrict__ f, double *__restrict__ u, int i,
+                                          int j)
+{
+    long long P = A.pitch, p = j * P + i;
+    double o = A.O[p], w = A.W[p], e = A.W[p + 1], s = A.S[p], n = A.S[p + P];
+    double acc = s * u[p - P];
+    acc += w * u[p - 1];
+    acc += e * u[p + 1];
+    acc += n * u[p + P];
+    u[p] = (f[p] - acc) * rcp_pos(o);
+}
+
+__device__ __forceinline__ void relax9_pt(const Op &A, const double *__restrict__ f, double *__restrict__ u, int i,
+                                          int j)
+{
+    long long P = A.pitch, p = j * P + i;
+    Row9 a = load_row9(A, p);
+    u[p] = (f[p] - offdiag(a, u, p, P)) * rcp_pos(a.o);
+}
+
+// r_p = f_p - (A u)_p at an interior point
+__device__ __forceinline__ double residual_pt(const Op &A, const double *__restrict__ f,
+                                              const double *__restrict__ u, int i, int j)
+{
+    long long P = A.pitch, p = j * P + i;
+    Row9 a = load_row9(A, p);
+    return f[p] - (a.o * u[p] + offdiag(a, u, p, P));
+}
+
+// 5-point: one thread per point of the colour.
 __global__ void k_relax5(Op A, const double *__restrict__ f, double *__restrict__ u, int colour)
 {
     int j = blockIdx.y * blockDim.y + threadIdx.y + 1;
@@ -35,13 +65,7 @@ __global__ void k_relax5(Op A, const double *__restrict__ f, double *__restrict_
     int i = i0 + 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     if (i > A.nx)
         return;
-    long long P = A.pitch, p = j * P + i;
-    double o = A.O[p], w = A.W[p], e = A.W[p + 1], s = A.S[p], n = A.S[p + P];
-    double acc = s * u[p - P];
-    acc += w * u[p - 1];
-    acc += e * u[p + 1];
-    acc += n * u[p + P];
-    u[p] = (f[p] - acc) / o;
+    relax5_pt(A, f, u, i, j);
 }
 
 // 9-point levels: colour (i&1) + 2(j&1), 4 colours.
@@ -53,9 +77,7 @@ __global__ void k_relax9(Op A, const double *__restrict__ f, double *__restrict_
     int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x) + ((colour & 1) ? 1 : 2);
     if (i > A.nx)
         return;
-    long long P = A.pitch, p = j * P + i;
-    Row9 a = load_row9(A, p);
-    u[p] = (f[p] - offdiag(a, u, p, P)) / a.o;
+    relax9_pt(A, f, u, i, j);
 }
 
 void launch_relax(const Op &A, const double *f, double *u, int nsweeps, cudaStream_t s, int *nlaunch)
@@ -86,12 +108,7 @@ __global__ void k_residual(Op A, const double *__restrict__ f, const double *__r
     if (i > A.nx + 1 || j > A.ny + 1)
         return;
     long long P = A.pitch, p = j * P + i;
-    if (i == 0 || j == 0 || i > A.nx || j > A.ny) {
-        r[p] = 0.0;
-        return;
-    }
-    Row9 a = load_row9(A, p);
-    r[p] = f[p] - (a.o * u[p] + offdiag(a, u, p, P));
+    r[p] = (i == 0 || j == 0 || i > A.nx || j > A.ny) ? 0.0 : residual_pt(A, f, u, i, j);
 }
 
 void launch_residual(const Op &A, const double *f, const double *u, double *r, cudaStream_t s)
@@ -107,20 +124,9 @@ void launch_residual(const Op &A, const double *f, const double *u, double *r, c
 // One thread per coarse point, all (ncx+2)(ncy+2) written (ring 0).
 // If uc != nullptr it is zeroed at the same points (the coarse correction's
 // zero start, DESIGN §3 c9), saving a separate memset launch.
-__global__ void k_restrict(Op A, CIv ci, const double *__restrict__ q, double *__restrict__ qc, double *__restrict__ uc)
+__device__ __forceinline__ double restrict_pt(const Op &A, const CIv &ci, const double *__restrict__ q, int I, int J)
 {
-    int ncx = A.nx / 2, ncy = A.ny / 2;
-    int I = blockIdx.x * blockDim.x + threadIdx.x;
-    int J = blockIdx.y * blockDim.y + threadIdx.y;
-    if (I > ncx + 1 || J > ncy + 1)
-        return;
     long long C = ci.pitch, c = J * C + I;
-    if (uc)
-        uc[c] = 0.0;
-    if (I == 0 || J == 0 || I > ncx || J > ncy) {
-        qc[c] = 0.0;
-        return;
-    }
     long long P = A.pitch, p = (2 * J) * P + 2 * I;
     double v = ci.w[CI_LNE][c] * q[p - P - 1];
     v += ci.w[CI_LA][c] * q[p - P];
@@ -131,7 +137,27 @@ __global__ void k_restrict(Op A, CIv ci, const double *__restrict__ q, double *_
     v += ci.w[CI_LSE][c + C] * q[p + P - 1];
     v += ci.w[CI_LB][c + C] * q[p + P];
     v += ci.w[CI_LSW][c + C + 1] * q[p + P + 1];
-    qc[c] = v;
+    return v;
+}
+
+// coarse point (I, J), 0 <= I <= ncx+1, 0 <= J <= ncy+1: qc (0 on the ring) and uc = 0
+__device__ __forceinline__ void restrict_store(const Op &A, const CIv &ci, const double *__restrict__ q,
+                                               double *__restrict__ qc, double *__restrict__ uc, int I, int J)
+{
+    int ncx = A.nx / 2, ncy = A.ny / 2;
+    long long c = J * ci.pitch + I;
+    if (uc)
+        uc[c] = 0.0;
+    qc[c] = (I == 0 || J == 0 || I > ncx || J > ncy) ? 0.0 : restrict_pt(A, ci, q, I, J);
+}
+
+__global__ void k_restrict(Op A, CIv ci, const double *__restrict__ q, double *__restrict__ qc, double *__restrict__ uc)
+{
+    int I = blockIdx.x * blockDim.x + threadIdx.x;
+    int J = blockIdx.y * blockDim.y + threadIdx.y;
+    if (I > A.nx / 2 + 1 || J > A.ny / 2 + 1)
+        return;
+    restrict_store(A, ci, q, qc, uc, I, J);
 }
 
 void launch_restrict(const Op &A, const CIv &ci, const double *r, double *fc, double *uc, cudaStream_t s)
@@ -140,15 +166,10 @@ void launch_restrict(const Op &A, const CIv &ci, const double *r, double *fc, do
     k_restrict<<<g, b, 0, s>>>(A, ci, r, fc, uc);
 }
 
-// u += P e (DESIGN §3 c7), one thread per fine interior point; e's ring is 0.
-__global__ void k_interp_add(Op A, CIv ci, const double *__restrict__ e, double *__restrict__ u)
+// (P e) at fine interior point (i, j) (DESIGN §3 c7); e's ring is 0.
+__device__ __forceinline__ double interp_pt(const CIv &ci, const double *__restrict__ e, int i, int j)
 {
-    int i = blockIdx.x * blockDim.x + threadIdx.x + 1;
-    int j = blockIdx.y * blockDim.y + threadIdx.y + 1;
-    if (i > A.nx || j > A.ny)
-        return;
     long long C = ci.pitch;
-    long long p = j * A.pitch + i;
     int I = (i + 1) >> 1, J = (j + 1) >> 1;  // storage index of X/Y/Z weights; C point: (i/2, j/2)
     long long c = J * C + I;
     double s;
@@ -168,7 +189,17 @@ __global__ void k_interp_add(Op A, CIv ci, const double *__restrict__ e, double 
         s += ci.w[CI_LNW][c] * e[c - 1];
         s += ci.w[CI_LNE][c] * e[c];
     }
-    u[p] += s;
+    return s;
+}
+
+// u += P e, one thread per fine interior point.
+__global__ void k_interp_add(Op A, CIv ci, const double *__restrict__ e, double *__restrict__ u)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    int j = blockIdx.y * blockDim.y + threadIdx.y + 1;
+    if (i > A.nx || j > A.ny)
+        return;
+    u[j * A.pitch + i] += interp_pt(ci, e, i, j);
 }
 
 void launch_interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s)
@@ -266,9 +297,10 @@ void launch_norm(const Op &A, const double *g, double *partials, double *result,
 // u = A_L^{-1} f with the setup Cholesky factor: forward then backward
 // substitution (fig:vcycle_flowchart "Cholesky"), one CTA, the
 // right-hand side staged in shared memory (n <= 6144).
-__global__ void k_coarse_solve(Op A, const double *__restrict__ Lf, const double *__restrict__ f, double *__restrict__ u)
+// b: n doubles of shared memory; all threads of the CTA call this.
+__device__ __forceinline__ void coarse_solve_cta(const Op &A, const double *__restrict__ Lf,
+                                                 const double *__restrict__ f, double *__restrict__ u, double *b)
 {
-    extern __shared__ double b[];
     int n = A.nx * A.ny;
     for (int p = threadIdx.x; p < n; p += blockDim.x)
         b[p] = f[(p / A.nx + 1) * A.pitch + p % A.nx + 1];
@@ -295,11 +327,106 @@ __global__ void k_coarse_solve(Op A, const double *__restrict__ Lf, const double
         u[(p / A.nx + 1) * A.pitch + p % A.nx + 1] = b[p];
 }
 
+__global__ void k_coarse_solve(Op A, const double *__restrict__ Lf, const double *__restrict__ f, double *__restrict__ u)
+{
+    extern __shared__ double b[];
+    coarse_solve_cta(A, Lf, f, u, b);
+}
+
 void launch_coarse_solve(const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s)
 {
     int n = A.nx * A.ny;
     int threads = n < 32 ? 32 : (n < 1024 ? ((n + 31) / 32) * 32 : 1024);
     k_coarse_solve<<<1, threads, sizeof(double) * n, s>>>(A, Lf, f, u);
+}
+
+// ---------------------------------------------------------------- tail kernel
+// The small levels l0..L-1 of a V-cycle in ONE single-CTA launch:
+// down legs (nu1 multicolour sweeps, residual, restriction + zero coarse start),
+// the Cholesky coarse solve, up legs (u += P e, nu2 sweeps), the steps ordered
+// by __syncthreads.  Same per-point arithmetic as the per-step kernels above
+// (and within one colour GS updates are independent), so the iterate is
+// bitwise that of the per-step path.  Replaces ~4 launches per small level,
+// each bounded by launch latency rather than by its few thousand points.
+template <int KIND>
+__device__ __forceinline__ void tail_relax(const Op &A, const double *f, double *u, int nsweeps)
+{
+    const int nt = blockDim.x;
+    for (int sw = 0; sw < nsweeps; sw++) {
+        if (KIND == 5) {
+            const int half = A.nx / 2 + 1, cnt = half * A.ny;
+            for (int c = 0; c < 2; c++) {
+                for (int k = threadIdx.x; k < cnt; k += nt) {
+                    const int j = k / half + 1, i = (((1 + j) & 1) == c ? 1 : 2) + 2 * (k % half);
+                    if (i <= A.nx)
+                        relax5_pt(A, f, u, i, j);
+                }
+                __syncthreads();
+            }
+        } else {
+            const int hx = A.nx / 2 + 1, hy = A.ny / 2 + 1, cnt = hx * hy;
+            for (int c = 0; c < 4; c++) {
+                for (int k = threadIdx.x; k < cnt; k += nt) {
+                    const int j = 2 * (k / hx) + ((c >> 1) ? 1 : 2), i = 2 * (k % hx) + ((c & 1) ? 1 : 2);
+                    if (i <= A.nx && j <= A.ny)
+                        relax9_pt(A, f, u, i, j);
+                }
+                __syncthreads();
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024, 1) k_tail(const TailPlan *__restrict__ tp, const double *f0, double *u0)
+{
+    extern __shared__ double b[];
+    const int l0 = tp->l0, L = tp->L, nt = blockDim.x;
+    auto F = [&](int l) { return l == 0 ? f0 : (const double *)tp->lv[l].f; };
+    auto U = [&](int l) { return l == 0 ? u0 : tp->lv[l].u; };
+    for (int l = l0; l + 1 < L; l++) {
+        const Op A = tp->lv[l].A;
+        const CIv ci = tp->lv[l].ci;
+        const double *f = F(l);
+        double *u = U(l), *r = tp->lv[l].r;
+        if (A.kind == 5)
+            tail_relax<5>(A, f, u, tp->nu1);
+        else
+            tail_relax<9>(A, f, u, tp->nu1);
+        const int wx = A.nx + 2, cnt = wx * (A.ny + 2);
+        for (int k = threadIdx.x; k < cnt; k += nt) {
+            const int j = k / wx, i = k % wx;
+            r[(long long)j * A.pitch + i] =
+                (i == 0 || j == 0 || i > A.nx || j > A.ny) ? 0.0 : residual_pt(A, f, u, i, j);
+        }
+        __syncthreads();
+        const int cx = A.nx / 2 + 2, ccnt = cx * (A.ny / 2 + 2);
+        for (int k = threadIdx.x; k < ccnt; k += nt)
+            restrict_store(A, ci, r, tp->lv[l + 1].f, tp->lv[l + 1].u, k % cx, k / cx);
+        __syncthreads();
+    }
+    coarse_solve_cta(tp->lv[L - 1].A, tp->chol, F(L - 1), U(L - 1), b);
+    __syncthreads();
+    for (int l = L - 2; l >= l0; l--) {
+        const Op A = tp->lv[l].A;
+        const CIv ci = tp->lv[l].ci;
+        double *u = U(l);
+        const double *e = U(l + 1);
+        const int cnt = A.nx * A.ny;
+        for (int k = threadIdx.x; k < cnt; k += nt) {
+            const int j = k / A.nx + 1, i = k % A.nx + 1;
+            u[(long long)j * A.pitch + i] += interp_pt(ci, e, i, j);
+        }
+        __syncthreads();
+        if (A.kind == 5)
+            tail_relax<5>(A, F(l), u, tp->nu2);
+        else
+            tail_relax<9>(A, F(l), u, tp->nu2);
+    }
+}
+
+void launch_tail(const TailPlan *tp_dev, int ncoarse, const double *f0, double *u0, cudaStream_t s)
+{
+    k_tail<<<1, 1024, sizeof(double) * (ncoarse > 0 ? ncoarse : 1), s>>>(tp_dev, f0, u0);
 }
 
 }  // namespace bmg

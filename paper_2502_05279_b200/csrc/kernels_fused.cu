@@ -54,16 +54,21 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, uint32_t bytes)
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
 
+// try_wait suspend-time hint (ns): a waiting warp sleeps until the phase
+// completes (or the hint expires) instead of re-polling and taking issue slots.
+#ifndef BMG_WAIT_HINT
+#define BMG_WAIT_HINT 0x989680
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity)
 {
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_LOOP:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@!P1 bra WAIT_LOOP;\n"
         "}\n" ::"r"(smem_u32(b)),
-        "r"(parity)
+        "r"(parity), "r"(BMG_WAIT_HINT)
         : "memory");
 }
 
@@ -100,22 +105,26 @@ __device__ __forceinline__ void tma_3d(void *dst, const CUtensorMap *m, int x, i
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
 // ------------------------------------------------------------------ configuration
-constexpr int DC = 4;  // coarse-row prefetch distance (row steps); < 6 for safe ring reuse
+constexpr int DC = 4;  // coarse-row prefetch distance (row steps), up leg (4-slot ring)
+constexpr int DC_DN = 3;  // down leg (3-slot weight ring: 2 slots in use + 1 in flight)
 constexpr int CH = 4;  // coarse halo columns on each side of a strip
 constexpr int NSLOT = 32;  // slots of each task group's step-completion ring
 
 // streamed arrays: index into the shared-memory array blocks
 enum { A_U = 0, A_F = 1, A_O = 2, A_W = 3, A_S = 4, A_SW = 5, A_NW = 6 };
 
-template <int KIND, int NS, int WD, int D, bool UP, int PPT>
+template <int KIND, int NS, int WD, int D, bool UP, int PPT, int E>
 struct Cfg {
-    static constexpr int NA = KIND == 5 ? 5 : 7;
+    static constexpr int NA = KIND == 5 ? 5 : 7;                // streamed arrays
+    static constexpr int NM = NA + 1;                           // main-ring arrays: + 1/O
+    static constexpr int A_DI = NA;                             // main-ring index of 1/O
+    static constexpr int CSL = UP ? 4 : 3;                      // coarse-row ring slots
     static constexpr int PASSES = KIND == 5 ? NS : 2 * NS;      // colour passes (x halo shrink)
     static constexpr int H0 = UP ? PASSES : PASSES + 2;         // + residual + restriction
     static constexpr int H = ((H0 < 2 ? 2 : H0) + 1) & ~1;      // even (16-byte TMA alignment)
     static constexpr int TX = WD - 2 * H;                      // output columns (multiple of 4)
     static constexpr int HW = WD / 2;                          // half row (one parity)
-    static constexpr int RM = UP ? 2 * NS + 3 : 2 * NS + 4;     // main (split) ring rows
+    static constexpr int RM = (UP ? 2 * NS + 3 : 2 * NS + 4) + E;  // main (split) ring rows; E = extra slack
     static constexpr int SD = D + 1;                           // staging (natural) ring rows
     static constexpr int AM = RM * WD, AS = SD * WD;           // doubles per array block
     static constexpr int WC = (TX / 2 + 2 * CH + 15) / 16 * 16;  // coarse box width (128-B rows)
@@ -126,7 +135,7 @@ struct Cfg {
     static constexpr int NTW = NG * NPG;                       // worker threads
     static constexpr int NT = NTW + 32;                        // + one TMA producer warp
     static constexpr size_t SMEM_DBL =
-        (size_t)NA * (AM + AS) + (UP ? 4 * (size_t)WC : 4 * (size_t)WD) + 32 * (size_t)WC;
+        (size_t)NM * AM + (size_t)NA * AS + (UP ? 4 * (size_t)WC : 4 * (size_t)WD) + 8 * CSL * (size_t)WC;
     static constexpr size_t SMEM = SMEM_DBL * 8 + (SD + 4 + (size_t)NG * NSLOT) * 8;
     static_assert(TX % 4 == 0 && TX > 0, "strip width");
     static_assert(NPG % 32 == 0, "task groups must be whole warps");
@@ -158,10 +167,10 @@ struct Rings {
             "{\n"
             ".reg .pred P1;\n"
             "RWAIT:\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
             "@!P1 bra RWAIT;\n"
             "}\n" ::"r"(at(r, t)),
-            "r"(par)
+            "r"(par), "r"(BMG_WAIT_HINT)
             : "memory");
     }
     // end of step t for one warp: arrive on rings a, b, c (-1: none)
@@ -218,8 +227,9 @@ __device__ __forceinline__ Col col_of(int h, int par)
 }
 
 // Loads of the operands of one point (row bases b0/bm/bp = slot*WD of rows r, r-1, r+1),
-// off-diagonal terms in fig:stencil_operator order SW,S,SE,W,E,NW,N,NE.
-template <int KIND, int AM>
+// off-diagonal terms in fig:stencil_operator order SW,S,SE,W,E,NW,N,NE; `o` is
+// main-ring array OI (A_O: the diagonal; the colour passes load 1/a_pp instead).
+template <int KIND, int AM, int OI>
 struct PointOps {
     double a[8], u[8], f, o, uc;
     __device__ __forceinline__ void load(const double *sm, int b0, int bm, int bp, const Col &c, bool with_uc)
@@ -252,7 +262,7 @@ struct PointOps {
             u[7] = sm[A_U * AM + bp + c.right];
         }
         f = sm[A_F * AM + b0 + c.same];
-        o = sm[A_O * AM + b0 + c.same];
+        o = sm[OI * AM + b0 + c.same];
         if (with_uc)
             uc = sm[A_U * AM + b0 + c.same];
     }
@@ -266,27 +276,6 @@ struct PointOps {
         return acc;
     }
 };
-
-// a / b for b > 0 normal, entirely on the FP64 FMA pipe.  The IEEE division
-// seeds its reciprocal with MUFU.RCP64H on the XU pipe, whose throughput (not
-// HBM) bounded these kernels (ncu: XU > 100% of peak, FP64 FMA pipe 8%).  Seed:
-// exponent/mantissa reflection 0x7FE0...0 - bits(b), relative error <= 1/8;
-// five Newton steps (error 2^-3 -> 2^-96) and one residual correction give a
-// quotient within 1 ulp of a/b (parity tolerance).
-#ifndef BMG_DIV_NEWTON
-#define BMG_DIV_NEWTON 1
-#endif
-__device__ __forceinline__ double div_pos(double a, double b)
-{
-    if (!BMG_DIV_NEWTON)
-        return a / b;
-    double r = __longlong_as_double(0x7FE0000000000000LL - __double_as_longlong(b));
-#pragma unroll
-    for (int i = 0; i < 5; i++)
-        r = fma(r, fma(-b, r, 1.0), r);
-    const double q = a * r;
-    return fma(fma(-b, q, a), r, q);
-}
 
 // Per-thread column data for its PPT pairs, both parities (loop invariant).
 // Neighbour offsets of a split row never leave the row (par 0: left/right in
@@ -316,16 +305,20 @@ __device__ __forceinline__ Cols<PPT> make_cols(int m, int xl, int nx)
 
 // One colour pass (c6: u <- (f - sum_{q!=p} a_pq u_q) / a_pp) on row r for this
 // thread's PPT pairs, column parity PAR.  Points outside [1,nx] are computed but not stored.
+// The division is a multiplication by 1/a_pp (rcp_pos, bmg_internal.cuh), formed
+// once per point and row pass by the split task: it keeps the
+// reciprocal's dependent FP64 chain off the colour stages, whose latency bounds
+// the pipeline's row step.
 template <int KIND, int AM, int WD, int PPT, int PAR>
 __device__ __forceinline__ void colour_pass(double *sm, int s0, int sm1, int sp1, const Cols<PPT> &k)
 {
-    PointOps<KIND, AM> pt[PPT];
+    PointOps<KIND, AM, KIND == 5 ? 5 : 7> pt[PPT];
 #pragma unroll
     for (int p = 0; p < PPT; p++)
         pt[p].load(sm, s0 * WD, sm1 * WD, sp1 * WD, k.c[PAR][p], false);
 #pragma unroll
     for (int p = 0; p < PPT; p++) {
-        const double v = div_pos(pt[p].f - pt[p].offdiag(), pt[p].o);
+        const double v = (pt[p].f - pt[p].offdiag()) * pt[p].o;
         if (k.on[PAR][p])
             sm[A_U * AM + s0 * WD + k.c[PAR][p].same] = v;
     }
@@ -342,10 +335,23 @@ __device__ __forceinline__ void colour_pass(double *sm, int s0, int sm1, int sp1
 
 // De-interleave staging row (natural order, slot ss) into main ring row (slot s0)
 // for arrays [q0, q1): even columns to the first half, odd to the second.
-template <int NA, int AM, int WD, int PPT, int NPG>
+// DI: also form 1/a_pp (rcp_pos) into main-ring array NA.
+template <int NA, int AM, int WD, int PPT, int NPG, bool DI>
 __device__ __forceinline__ void split_row(double *smM, const double *smS, int ss, int s0, int q0, int q1, int m)
 {
     constexpr int HW = WD / 2;
+    if (DI) {
+        double2 v[PPT];
+#pragma unroll
+        for (int p = 0; p < PPT; p++)
+            v[p] = *reinterpret_cast<const double2 *>(smS + (ss * NA + A_O) * WD + 2 * (m + p * NPG));
+#pragma unroll
+        for (int p = 0; p < PPT; p++) {
+            double *row = smM + NA * AM + s0 * WD;
+            row[m + p * NPG] = rcp_pos(v[p].x);  // ring / out-of-range columns: never stored
+            row[HW + m + p * NPG] = rcp_pos(v[p].y);
+        }
+    }
 #pragma unroll
     for (int q = 0; q < 7; q++) {
         if (q < q0 || q >= q1)
@@ -364,18 +370,18 @@ __device__ __forceinline__ void split_row(double *smM, const double *smS, int ss
 }
 
 // ------------------------------------------------------------------ down kernel
-template <int KIND, int NS, int WD, int D, int PPT>
-__global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT, 1)
+template <int KIND, int NS, int WD, int D, int PPT, int E>
+__global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
     k_fused_down(FArgs a, const __grid_constant__ TMaps tmaps)
 {
-    using C = Cfg<KIND, NS, WD, D, false, PPT>;
+    using C = Cfg<KIND, NS, WD, D, false, PPT, E>;
     constexpr int NA = C::NA, H = C::H, TX = C::TX, WC = C::WC, HW = C::HW, NPG = C::NPG;
     constexpr int RM = C::RM, SD = C::SD, AM = C::AM, AS = C::AS;
     extern __shared__ __align__(128) double sm[];
-    double *smS = sm + NA * AM;                 // staging ring (natural rows)
+    double *smS = sm + C::NM * AM;              // staging ring (natural rows)
     double *sR = smS + NA * AS;                 // residual ring [4][WD], split
     double *sC = sR + 4 * WD;                   // weights ring [4][8][WC]
-    uint64_t *bar = (uint64_t *)(sC + 32 * WC); // SD staging + 4 coarse
+    uint64_t *bar = (uint64_t *)(sC + 8 * C::CSL * WC); // SD staging + 4 coarse
 
     const int nx = a.A.nx, ny = a.A.ny, ncx = a.ncx;
     const long long P = a.A.pitch, CP = a.ci.pitch;
@@ -441,9 +447,9 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT, 1)
     auto issue_coarse = [&](int t) {
         while (Knext <= Kend) {
             const int use = (Knext == Jlo) ? 2 * Jlo + 2 * NS + 4 : 2 * Knext + 2 * NS + 2;
-            if (use - DC > t)
+            if (use - DC_DN > t)
                 break;
-            const int slot = (Knext - Jlo) & 3;
+            const int slot = (Knext - Jlo) % C::CSL;
             uint64_t *b = &bar[SD + slot];
             mbar_arrive_tx(b, (uint32_t)(8 * WC * 8));
             tma_3d(sC + slot * 8 * WC, &tmaps.c, cxl, Knext - a.ci.roff, 0, b);
@@ -458,10 +464,10 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT, 1)
 
     // residual of row rr at the columns of parity e of this thread's pairs;
     // 0 off the interior (the restriction reads the ring as zeros)
-    auto resid_par = [&](int rr, int s0, int sm1, int sp1, auto E) {
-        constexpr int e = decltype(E)::value;
+    auto resid_par = [&](int rr, int s0, int sm1, int sp1, auto PARC) {
+        constexpr int e = decltype(PARC)::value;
         const bool rin = rr >= 1 && rr <= ny;
-        PointOps<KIND, AM> pt[PPT];
+        PointOps<KIND, AM, A_O> pt[PPT];
 #pragma unroll
         for (int p = 0; p < PPT; p++)
             pt[p].load(sm, s0 * WD, sm1 * WD, sp1 * WD, kc.c[e][p], true);
@@ -504,11 +510,12 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT, 1)
     };
     // restriction (fig:restrict_kernel) of coarse row J at the coarse points centred on columns 2h
     auto restrict_task = [&](int J) {
-        mbar_wait(&bar[SD + ((J - Jlo) & 3)], ((J - Jlo) >> 2) & 1);
-        mbar_wait(&bar[SD + ((J + 1 - Jlo) & 3)], ((J + 1 - Jlo) >> 2) & 1);
+        constexpr int CS = C::CSL;
+        mbar_wait(&bar[SD + (J - Jlo) % CS], ((J - Jlo) / CS) & 1);
+        mbar_wait(&bar[SD + (J + 1 - Jlo) % CS], ((J + 1 - Jlo) / CS) & 1);
         const double *rm = sR + ((2 * J - 1) & 3) * WD, *r0 = sR + ((2 * J) & 3) * WD,
                      *rp = sR + ((2 * J + 1) & 3) * WD;
-        const double *c0 = sC + ((J - Jlo) & 3) * 8 * WC, *c1 = sC + ((J + 1 - Jlo) & 3) * 8 * WC;
+        const double *c0 = sC + ((J - Jlo) % CS) * 8 * WC, *c1 = sC + ((J + 1 - Jlo) % CS) * 8 * WC;
 #pragma unroll
         for (int p = 0; p < PPT; p++) {
             const int h = m + p * NPG;
@@ -569,13 +576,13 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT, 1)
     int tm = 0, tsd = 0;  // main / staging ring slots of row t
     for (int t = lo; t <= tend; t++, tm = (tm + 1 == RM) ? 0 : tm + 1, tsd = (tsd + 1 == SD) ? 0 : tsd + 1) {
         if (grp >= G_SPLIT) {
-            rg.wait(R_SPLIT, t - 1);
+            rg.wait(R_SPLIT, t - 1 - E);
             if (t <= hi) {
                 mbar_wait(&bar[tsd], ((t - lo) / SD) & 1);
                 if (grp == G_SPLIT)
-                    split_row<NA, AM, WD, PPT, NPG>(sm, smS, tsd, tm, 0, QSPLIT, m);
+                    split_row<NA, AM, WD, PPT, NPG, false>(sm, smS, tsd, tm, 0, QSPLIT, m);
                 else
-                    split_row<NA, AM, WD, PPT, NPG>(sm, smS, tsd, tm, QSPLIT, NA, m);
+                    split_row<NA, AM, WD, PPT, NPG, true>(sm, smS, tsd, tm, QSPLIT, NA, m);
             }
         } else if (grp < NSG) {
             rg.wait(grp, t - 1);
@@ -616,18 +623,18 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT>::NT, 1)
 }
 
 // ------------------------------------------------------------------ up kernel
-template <int KIND, int NS, int WD, int D, int PPT>
-__global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT, 1)
+template <int KIND, int NS, int WD, int D, int PPT, int E>
+__global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
     k_fused_up(FArgs a, const __grid_constant__ TMaps tmaps)
 {
-    using C = Cfg<KIND, NS, WD, D, true, PPT>;
+    using C = Cfg<KIND, NS, WD, D, true, PPT, E>;
     constexpr int NA = C::NA, H = C::H, TX = C::TX, WC = C::WC, HW = C::HW, NPG = C::NPG;
     constexpr int RM = C::RM, SD = C::SD, AM = C::AM, AS = C::AS;
     extern __shared__ __align__(128) double sm[];
-    double *smS = sm + NA * AM;                 // staging ring
+    double *smS = sm + C::NM * AM;              // staging ring
     double *sE = smS + NA * AS;                 // coarse correction ring [4][WC]
     double *sC = sE + 4 * WC;                   // weights ring [4][8][WC]
-    uint64_t *bar = (uint64_t *)(sC + 32 * WC);
+    uint64_t *bar = (uint64_t *)(sC + 8 * C::CSL * WC);
 
     const int nx = a.A.nx, ny = a.A.ny;
     const long long P = a.A.pitch;
@@ -799,13 +806,13 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT>::NT, 1)
     int tm = 0, tsd = 0;
     for (int t = lo; t <= tend; t++, tm = (tm + 1 == RM) ? 0 : tm + 1, tsd = (tsd + 1 == SD) ? 0 : tsd + 1) {
         if (grp >= G_SPLIT) {
-            rg.wait(R_SPLIT, t - 1);
+            rg.wait(R_SPLIT, t - 1 - E);
             if (t <= hi) {
                 mbar_wait(&bar[tsd], ((t - lo) / SD) & 1);
                 if (grp == G_SPLIT)
-                    split_row<NA, AM, WD, PPT, NPG>(sm, smS, tsd, tm, 0, QSPLIT, m);
+                    split_row<NA, AM, WD, PPT, NPG, false>(sm, smS, tsd, tm, 0, QSPLIT, m);
                 else
-                    split_row<NA, AM, WD, PPT, NPG>(sm, smS, tsd, tm, QSPLIT, NA, m);
+                    split_row<NA, AM, WD, PPT, NPG, true>(sm, smS, tsd, tm, QSPLIT, NA, m);
             }
         } else if (grp == G_CORR || grp == G_CORR + 1) {
             rg.wait(R_CORR, t - 1);
@@ -856,23 +863,55 @@ static void device_limits()
     g_smem_sm = v > 0 ? (size_t)v : 228 * 1024;
 }
 
+// Deepest TMA prefetch (rows, <= 4) whose shared-memory footprint fits a CTA.
+constexpr size_t SMEM_CTA_MAX = 232448;  // 227 KB opt-in
+template <int KIND, int NS, int WD, bool UP, int PPT, int E>
+constexpr int pick_D()
+{
+    return Cfg<KIND, NS, WD, 4, UP, PPT, E>::SMEM <= SMEM_CTA_MAX   ? 4
+           : Cfg<KIND, NS, WD, 3, UP, PPT, E>::SMEM <= SMEM_CTA_MAX ? 3
+                                                                    : 2;
+}
+
 // Kernel instances: (kind, NS) -> (WD, D, pairs per thread).  WD = smem row width.
 template <int KIND, int NS>
 struct Inst {
 #ifndef BMG_WD5
 #define BMG_WD5 256
 #endif
-    static constexpr int WD_DN = KIND == 5 ? BMG_WD5 : 192;
-    static constexpr int D_DN = 4;
+#ifndef BMG_WD9DN
+#define BMG_WD9DN 192
+#endif
+#ifndef BMG_WD9UP
+#define BMG_WD9UP 256
+#endif
+    static constexpr int WD_DN = KIND == 5 ? BMG_WD5 : BMG_WD9DN;
+
 #ifndef BMG_PPT5
 #define BMG_PPT5 2
 #endif
     static constexpr int PPT_DN = KIND == 5 ? BMG_PPT5 : 1;
-    static constexpr int WD_UP = KIND == 5 ? BMG_WD5 : 256;
-    static constexpr int D_UP = 4;
-    static constexpr int PPT_UP = KIND == 5 ? BMG_PPT5 : 2;
-    using CD = Cfg<KIND, NS, WD_DN, D_DN, false, PPT_DN>;
-    using CU = Cfg<KIND, NS, WD_UP, D_UP, true, PPT_UP>;
+    static constexpr int WD_UP = KIND == 5 ? BMG_WD5 : (NS == 4 ? 192 : BMG_WD9UP);
+
+    static constexpr int PPT_UP = KIND == 5 ? BMG_PPT5 : (NS == 4 ? 1 : 2);
+#ifndef BMG_E5DN
+#define BMG_E5DN 0
+#endif
+#ifndef BMG_E9DN
+#define BMG_E9DN 0
+#endif
+#ifndef BMG_E5UP
+#define BMG_E5UP 0
+#endif
+#ifndef BMG_E9UP
+#define BMG_E9UP 0
+#endif
+    static constexpr int E_DN = KIND == 5 ? BMG_E5DN : BMG_E9DN;  // main-ring slack rows
+    static constexpr int E_UP = KIND == 5 ? BMG_E5UP : BMG_E9UP;
+    static constexpr int D_DN = pick_D<KIND, NS, WD_DN, false, PPT_DN, E_DN>();
+    static constexpr int D_UP = pick_D<KIND, NS, WD_UP, true, PPT_UP, E_UP>();
+    using CD = Cfg<KIND, NS, WD_DN, D_DN, false, PPT_DN, E_DN>;
+    using CU = Cfg<KIND, NS, WD_UP, D_UP, true, PPT_UP, E_UP>;
 };
 
 template <int KIND, int NS>
@@ -898,10 +937,10 @@ static void set_attrs()
     device_limits();
     constexpr size_t sd = I::CD::SMEM, su = I::CU::SMEM;
     if (sd <= g_smem_optin)
-        cudaFuncSetAttribute(k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN>,
+        cudaFuncSetAttribute(k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN, I::E_DN>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sd);
     if (su <= g_smem_optin)
-        cudaFuncSetAttribute(k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP>,
+        cudaFuncSetAttribute(k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)su);
     cudaGetLastError();  // an unsupported instance is simply not planned (plan_grid checks the size)
 }
@@ -1054,14 +1093,14 @@ template <int KIND, int NS>
 static void launch_down(const FusedGeom &g, const FArgs &a, const TMaps &tm, cudaStream_t s)
 {
     using I = Inst<KIND, NS>;
-    k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a, tm);
+    k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN, I::E_DN><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a, tm);
 }
 
 template <int KIND, int NS>
 static void launch_up(const FusedGeom &g, const FArgs &a, const TMaps &tm, cudaStream_t s)
 {
     using I = Inst<KIND, NS>;
-    k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a, tm);
+    k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a, tm);
 }
 
 static FArgs make_args(const FusedGeom &g, const Op &A, const CIv &ci)
