@@ -55,6 +55,7 @@ def lib():
             "orc_setup_interp": (c_int, [c_int, c_int, _dp, _dp]),
             "orc_rap": (c_int, [c_int, c_int, _dp, _dp, _dp]),
             "orc_relax": (None, [c_int, c_int, c_int, _dp, _dp, _dp, c_int]),
+            "orc_relax_lines": (c_int, [c_int, c_int, _dp, _dp, _dp, c_int, c_int]),
             "orc_residual": (None, [c_int, c_int, _dp, _dp, _dp, _dp]),
             "orc_restrict": (None, [c_int, c_int, _dp, _dp, _dp]),
             "orc_interp_add": (None, [c_int, c_int, _dp, _dp, _dp]),
@@ -63,7 +64,7 @@ def lib():
             "orc_assemble_dense": (None, [c_int, c_int, _dp, _dp]),
             "orc_norm2": (c_double, [c_int, c_int, _dp]),
             "orc_setup": (c_int, [c_int, c_int, c_int, c_long, _dp, _dp, _dp, _dp, _dp, c_int, c_int, c_int,
-                                  c_int, ctypes.POINTER(c_void_p)]),
+                                  c_int, c_int, ctypes.POINTER(c_void_p)]),
             "orc_destroy": (None, [c_void_p]),
             "orc_num_levels": (c_int, [c_void_p]),
             "orc_level_shape": (None, [c_void_p, c_int, _ip, _ip, _ip]),
@@ -137,6 +138,21 @@ def relax(st, kind, f, u, nsweeps=1) -> np.ndarray:
     return u
 
 
+POINT, XLINES, YLINES, ALTLINES = 0, 1, 2, 3
+RELAX_MODES = {"point": POINT, "xline": XLINES, "yline": YLINES, "altline": ALTLINES}
+
+
+def relax_lines(st, f, u, nsweeps=1, mode=XLINES) -> np.ndarray:
+    """c11 zebra line GS (x-lines, y-lines or alternating), nsweeps sweeps."""
+    ny, nx = st.shape[0] - 2, st.shape[1] - 2
+    u = np.array(u, dtype=np.float64, copy=True, order="C")
+    rc = lib().orc_relax_lines(nx, ny, _p(np.ascontiguousarray(st)), _p(np.ascontiguousarray(f)), _p(u), nsweeps,
+                               RELAX_MODES.get(mode, mode))
+    if rc != OK:
+        raise np.linalg.LinAlgError(f"orc_relax_lines: status {rc} (line block not SPD)")
+    return u
+
+
 def residual(st, f, u) -> np.ndarray:
     ny, nx = st.shape[0] - 2, st.shape[1] - 2
     r = _grid(nx, ny)
@@ -187,7 +203,7 @@ def norm2(g) -> float:
 class Hierarchy:
     """Oracle BoxMG hierarchy (setup c0-c4, c8) with V-cycle / solve (c9)."""
 
-    def __init__(self, stencil, nu1=2, nu2=1, coarsest=3, max_levels=0):
+    def __init__(self, stencil, nu1=2, nu2=1, coarsest=3, max_levels=0, relax="point"):
         nx, ny = stencil.nx, stencil.ny
         self.nx, self.ny = nx, ny
         planes = [np.ascontiguousarray(p, dtype=np.float64) for p in stencil.plane_list()]
@@ -195,7 +211,7 @@ class Hierarchy:
             planes.append(None)
         h = ctypes.c_void_p()
         rc = lib().orc_setup(nx, ny, stencil.kind, nx + 2, *[_p(p) for p in planes], nu1, nu2, coarsest,
-                             max_levels, ctypes.byref(h))
+                             max_levels, RELAX_MODES.get(relax, relax), ctypes.byref(h))
         if rc != OK:
             raise ValueError(f"orc_setup: status {rc}")
         self._h = h

@@ -37,6 +37,12 @@
 #define ORC_ENOTSPD 5
 #define ORC_ENOTCONV 6
 
+/* ---- relaxation modes (c6 point GS; c11 line GS) ---- */
+#define ORC_POINT 0
+#define ORC_XLINES 1
+#define ORC_YLINES 2
+#define ORC_ALTLINES 3
+
 /* ---- stencil entry order (fig:stencil_operator) ---- */
 enum { SW = 0, S_ = 1, SE = 2, W_ = 3, O_ = 4, E_ = 5, NW = 6, N_ = 7, NE = 8 };
 static const int DX[9] = {-1, 0, 1, -1, 0, 1, -1, 0, 1};
@@ -288,6 +294,107 @@ void orc_relax(int nx, int ny, int kind, const double *st, const double *f, doub
                 }
 }
 
+/*
+ * Thomas algorithm (tridiagonal LU without pivoting, the textbook
+ * forward-elimination / back-substitution): solve
+ *   lo[k] x[k-1] + di[k] x[k] + up[k] x[k+1] = rhs[k],  k = 0..n-1,
+ * lo[0] and up[n-1] ignored.  x receives the solution; gam is n doubles of
+ * scratch.  Returns ORC_ENOTSPD if an elimination pivot is <= 0 (a line block
+ * of an SPD operator is SPD, so its pivots are positive).
+ */
+static int thomas(int n, const double *lo, const double *di, const double *up, const double *rhs, double *x,
+                  double *gam)
+{
+    double beta = di[0];
+    if (!(beta > 0.0))
+        return ORC_ENOTSPD;
+    x[0] = rhs[0] / beta;
+    for (int k = 1; k < n; k++) {
+        gam[k] = up[k - 1] / beta;
+        beta = di[k] - lo[k] * gam[k];
+        if (!(beta > 0.0))
+            return ORC_ENOTSPD;
+        x[k] = (rhs[k] - lo[k] * x[k - 1]) / beta;
+    }
+    for (int k = n - 2; k >= 0; k--)
+        x[k] -= gam[k + 1] * x[k + 1];
+    return ORC_OK;
+}
+
+/*
+ * c11: zebra line Gauss-Seidel (fig:vcycle_flowchart's "Line" relaxation box,
+ * P:144; the paper gives no formula, reading in DESIGN.md §3 c11).
+ * dir = ORC_XLINES: the lines are the grid rows; one sweep = rows j with
+ * j mod 2 == 0 (the rows through coarse points, as c6's colour 0), then rows
+ * with j mod 2 == 1.  Every row of a colour is solved exactly for its nx
+ * unknowns, the couplings to the two neighbouring rows (the other colour,
+ * current values) moved to the right-hand side:
+ *   W u(i-1,j) + O u(i,j) + E u(i+1,j)
+ *     = f(i,j) - [SW u(i-1,j-1) + S u(i,j-1) + SE u(i+1,j-1)
+ *                 + NW u(i-1,j+1) + N u(i,j+1) + NE u(i+1,j+1)]
+ * (off-line terms summed in fig:stencil_operator order).  A 9-point stencil
+ * couples row j only to rows j-1, j+1, so the rows of one colour are
+ * independent.  dir = ORC_YLINES: the same with the roles of x and y swapped
+ * (columns i, colour i mod 2, couplings S, N on the line, SW,W,NW,SE,E,NE
+ * off it).  dir = ORC_ALTLINES: one sweep = an x-line sweep then a y-line
+ * sweep.  Returns ORC_ENOTSPD if a line pivot is <= 0 (u then partial).
+ */
+int orc_relax_lines(int nx, int ny, const double *st, const double *f, double *u, int nsweeps, int dir)
+{
+    int nmax = nx > ny ? nx : ny;
+    double *lo = (double *)malloc(sizeof(double) * (size_t)nmax * 6);
+    if (!lo)
+        return ORC_ENOMEM;
+    double *di = lo + nmax, *up = di + nmax, *rhs = up + nmax, *x = rhs + nmax, *gam = x + nmax;
+    int rc = ORC_OK;
+    for (int s = 0; s < nsweeps && rc == ORC_OK; s++) {
+        for (int pass = 0; pass < 2 && rc == ORC_OK; pass++) {
+            int on = pass == 0 ? (dir == ORC_XLINES || dir == ORC_ALTLINES) : (dir == ORC_YLINES || dir == ORC_ALTLINES);
+            if (!on)
+                continue;
+            int ylines = pass == 1;
+            int nl = ylines ? nx : ny;  /* number of lines */
+            int n = ylines ? ny : nx;   /* unknowns per line */
+            for (int c = 0; c < 2 && rc == ORC_OK; c++)
+                for (int line = 1; line <= nl && rc == ORC_OK; line++) {
+                    if ((line & 1) != c)
+                        continue;
+                    for (int k = 0; k < n; k++) {
+                        int i = ylines ? line : k + 1, j = ylines ? k + 1 : line;
+                        const double *a = st + 9 * gidx(nx, i, j);
+                        double off = 0.0;
+                        for (int d = 0; d < 9; d++) {
+                            int online = ylines ? DX[d] == 0 : DY[d] == 0;
+                            if (!online)
+                                off += a[d] * u[gidx(nx, i + DX[d], j + DY[d])];
+                        }
+                        rhs[k] = f[gidx(nx, i, j)] - off;
+                        di[k] = a[O_];
+                        lo[k] = ylines ? a[S_] : a[W_];
+                        up[k] = ylines ? a[N_] : a[E_];
+                    }
+                    rc = thomas(n, lo, di, up, rhs, x, gam);
+                    for (int k = 0; k < n && rc == ORC_OK; k++) {
+                        int i = ylines ? line : k + 1, j = ylines ? k + 1 : line;
+                        u[gidx(nx, i, j)] = x[k];
+                    }
+                }
+        }
+    }
+    free(lo);
+    return rc;
+}
+
+/* Relaxation of the cycle: point GS (c6) or line GS (c11) by mode. */
+static int relax_mode(int mode, int nx, int ny, int kind, const double *st, const double *f, double *u, int nsweeps)
+{
+    if (mode == ORC_POINT) {
+        orc_relax(nx, ny, kind, st, f, u, nsweeps);
+        return ORC_OK;
+    }
+    return orc_relax_lines(nx, ny, st, f, u, nsweeps, mode);
+}
+
 /* fig:vcycle_flowchart "Residual": r = f - A u on the interior; ring 0. */
 void orc_residual(int nx, int ny, const double *st, const double *f, const double *u, double *r)
 {
@@ -439,7 +546,7 @@ typedef struct {
 } orc_level;
 
 typedef struct {
-    int L, nu1, nu2;
+    int L, nu1, nu2, relax;
     orc_level lv[ORC_MAXLEV];
     double *chol; /* coarsest L factor, n*n */
     int nco;
@@ -466,11 +573,11 @@ void orc_destroy(orc_hier *h)
  * Cholesky factor (c8).  Coarse levels are 9-point.
  */
 int orc_setup(int nx, int ny, int kind, long pitch, const double *O, const double *W, const double *S,
-              const double *SWp, const double *NWp, int nu1, int nu2, int coarsest, int max_levels,
+              const double *SWp, const double *NWp, int nu1, int nu2, int coarsest, int max_levels, int relax,
               orc_hier **out)
 {
     *out = NULL;
-    if (nx < 1 || ny < 1 || (kind != 5 && kind != 9) || pitch < nx + 2)
+    if (nx < 1 || ny < 1 || (kind != 5 && kind != 9) || pitch < nx + 2 || relax < ORC_POINT || relax > ORC_ALTLINES)
         return ORC_EINVAL;
     orc_hier *h = (orc_hier *)calloc(1, sizeof(orc_hier));
     if (!h)
@@ -482,6 +589,7 @@ int orc_setup(int nx, int ny, int kind, long pitch, const double *O, const doubl
     }
     h->nu1 = nu1;
     h->nu2 = nu2;
+    h->relax = relax;
     int cx = nx, cy = ny;
     for (int l = 0; l < h->L; l++) {
         orc_level *v = &h->lv[l];
@@ -508,6 +616,18 @@ int orc_setup(int nx, int ny, int kind, long pitch, const double *O, const doubl
         rc = orc_setup_interp(v->nx, v->ny, v->st, v->ci);
         if (rc == ORC_OK)
             rc = orc_rap(v->nx, v->ny, v->st, v->ci, h->lv[l + 1].st);
+    }
+    /* c11: every line block of every relaxed level must have positive pivots */
+    for (int l = 0; rc == ORC_OK && relax != ORC_POINT && l + 1 < h->L; l++) {
+        orc_level *v = &h->lv[l];
+        size_t np = (size_t)(v->nx + 2) * (size_t)(v->ny + 2);
+        double *z = (double *)calloc(np, sizeof(double));
+        if (!z)
+            rc = ORC_ENOMEM;
+        else {
+            rc = orc_relax_lines(v->nx, v->ny, v->st, z, z, 1, relax);
+            free(z);
+        }
     }
     if (rc == ORC_OK) {
         orc_level *c = &h->lv[h->L - 1];
@@ -561,7 +681,8 @@ static void coarse_solve(orc_hier *h, orc_level *c)
 }
 
 /*
- * c9: V(nu1,nu2) cycle at level l (fig:vcycle_flowchart): relax nu1, r = f -
+ * c9: V(nu1,nu2) cycle at level l (fig:vcycle_flowchart): relax nu1 (c6
+ * point or c11 line GS, the hierarchy's mode; line pivots checked at setup), r = f -
  * A u, f_{l+1} = P^T r, u_{l+1} = 0, recurse (coarsest: Cholesky solve),
  * u += P u_{l+1}, relax nu2.
  */
@@ -573,13 +694,13 @@ static void vcycle_level(orc_hier *h, int l)
         return;
     }
     orc_level *c = &h->lv[l + 1];
-    orc_relax(v->nx, v->ny, v->kind, v->st, v->f, v->u, h->nu1);
+    relax_mode(h->relax, v->nx, v->ny, v->kind, v->st, v->f, v->u, h->nu1);
     orc_residual(v->nx, v->ny, v->st, v->f, v->u, v->r);
     orc_restrict(v->nx, v->ny, v->ci, v->r, c->f);
     memset(c->u, 0, sizeof(double) * (size_t)(c->nx + 2) * (size_t)(c->ny + 2));
     vcycle_level(h, l + 1);
     orc_interp_add(v->nx, v->ny, v->ci, c->u, v->u);
-    orc_relax(v->nx, v->ny, v->kind, v->st, v->f, v->u, h->nu2);
+    relax_mode(h->relax, v->nx, v->ny, v->kind, v->st, v->f, v->u, h->nu2);
 }
 
 /* ncycles V-cycles on the fine level; f, u are (nx+2)*(ny+2), u in/out. */
