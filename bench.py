@@ -26,6 +26,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "V(2,1) cycles/s and Munknowns/s at 8193^2; HBM GB/s vs peak; 1/2/4/8 GPU"
 CONFIG_KIND = {"aniso": 9}
+SOLVE_TOL = {"aniso4097": 1e-8}  # BASELINE config 3 solves to 1e-8; others 1e-10
+SOLVE_MAXIT = 100
 
 CONFIGS = {
     # name: (workload, nx, ny, description)
@@ -136,9 +138,10 @@ def host_info():
 
 # ------------------------------------------------------------------ oracle (CPU) legs
 ORACLE_SAMPLE_N = 2047
+RELAX = {"point": 0, "xline": 1, "yline": 2, "altline": 3}
 
 
-def oracle_cycles_per_s(wl, nx, ny, ncycles, warm=1):
+def oracle_cycles_per_s(wl, nx, ny, ncycles, warm=1, relax="point"):
     """Time the oracle V(2,1) on a bounded sample (n=2047, 1/16 of the 8191^2
     unknowns); returns (cycles/s scaled to the full workload, sample string)."""
     import numpy as np
@@ -146,10 +149,10 @@ def oracle_cycles_per_s(wl, nx, ny, ncycles, warm=1):
     import oracle
     from paper_2502_05279_b200 import problems as P
 
-    n = ORACLE_SAMPLE_N
+    n = min(ORACLE_SAMPLE_N, nx, ny)
     st = P.workload(wl, n, n)
     f = P.rhs_const(n, n)
-    h = oracle.Hierarchy(st)
+    h = oracle.Hierarchy(st, relax=relax)
     u = np.zeros_like(f)
     for _ in range(warm):
         u = h.vcycle(f, u, 1)
@@ -158,7 +161,8 @@ def oracle_cycles_per_s(wl, nx, ny, ncycles, warm=1):
     dt = time.perf_counter() - t
     scale = (n * n) / (float(nx) * float(ny))
     per_cycle = dt / ncycles
-    return ncycles / dt * scale, per_cycle, (f"oracle V(2,1) on {wl} {n}x{n} (same recipe, {n*n/(nx*ny):.4f} of the "
+    return ncycles / dt * scale, per_cycle, (f"oracle V(2,1) [{relax} relaxation] on {wl} {n}x{n} (same recipe, "
+                                             f"{n*n/(nx*ny):.4f} of the "
                                              f"{nx}x{ny} unknowns), {ncycles} timed cycles after {warm} warm-up, "
                                              f"setup untimed; cycles/s scaled by the unknown ratio to {nx}x{ny}")
 
@@ -170,10 +174,10 @@ def run_reference(args, cfg):
         return
     wl, nx, ny, desc = CONFIGS[cfg]
     model, cores = host_info()
-    val, per_cycle, sample = oracle_cycles_per_s(wl, nx, ny, args.steps, warm=args.warmup)
+    val, per_cycle, sample = oracle_cycles_per_s(wl, nx, ny, args.steps, warm=args.warmup, relax=args.relax)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "cycles/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_cycle * 1e3 * (nx * ny) / ORACLE_SAMPLE_N ** 2,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / val,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "nx": nx, "ny": ny, "cycle": "V(2,1)"},
         "munknowns_per_s": val * nx * ny / 1e6,
@@ -196,6 +200,9 @@ def main():
     ap.add_argument("--unfused", action="store_true", help="one kernel per method step (debug/comparison)")
     ap.add_argument("--dist", action="store_true", help="use the row-slab NCCL solver even on one GPU")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--relax", default="point", choices=sorted(RELAX),
+                    help="relaxation: point GS (c6, default) or zebra line GS (c11)")
+    ap.add_argument("--solve-tol", type=float, default=None, help="tolerance of the timed solve (default per config)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -219,6 +226,7 @@ def main():
     st = P.workload(wl, nx, ny)
     prm = bmg.bmg_params_default()
     prm.fused = 0 if args.unfused else 1
+    prm.relax = RELAX[args.relax]
     distributed = world > 1 or args.dist
     if distributed:
         # strong scaling (BASELINE config 4): one global problem in row slabs, NCCL ghost rows
@@ -299,6 +307,26 @@ def main():
     rnorm = solver.residual_norm(f, x)
     fnorm = P.h_of(max(nx, ny)) ** 2 * (float(nx) * ny) ** 0.5
 
+    # the solve loop (bmg_solve: V-cycles + residual norm per cycle, host-checked stopping
+    # test) from x0 = 0, timed separately (SURVEY §8(d) "GPU timing")
+    solve = None
+    if not distributed:
+        tol = args.solve_tol or SOLVE_TOL.get(args.config, 1e-10)
+        xs = solver.grid()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        it, hist, rc = solver.solve(f, xs, tol, SOLVE_MAXIT)
+        dt = time.perf_counter() - t0
+        k = len(hist) - 1
+        solve = {"tol": tol, "iterations": it, "converged": rc == 0, "ms": dt * 1e3,
+                 "final_rel_residual": float(hist[-1] / fnorm) if len(hist) else None,
+                 "mean_factor": float((hist[-1] / hist[0]) ** (1.0 / k)) if k > 0 and hist[0] > 0 else None,
+                 "last_factor": float(hist[-1] / hist[-2]) if k > 0 and hist[-2] > 0 else None,
+                 "setup_ms": solver.setup_ms,
+                 "note": "x0 = 0; ms = wall clock of bmg_solve (norm + stopping test synchronised per cycle); "
+                         "setup_ms = wall clock of bmg_setup (S0-S3 + graph-free allocation, synchronised)"}
+        del xs
+
     # e2e: the same metric through the public API with HOST buffers (pinned): per step
     # H2D of rhs and x, one V(2,1) cycle, D2H of x; host wall clock, max over ranks
     e2e = None
@@ -338,7 +366,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        val, per_cycle, sample = oracle_cycles_per_s(wl, nx, ny, 8, warm=1)
+        val, per_cycle, sample = oracle_cycles_per_s(wl, nx, ny, 8, warm=1, relax=args.relax)
         model, cores = host_info()
         cpu = {"value": val, "unit": "cycles/s", "cores": 1, "kind": "oracle", "sample": sample,
                "host_cpu": model, "host_cores": cores}
@@ -361,7 +389,7 @@ def main():
         "config": {"workload": desc, "nx": nx, "ny": ny, "levels": L, "cycle": "V(2,1)",
                    "parallelism": parallelism,
                    "l2": "inputs > L2 (level-0 arrays 537 MB each); no flush needed",
-                   "fused": bool(prm.fused)},
+                   "fused": bool(prm.fused) and args.relax == "point", "relax": args.relax},
         "munknowns_per_s": cycles_per_s * nx * ny / 1e6,
         "model_B_GBps": B / (ms_per_step / 1e3) / 1e9,
         "model_B_frac": B / (ms_per_step / 1e3) / 1e9 / (peak * world),
@@ -373,6 +401,7 @@ def main():
         "clocks": {"sm_mhz": cs["sm_mhz"], "sm_max_mhz": cs["sm_max_mhz"], "reasons": cs["reasons"],
                    "samples": cs["samples"]},
         "e2e": e2e,
+        "solve": solve,
         "cpu_baseline": cpu,
     }
     if rank == 0:
@@ -407,12 +436,18 @@ def roofline(leg, nx, ny, kind, peak, peak_src, ms_per_step, args):
     # compulsory bytes of the down leg per fine unknown: read u, f and the
     # s operator planes, write u, read the 2N-double CI planes, write f_c and zero u_c (N/4 each)
     per_unk = 8.0 * (s_planes + 2 + 1 + 2 + 0.25 + 0.25)
+    if args.relax != "point":
+        # per-step kernels: every line sweep direction reads the s planes, f and
+        # u and writes u once ((s+3) doubles); then residual (s+3) and restriction (3.25)
+        ndir = 2 if args.relax == "altline" else 1
+        per_unk = 8.0 * (2 * ndir * (s_planes + 3) + (s_planes + 3) + 3.25)
     algo = per_unk * nx * ny
     achieved = algo / (dur_ms / 1e3) / 1e9
-    kname = f"k_fused_down<{kind}, 4>" if not args.unfused else None
+    kname = f"k_fused_down<{kind}, 4>" if not args.unfused and args.relax == "point" else None
     traffic = traffic_per_launch(kname, nx, ny) if kname else None
-    return {"bound": "hbm", "kernel": "level-0 down leg (bmg_smooth_restrict: nu1 GS sweeps + residual + "
-                                      "restriction)", "achieved": achieved, "peak": peak, "unit": "GB/s",
+    what = ("nu1 GS sweeps + residual + restriction" if args.relax == "point" else
+            f"nu1 {args.relax} GS sweeps (3 line kernels per colour) + residual + restriction")
+    return {"bound": "hbm", "kernel": f"level-0 down leg (bmg_smooth_restrict: {what})", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": algo, "algorithmic_bytes_per_unknown": per_unk,
             "launch_ms": dur_ms, "launches_timed": launches, "share_of_step": dur_ms / ms_per_step}

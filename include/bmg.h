@@ -41,7 +41,7 @@ typedef enum {
     BMG_ENOMEM = 2,   /* device allocation failed */
     BMG_ECUDA = 3,    /* CUDA runtime error (detail in bmg_last_error_detail) */
     BMG_ENCCL = 4,    /* reserved for the multi-GPU path */
-    BMG_ENOTSPD = 5,  /* coarsest-level Cholesky pivot <= 0 */
+    BMG_ENOTSPD = 5,  /* coarsest-level Cholesky pivot <= 0, or a line-block pivot <= 0 */
     BMG_ENOTCONV = 6  /* bmg_solve reached maxiter; x and hist stay valid */
 } bmg_status_t;
 
@@ -71,7 +71,20 @@ typedef struct {
     int agglom_rows; /* multi-GPU: agglomerate below this many rows per rank (default 128) */
     int cycle_sym;   /* 0 = same colour order on both legs (default); 1 reserved */
     int fused;       /* 1 = fused streaming kernels on large levels (default), 0 = one kernel per step */
+    int relax;       /* relaxation (fig:vcycle_flowchart's "Relaxation" boxes):
+                        BMG_RELAX_POINT (default) multicolour point Gauss-Seidel (DESIGN §3 c6);
+                        BMG_RELAX_XLINES / _YLINES zebra line Gauss-Seidel along x / y, one
+                        sweep = the lines of colour (line index mod 2) 0 then 1, each line's
+                        tridiagonal block solved exactly (the "Line" box; c11);
+                        BMG_RELAX_ALTLINES one sweep = an x-line then a y-line sweep.
+                        Line modes run the per-step kernels (fused ignored) and need
+                        nx, ny <= 32768 (EINVAL otherwise). */
 } bmg_params_t;
+
+#define BMG_RELAX_POINT 0
+#define BMG_RELAX_XLINES 1
+#define BMG_RELAX_YLINES 2
+#define BMG_RELAX_ALTLINES 3
 
 /* Fill *p with the defaults above. */
 void bmg_params_default(bmg_params_t *p);
@@ -83,8 +96,12 @@ void bmg_params_default(bmg_params_t *p);
  * (S2, c4); factor the coarsest level densely by Cholesky (S3, c8).
  * Levels: n_{l+1} = floor(n_l/2) until min(nx,ny) <= coarsest (c1).
  * params may be NULL (defaults).  On success *out owns all device memory.
- * Errors: EINVAL (sizes, kind, pitch, a_O <= 0, den <= 0), ENOMEM, ENOTSPD,
- * ECUDA.  Synchronises cuda_stream.
+ * Line relaxation modes also check that every line block (the tridiagonal
+ * part of A along each relaxed line, on every level but the coarsest) has
+ * positive elimination pivots, as the blocks of an SPD operator do.
+ * Errors: EINVAL (sizes, kind, pitch, a_O <= 0, den <= 0, relax not a mode),
+ * ENOMEM, ENOTSPD (coarsest Cholesky pivot or line pivot <= 0), ECUDA.
+ * Synchronises cuda_stream.
  */
 bmg_status_t bmg_setup(const bmg_stencil_t *stencil, const bmg_params_t *params, void *cuda_stream,
                        bmg_solver_t *out);
@@ -142,7 +159,8 @@ bmg_status_t bmg_export_level(bmg_solver_t h, int level, double *stencil_host, d
  * Single method steps on one level, for per-kernel parity tests.  All arrays
  * are device grid functions of that level with bmg_level_pitch(level); for
  * restriction/interpolation the coarse array uses bmg_level_pitch(level+1).
- *  bmg_relax:      nsweeps multicolour GS sweeps (c6), u in/out.
+ *  bmg_relax:      nsweeps sweeps of the handle's relaxation (params.relax:
+ *                  multicolour point GS, c6, or zebra line GS, c11), u in/out.
  *  bmg_residual:   r = f - A u on the interior; r's ring set to 0.
  *  bmg_restrict:   fc = P^T r, the fig:restrict_kernel listing (c5); ring 0.
  *  bmg_interp_add: u += P ec (c7); ec's ring must be 0.
@@ -220,7 +238,8 @@ bmg_status_t bmg_partition(int nx, int ny, int nranks, const bmg_params_t *param
  * communicator.  The returned handle works with bmg_vcycle, bmg_solve,
  * bmg_residual_norm, bmg_num_levels, bmg_local_rows and bmg_destroy; rhs and x are
  * local arrays (NCCL) or global arrays (loopback).  Errors: EINVAL (grid too small,
- * params unsupported: needs fused = 1, nu1, nu2 in {1,2}), ENCCL, ENOMEM, ECUDA.
+ * params unsupported: needs fused = 1, relax = BMG_RELAX_POINT, nu1, nu2 in {1,2}),
+ * ENCCL, ENOMEM, ECUDA.
  */
 bmg_status_t bmg_setup_dist(const bmg_stencil_t *stencil, const bmg_comm_t *comm, const bmg_params_t *params,
                             void *cuda_stream, bmg_solver_t *out);

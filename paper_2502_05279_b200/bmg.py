@@ -9,6 +9,7 @@ call raises ``RuntimeError``.
 from __future__ import annotations
 
 import ctypes
+import time
 import os
 
 import numpy as np
@@ -29,6 +30,9 @@ EXPORTS = (
 
 BMG_HALO = 6
 
+# bmg_params_t.relax (include/bmg.h)
+BMG_RELAX_POINT, BMG_RELAX_XLINES, BMG_RELAX_YLINES, BMG_RELAX_ALTLINES = range(4)
+
 
 class bmg_stencil_t(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int), ("nx", ctypes.c_int), ("ny", ctypes.c_int), ("pitch", ctypes.c_longlong),
@@ -38,7 +42,7 @@ class bmg_stencil_t(ctypes.Structure):
 class bmg_params_t(ctypes.Structure):
     _fields_ = [("nu1", ctypes.c_int), ("nu2", ctypes.c_int), ("coarsest", ctypes.c_int),
                 ("max_levels", ctypes.c_int), ("agglom_rows", ctypes.c_int), ("cycle_sym", ctypes.c_int),
-                ("fused", ctypes.c_int)]
+                ("fused", ctypes.c_int), ("relax", ctypes.c_int)]
 
 
 class bmg_comm_t(ctypes.Structure):
@@ -303,7 +307,9 @@ class Solver:
         self.pitch = pitch or default_pitch(self.nx)
         self.device = device
         planes = [to_device(p, self.pitch, device) for p in stencil.plane_list()]
-        self.h = bmg_setup(planes, self.kind, self.nx, self.ny, self.pitch, params)
+        t0 = time.perf_counter()
+        self.h = bmg_setup(planes, self.kind, self.nx, self.ny, self.pitch, params)  # synchronises
+        self.setup_ms = (time.perf_counter() - t0) * 1e3
         self.L = bmg_num_levels(self.h)
 
     def grid(self, a: np.ndarray | None = None):

@@ -102,6 +102,7 @@ struct bmg_solver {
     bmg_solver_t dist_inner = nullptr;  // its replicated coarse solver (owned by dist)
     long long dist_rows_total = 0;      // doubles of a level-0 rhs/x array of this handle
     int dist_local_ranks = 1;
+    double *line_scr = nullptr;       // c11 line relaxation scratch (line modes only)
     int tail_l0 = 1 << 30;            // first level of the tail kernel (none: > L)
     TailPlan *tail = nullptr;         // its device-side plan
     bool timing = false;              // bmg_timing: timed graph variant, event pair per launch
@@ -147,6 +148,7 @@ void bmg_params_default(bmg_params_t *p)
     p->agglom_rows = 128;
     p->cycle_sym = 0;
     p->fused = 1;
+    p->relax = BMG_RELAX_POINT;
 }
 
 const char *bmg_strerror(bmg_status_t s)
@@ -289,9 +291,22 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
         return fail(BMG_EINVAL, "interpolation denominator <= 0 (operator not suited to BoxMG collapse)");
     if (herr & ERR_PIVOT)
         return fail(BMG_ENOTSPD, "coarsest-level Cholesky pivot <= 0");
+    // c11 line relaxation: scratch sized for level 0, line pivots of every relaxed level
+    if (pr.relax != BMG_RELAX_POINT) {
+        if (h->lv[0].nx > LINE_NMAX || h->lv[0].ny > LINE_NMAX)
+            return fail(BMG_EINVAL, "line relaxation: lines of at most 32768 unknowns");
+        TRY(dalloc(h, &h->line_scr, line_scratch_doubles(h->lv[0].nx, h->lv[0].ny)));
+        for (int l = 0; l + 1 < h->L; l++)
+            launch_line_pivots(h->lv[l].op(), pr.relax, h->d_err, s);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (herr & ERR_LINE)
+            return fail(BMG_ENOTSPD, "line relaxation: a line block has an elimination pivot <= 0");
+    }
     CK(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
     // tail kernel: levels from the first with <= TAIL_POINTS unknowns down to the coarsest
-    if (h->prm.fused && h->L >= 2 && h->L <= 32) {
+    if (h->prm.fused && h->prm.relax == BMG_RELAX_POINT && h->L >= 2 && h->L <= 32) {
         long long lim = TAIL_POINTS;
         if (const char *e = getenv("BMG_TAIL_POINTS"))  // tuning knob (bench sweeps)
             lim = atoll(e);
@@ -324,7 +339,7 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
     // fused streaming plan + ping-pong partner of u for every fused level above the tail
     for (int l = 0; l + 1 < h->L && l < 32 && l < h->tail_l0; l++) {
         Level &v = h->lv[l];
-        if (!h->prm.fused)
+        if (!h->prm.fused || h->prm.relax != BMG_RELAX_POINT)
             break;
         TRY(fused_plan_level(h->fplan, l, v.nx, v.ny, v.pitch, v.kind, h->prm.nu1, h->prm.nu2, (v.pitch & 1) == 0));
         LevelPlan &lp = h->fplan.lv[l];
@@ -356,7 +371,8 @@ bmg_status_t bmg_setup(const bmg_stencil_t *st, const bmg_params_t *params, void
         h->prm = *params;
     else
         bmg_params_default(&h->prm);
-    if (h->prm.nu1 < 0 || h->prm.nu2 < 0 || h->prm.coarsest < 1) {
+    if (h->prm.nu1 < 0 || h->prm.nu2 < 0 || h->prm.coarsest < 1 || h->prm.relax < BMG_RELAX_POINT ||
+        h->prm.relax > BMG_RELAX_ALTLINES) {
         delete h;
         return fail(BMG_EINVAL, "bad params");
     }
@@ -384,6 +400,15 @@ static bool use_fused(bmg_solver *h, int l, const void *f, const void *uin, cons
     return lp.down && lp.up && al16(f) && al16(uin) && al16(uout) && uin != uout;
 }
 
+// nsweeps sweeps of the handle's relaxation on level l (c6 point or c11 line GS)
+static void relax_level(bmg_solver *h, int l, const double *f, double *u, int nsweeps, cudaStream_t s, int *n)
+{
+    if (h->prm.relax == BMG_RELAX_POINT)
+        launch_relax(h->lv[l].op(), f, u, nsweeps, s, n);
+    else
+        launch_relax_lines(h->lv[l].op(), f, u, nsweeps, h->prm.relax, h->line_scr, s, n);
+}
+
 static void copy_level(bmg_solver *h, int l, double *dst, const double *src, cudaStream_t s)
 {
     if (dst != src)
@@ -399,7 +424,7 @@ static void enqueue_down(bmg_solver *h, int l, bool fused, const double *f, cons
     if (fused && fused_down(h->fplan, l, v.op(), h->civ(l), f, uin, uout, fc, uc, s, n))
         return;
     copy_level(h, l, uout, uin, s);
-    launch_relax(v.op(), f, uout, h->prm.nu1, s, n);
+    relax_level(h, l, f, uout, h->prm.nu1, s, n);
     launch_residual(v.op(), f, uout, v.r, s);
     launch_restrict(v.op(), h->civ(l), v.r, fc, uc, s);
     *n += 2;
@@ -415,7 +440,7 @@ static void enqueue_up(bmg_solver *h, int l, bool fused, const double *f, const 
     copy_level(h, l, uout, uin, s);
     launch_interp_add(v.op(), h->civ(l), ec, uout, s);
     *n += 1;
-    launch_relax(v.op(), f, uout, h->prm.nu2, s, n);
+    relax_level(h, l, f, uout, h->prm.nu2, s, n);
 }
 
 // Enqueue one V(nu1,nu2) cycle (fig:vcycle_flowchart; DESIGN §3 c9) on s.
@@ -765,7 +790,7 @@ static bmg_status_t check_level(bmg_solver_t h, int level, bool need_coarse)
 bmg_status_t bmg_relax(bmg_solver_t h, int level, const double *f, double *u, int nsweeps, void *cuda_stream)
 {
     TRY(check_level(h, level, false));
-    launch_relax(h->lv[level].op(), f, u, nsweeps, (cudaStream_t)cuda_stream, nullptr);
+    relax_level(h, level, f, u, nsweeps, (cudaStream_t)cuda_stream, nullptr);
     CK(cudaGetLastError());
     return BMG_OK;
 }

@@ -17,7 +17,17 @@ namespace bmg {
 enum { CI_LNE = 0, CI_LA = 1, CI_LNW = 2, CI_LR = 3, CI_LL = 4, CI_LSE = 5, CI_LB = 6, CI_LSW = 7 };
 
 // error bits raised by setup kernels (device int, OR-ed)
-enum { ERR_DIAG = 1, ERR_DEN = 2, ERR_PIVOT = 4 };
+enum { ERR_DIAG = 1, ERR_DEN = 2, ERR_PIVOT = 4, ERR_LINE = 8 };
+
+// relaxation modes (bmg_params_t.relax): c6 point GS, c11 zebra line GS
+enum { RELAX_POINT = 0, RELAX_XLINES = 1, RELAX_YLINES = 2, RELAX_ALTLINES = 3 };
+
+// line relaxation: unknowns per chunk of a line (kernels_line.cu)
+constexpr int LINE_M = 8;
+// shared memory of the reduced-system kernel (one line's 3 x 2*ceil(n/LINE_M)
+// doubles must fit): lines of at most LINE_NMAX unknowns
+constexpr int LINE_SMEM = 227 * 1024;
+constexpr int LINE_NMAX = 32768;
 
 // One level's operator (read-only view).  SW/NW are nullptr on 5-point levels.
 // Pointers are GLOBAL-row indexed: element (i, j) is at p[j*pitch + i] for the
@@ -97,6 +107,13 @@ void launch_relax(const Op &A, const double *f, double *u, int nsweeps, cudaStre
 void launch_residual(const Op &A, const double *f, const double *u, double *r, cudaStream_t s);
 void launch_restrict(const Op &A, const CIv &ci, const double *r, double *fc, double *uc, cudaStream_t s);
 void launch_interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s);
+// c11 zebra line GS (kernels_line.cu): nsweeps sweeps in `mode`; scr holds
+// line_scratch_doubles(nx, ny) doubles.  launch_line_pivots ORs ERR_LINE into
+// *err if a line block has a pivot <= 0.
+void launch_relax_lines(const Op &A, const double *f, double *u, int nsweeps, int mode, double *scr, cudaStream_t s,
+                        int *nlaunch);
+void launch_line_pivots(const Op &A, int mode, int *err, cudaStream_t s);
+size_t line_scratch_doubles(int nx, int ny);
 void launch_resid_norm(const Op &A, const double *f, const double *u, double *r_out, double *partials,
                        double *result, cudaStream_t s);
 void launch_norm(const Op &A, const double *g, double *partials, double *result, cudaStream_t s);

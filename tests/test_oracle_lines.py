@@ -225,13 +225,22 @@ def test_vcycle_line_matches_dense_vcycle(orc):
 
 
 def test_line_not_spd_reported(orc):
-    """p-L6: O = 1, W = -1 along x (row diag > 0 but tridiag(-1, 1, -1) is
-    indefinite): x-line relaxation reports ENOTSPD, at setup too."""
-    nx, ny = 6, 6
-    shape = (ny + 2, nx + 2)
-    O = np.zeros(shape)
-    O[1:-1, 1:-1] = 1.0
-    stc = P.Stencil(5, nx, ny, {"O": O, "W": -np.ones(shape), "S": np.zeros(shape)})
+    """p-L6: an x-line segment with O = 1, W = -1 (tridiag(-1, 1, -1) is singular:
+    second pivot 0) inside a Poisson grid: x-line relaxation reports ENOTSPD (also
+    at setup), while the hierarchy with point or y-line relaxation sets up fine."""
+    n = 31
+    stc = P.workload("poisson", n, n)
+    stc.planes = {k: v.copy() for k, v in stc.planes.items()}
+    stc.planes["O"][5, 3:6] = 1.0
+    stc.planes["W"][5, 4:6] = -1.0
+    stc.planes["S"][5, 3:6] = -0.001
+    stc.planes["S"][6, 3:6] = -0.001
     st = orc.expand_stencil(stc)
+    z = np.zeros((n + 2, n + 2))
     with pytest.raises(np.linalg.LinAlgError):
-        orc.relax_lines(st, np.zeros(shape), np.zeros(shape), 1, "xline")
+        orc.relax_lines(st, z, z, 1, "xline")
+    orc.relax_lines(st, z, z, 1, "yline")
+    with pytest.raises(ValueError, match="status 5"):
+        orc.Hierarchy(stc, relax="xline")
+    orc.Hierarchy(stc, relax="yline")
+    orc.Hierarchy(stc, relax="point")

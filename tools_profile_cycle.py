@@ -6,7 +6,9 @@ from paper_2502_05279_b200 import bmg, problems as P
 
 n = int(os.environ.get("N", "8191")); wl = os.environ.get("WL", "poisson")
 st = P.workload(wl, n, n)
-s = bmg.Solver(st)
+prm = bmg.bmg_params_default()
+prm.relax = int(os.environ.get("RELAX", "0"))
+s = bmg.Solver(st, prm)
 f = s.grid(P.rhs_const(n, n)); x = s.grid()
 s.vcycle(f, x, 3)
 torch.cuda.synchronize()
