@@ -359,16 +359,32 @@ __global__ void __launch_bounds__(128) k_line_reduced(Op A, double *__restrict__
     const int s0 = (lane * nq) / 32, m = ((lane + 1) * nq) / 32 - s0;  // m >= 3
     double *a = lo + lane, *c = up + lane, *d = rh + lane;             // row k at [k*32]
     // coalesced loads (lane L reads rows it*32 + L), stored to the owner's slot;
-    // unrolled so that several loads per lane are in flight
-#pragma unroll 4
-    for (int q = lane; q < nq; q += 32) {
-        int t = (q * 32 + 31) / nq;  // owner: the t with t*nq/32 <= q < (t+1)*nq/32
-        if ((t * nq) / 32 > q)
-            t--;
-        const int i = (q - (t * nq) / 32) * 32 + t;
-        lo[i] = sc.rlo[base + q];
-        up[i] = sc.rup[base + q];
-        rh[i] = sc.rrhs[base + q];
+    // batches of 16 rows per lane in flight (the loads, not the arithmetic, bound
+    // this kernel otherwise)
+    for (int q0 = 0; q0 < nq; q0 += 16 * 32) {
+        double vl[16], vu[16], vr[16];
+#pragma unroll
+        for (int b = 0; b < 16; b++) {
+            const int q = q0 + b * 32 + lane;
+            if (q < nq) {
+                vl[b] = sc.rlo[base + q];
+                vu[b] = sc.rup[base + q];
+                vr[b] = sc.rrhs[base + q];
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < 16; b++) {
+            const int q = q0 + b * 32 + lane;
+            if (q < nq) {
+                int t = (q * 32 + 31) / nq;  // owner: the t with t*nq/32 <= q < (t+1)*nq/32
+                if ((t * nq) / 32 > q)
+                    t--;
+                const int i = (q - (t * nq) / 32) * 32 + t;
+                lo[i] = vl[b];
+                up[i] = vu[b];
+                rh[i] = vr[b];
+            }
+        }
     }
     __syncwarp();
     for (int k = 2; k < m; k++) {
