@@ -56,6 +56,9 @@ def lib():
             "orc_rap": (c_int, [c_int, c_int, _dp, _dp, _dp]),
             "orc_relax": (None, [c_int, c_int, c_int, _dp, _dp, _dp, c_int]),
             "orc_relax_lines": (c_int, [c_int, c_int, _dp, _dp, _dp, c_int, c_int]),
+            "orc_relax_adjoint": (None, [c_int, c_int, c_int, _dp, _dp, _dp, c_int]),
+            "orc_relax_lines_adjoint": (c_int, [c_int, c_int, _dp, _dp, _dp, c_int, c_int]),
+            "orc_pcg": (c_int, [c_void_p, _dp, _dp, c_double, c_int, _ip, _dp]),
             "orc_residual": (None, [c_int, c_int, _dp, _dp, _dp, _dp]),
             "orc_restrict": (None, [c_int, c_int, _dp, _dp, _dp]),
             "orc_interp_add": (None, [c_int, c_int, _dp, _dp, _dp]),
@@ -64,7 +67,7 @@ def lib():
             "orc_assemble_dense": (None, [c_int, c_int, _dp, _dp]),
             "orc_norm2": (c_double, [c_int, c_int, _dp]),
             "orc_setup": (c_int, [c_int, c_int, c_int, c_long, _dp, _dp, _dp, _dp, _dp, c_int, c_int, c_int,
-                                  c_int, c_int, ctypes.POINTER(c_void_p)]),
+                                  c_int, c_int, c_int, ctypes.POINTER(c_void_p)]),
             "orc_destroy": (None, [c_void_p]),
             "orc_num_levels": (c_int, [c_void_p]),
             "orc_level_shape": (None, [c_void_p, c_int, _ip, _ip, _ip]),
@@ -153,6 +156,25 @@ def relax_lines(st, f, u, nsweeps=1, mode=XLINES) -> np.ndarray:
     return u
 
 
+def relax_adjoint(st, kind, f, u, nsweeps=1) -> np.ndarray:
+    """c12: multicolour point GS with the colours in descending order."""
+    ny, nx = st.shape[0] - 2, st.shape[1] - 2
+    u = np.array(u, dtype=np.float64, copy=True, order="C")
+    lib().orc_relax_adjoint(nx, ny, kind, _p(st), _p(np.ascontiguousarray(f)), _p(u), nsweeps)
+    return u
+
+
+def relax_lines_adjoint(st, f, u, nsweeps=1, mode=XLINES) -> np.ndarray:
+    """c12: line GS with every sweep's (direction, colour) passes reversed."""
+    ny, nx = st.shape[0] - 2, st.shape[1] - 2
+    u = np.array(u, dtype=np.float64, copy=True, order="C")
+    rc = lib().orc_relax_lines_adjoint(nx, ny, _p(np.ascontiguousarray(st)), _p(np.ascontiguousarray(f)), _p(u),
+                                       nsweeps, RELAX_MODES.get(mode, mode))
+    if rc != OK:
+        raise np.linalg.LinAlgError(f"orc_relax_lines_adjoint: status {rc}")
+    return u
+
+
 def residual(st, f, u) -> np.ndarray:
     ny, nx = st.shape[0] - 2, st.shape[1] - 2
     r = _grid(nx, ny)
@@ -203,7 +225,7 @@ def norm2(g) -> float:
 class Hierarchy:
     """Oracle BoxMG hierarchy (setup c0-c4, c8) with V-cycle / solve (c9)."""
 
-    def __init__(self, stencil, nu1=2, nu2=1, coarsest=3, max_levels=0, relax="point"):
+    def __init__(self, stencil, nu1=2, nu2=1, coarsest=3, max_levels=0, relax="point", cycle_sym=0):
         nx, ny = stencil.nx, stencil.ny
         self.nx, self.ny = nx, ny
         planes = [np.ascontiguousarray(p, dtype=np.float64) for p in stencil.plane_list()]
@@ -211,7 +233,7 @@ class Hierarchy:
             planes.append(None)
         h = ctypes.c_void_p()
         rc = lib().orc_setup(nx, ny, stencil.kind, nx + 2, *[_p(p) for p in planes], nu1, nu2, coarsest,
-                             max_levels, RELAX_MODES.get(relax, relax), ctypes.byref(h))
+                             max_levels, RELAX_MODES.get(relax, relax), cycle_sym, ctypes.byref(h))
         if rc != OK:
             raise ValueError(f"orc_setup: status {rc}")
         self._h = h
@@ -245,6 +267,14 @@ class Hierarchy:
 
     def residual_norm(self, f, u) -> float:
         return lib().orc_residual_norm(self._h, _p(np.ascontiguousarray(f)), _p(np.ascontiguousarray(u)))
+
+    def pcg(self, f, u, tol, maxiter):
+        """c13: V-cycle-preconditioned CG (needs nu1 == nu2, cycle_sym=1)."""
+        u = np.array(u, dtype=np.float64, copy=True, order="C")
+        hist = np.zeros(maxiter + 1)
+        it = ctypes.c_int()
+        rc = lib().orc_pcg(self._h, _p(np.ascontiguousarray(f)), _p(u), tol, maxiter, ctypes.byref(it), _p(hist))
+        return u, it.value, hist[: it.value + 1], rc
 
     def solve(self, f, u, tol, maxiter):
         u = np.array(u, dtype=np.float64, copy=True, order="C")

@@ -277,13 +277,15 @@ static double offdiag_dot(int nx, const double *a, const double *u, int i, int j
  * c6: Gauss-Seidel point relaxation (fig:vcycle_flowchart "Gauss Seidel",
  * P:96) in multicolour order: one sweep = for each colour c in
  * ascending order, u_p <- (f_p - sum_{q!=p} A_pq u_q) / A_pp for every p of
- * colour c.
+ * colour c.  rev = 1 (c12, the adjoint smoother of the symmetric cycle):
+ * colours in descending order.
  */
-void orc_relax(int nx, int ny, int kind, const double *st, const double *f, double *u, int nsweeps)
+static void relax_point(int nx, int ny, int kind, const double *st, const double *f, double *u, int nsweeps, int rev)
 {
     int ncol = kind == 5 ? 2 : 4;
     for (int s = 0; s < nsweeps; s++)
-        for (int c = 0; c < ncol; c++)
+        for (int cc = 0; cc < ncol; cc++) {
+            int c = rev ? ncol - 1 - cc : cc;
             for (int j = 1; j <= ny; j++)
                 for (int i = 1; i <= nx; i++) {
                     if (colour(kind, i, j) != c)
@@ -292,6 +294,17 @@ void orc_relax(int nx, int ny, int kind, const double *st, const double *f, doub
                     size_t p = gidx(nx, i, j);
                     u[p] = (f[p] - offdiag_dot(nx, a, u, i, j)) / a[O_];
                 }
+        }
+}
+
+void orc_relax(int nx, int ny, int kind, const double *st, const double *f, double *u, int nsweeps)
+{
+    relax_point(nx, ny, kind, st, f, u, nsweeps, 0);
+}
+
+void orc_relax_adjoint(int nx, int ny, int kind, const double *st, const double *f, double *u, int nsweeps)
+{
+    relax_point(nx, ny, kind, st, f, u, nsweeps, 1);
 }
 
 /*
@@ -339,7 +352,21 @@ static int thomas(int n, const double *lo, const double *di, const double *up, c
  * off it).  dir = ORC_ALTLINES: one sweep = an x-line sweep then a y-line
  * sweep.  Returns ORC_ENOTSPD if a line pivot is <= 0 (u then partial).
  */
+static int relax_lines(int nx, int ny, const double *st, const double *f, double *u, int nsweeps, int dir, int rev);
+
 int orc_relax_lines(int nx, int ny, const double *st, const double *f, double *u, int nsweeps, int dir)
+{
+    return relax_lines(nx, ny, st, f, u, nsweeps, dir, 0);
+}
+
+/* c12: the adjoint line smoother: each sweep runs its (direction, colour)
+ * passes in reverse order (y-lines before x-lines, colour 1 before 0). */
+int orc_relax_lines_adjoint(int nx, int ny, const double *st, const double *f, double *u, int nsweeps, int dir)
+{
+    return relax_lines(nx, ny, st, f, u, nsweeps, dir, 1);
+}
+
+static int relax_lines(int nx, int ny, const double *st, const double *f, double *u, int nsweeps, int dir, int rev)
 {
     int nmax = nx > ny ? nx : ny;
     double *lo = (double *)malloc(sizeof(double) * (size_t)nmax * 6);
@@ -348,15 +375,17 @@ int orc_relax_lines(int nx, int ny, const double *st, const double *f, double *u
     double *di = lo + nmax, *up = di + nmax, *rhs = up + nmax, *x = rhs + nmax, *gam = x + nmax;
     int rc = ORC_OK;
     for (int s = 0; s < nsweeps && rc == ORC_OK; s++) {
-        for (int pass = 0; pass < 2 && rc == ORC_OK; pass++) {
+        for (int pp = 0; pp < 2 && rc == ORC_OK; pp++) {
+            int pass = rev ? 1 - pp : pp;
             int on = pass == 0 ? (dir == ORC_XLINES || dir == ORC_ALTLINES) : (dir == ORC_YLINES || dir == ORC_ALTLINES);
             if (!on)
                 continue;
             int ylines = pass == 1;
             int nl = ylines ? nx : ny;  /* number of lines */
             int n = ylines ? ny : nx;   /* unknowns per line */
-            for (int c = 0; c < 2 && rc == ORC_OK; c++)
+            for (int cc = 0; cc < 2 && rc == ORC_OK; cc++)
                 for (int line = 1; line <= nl && rc == ORC_OK; line++) {
+                    int c = rev ? 1 - cc : cc;
                     if ((line & 1) != c)
                         continue;
                     for (int k = 0; k < n; k++) {
@@ -385,14 +414,16 @@ int orc_relax_lines(int nx, int ny, const double *st, const double *f, double *u
     return rc;
 }
 
-/* Relaxation of the cycle: point GS (c6) or line GS (c11) by mode. */
-static int relax_mode(int mode, int nx, int ny, int kind, const double *st, const double *f, double *u, int nsweeps)
+/* Relaxation of the cycle: point GS (c6) or line GS (c11) by mode; rev = 1
+ * the adjoint ordering (c12). */
+static int relax_mode(int mode, int nx, int ny, int kind, const double *st, const double *f, double *u, int nsweeps,
+                      int rev)
 {
     if (mode == ORC_POINT) {
-        orc_relax(nx, ny, kind, st, f, u, nsweeps);
+        relax_point(nx, ny, kind, st, f, u, nsweeps, rev);
         return ORC_OK;
     }
-    return orc_relax_lines(nx, ny, st, f, u, nsweeps, mode);
+    return relax_lines(nx, ny, st, f, u, nsweeps, mode, rev);
 }
 
 /* fig:vcycle_flowchart "Residual": r = f - A u on the interior; ring 0. */
@@ -546,7 +577,7 @@ typedef struct {
 } orc_level;
 
 typedef struct {
-    int L, nu1, nu2, relax;
+    int L, nu1, nu2, relax, cycle_sym;
     orc_level lv[ORC_MAXLEV];
     double *chol; /* coarsest L factor, n*n */
     int nco;
@@ -574,10 +605,11 @@ void orc_destroy(orc_hier *h)
  */
 int orc_setup(int nx, int ny, int kind, long pitch, const double *O, const double *W, const double *S,
               const double *SWp, const double *NWp, int nu1, int nu2, int coarsest, int max_levels, int relax,
-              orc_hier **out)
+              int cycle_sym, orc_hier **out)
 {
     *out = NULL;
-    if (nx < 1 || ny < 1 || (kind != 5 && kind != 9) || pitch < nx + 2 || relax < ORC_POINT || relax > ORC_ALTLINES)
+    if (nx < 1 || ny < 1 || (kind != 5 && kind != 9) || pitch < nx + 2 || relax < ORC_POINT || relax > ORC_ALTLINES ||
+        (cycle_sym != 0 && cycle_sym != 1))
         return ORC_EINVAL;
     orc_hier *h = (orc_hier *)calloc(1, sizeof(orc_hier));
     if (!h)
@@ -590,6 +622,7 @@ int orc_setup(int nx, int ny, int kind, long pitch, const double *O, const doubl
     h->nu1 = nu1;
     h->nu2 = nu2;
     h->relax = relax;
+    h->cycle_sym = cycle_sym;
     int cx = nx, cy = ny;
     for (int l = 0; l < h->L; l++) {
         orc_level *v = &h->lv[l];
@@ -682,7 +715,8 @@ static void coarse_solve(orc_hier *h, orc_level *c)
 
 /*
  * c9: V(nu1,nu2) cycle at level l (fig:vcycle_flowchart): relax nu1 (c6
- * point or c11 line GS, the hierarchy's mode; line pivots checked at setup), r = f -
+ * point or c11 line GS, the hierarchy's mode; line pivots checked at setup;
+ * with cycle_sym the post-smoother is the adjoint ordering, c12), r = f -
  * A u, f_{l+1} = P^T r, u_{l+1} = 0, recurse (coarsest: Cholesky solve),
  * u += P u_{l+1}, relax nu2.
  */
@@ -694,13 +728,13 @@ static void vcycle_level(orc_hier *h, int l)
         return;
     }
     orc_level *c = &h->lv[l + 1];
-    relax_mode(h->relax, v->nx, v->ny, v->kind, v->st, v->f, v->u, h->nu1);
+    relax_mode(h->relax, v->nx, v->ny, v->kind, v->st, v->f, v->u, h->nu1, 0);
     orc_residual(v->nx, v->ny, v->st, v->f, v->u, v->r);
     orc_restrict(v->nx, v->ny, v->ci, v->r, c->f);
     memset(c->u, 0, sizeof(double) * (size_t)(c->nx + 2) * (size_t)(c->ny + 2));
     vcycle_level(h, l + 1);
     orc_interp_add(v->nx, v->ny, v->ci, c->u, v->u);
-    relax_mode(h->relax, v->nx, v->ny, v->kind, v->st, v->f, v->u, h->nu2);
+    relax_mode(h->relax, v->nx, v->ny, v->kind, v->st, v->f, v->u, h->nu2, h->cycle_sym);
 }
 
 /* ncycles V-cycles on the fine level; f, u are (nx+2)*(ny+2), u in/out. */
@@ -751,6 +785,116 @@ int orc_solve(orc_hier *h, const double *f, double *u, double tol, int maxiter, 
         if (hist)
             hist[k] = rn;
     }
+    *iters = k;
+    return rn <= tol * fn ? ORC_OK : ORC_ENOTCONV;
+}
+
+/* ------------------------------------------------------------------------
+ * c13: V-cycle-preconditioned conjugate gradients (the
+ * Krylov acceleration Cedar offers around BoxMG)
+ * ---------------------------------------------------------------------- */
+
+/* q = A p on the interior (full stencil, fig:stencil_operator order); ring 0. */
+static void apply_A(int nx, int ny, const double *st, const double *p, double *q)
+{
+    memset(q, 0, sizeof(double) * (size_t)(nx + 2) * (size_t)(ny + 2));
+    for (int j = 1; j <= ny; j++)
+        for (int i = 1; i <= nx; i++) {
+            const double *a = st + 9 * gidx(nx, i, j);
+            size_t k = gidx(nx, i, j);
+            q[k] = a[O_] * p[k] + offdiag_dot(nx, a, p, i, j);
+        }
+}
+
+/* <a, b> over the interior, lexicographic summation. */
+static double dot_int(int nx, int ny, const double *a, const double *b)
+{
+    double s = 0.0;
+    for (int j = 1; j <= ny; j++)
+        for (int i = 1; i <= nx; i++)
+            s += a[gidx(nx, i, j)] * b[gidx(nx, i, j)];
+    return s;
+}
+
+/* z = M^{-1} r: one V-cycle of the hierarchy from a zero guess (c9). */
+static void precondition(orc_hier *h, const double *r, double *z)
+{
+    orc_level *v = &h->lv[0];
+    size_t np = (size_t)(v->nx + 2) * (size_t)(v->ny + 2);
+    memcpy(v->f, r, sizeof(double) * np);
+    memset(v->u, 0, sizeof(double) * np);
+    vcycle_level(h, 0);
+    memcpy(z, v->u, sizeof(double) * np);
+}
+
+/*
+ * Textbook PCG (Hestenes-Stiefel) with M^{-1} = one V(nu,nu) cycle from a zero
+ * guess; M is SPD when nu1 == nu2 and cycle_sym == 1 (the post-smoother is the
+ * adjoint of the pre-smoother, c12; R = P^T, Galerkin coarse operators, exact
+ * coarsest solve):
+ *   r = f - A x; z = M^{-1} r; p = z; rho = <r, z>
+ *   repeat: q = A p; alpha = rho / <p, q>; x += alpha p; r -= alpha q;
+ *           stop if ||r|| <= tol ||f||; z = M^{-1} r; rho' = <r, z>;
+ *           p = z + (rho'/rho) p; rho = rho'.
+ * hist[0] = ||f - A x0||, hist[k] = ||r_k|| of the recursively updated r.
+ * ORC_EINVAL unless nu1 == nu2 and cycle_sym == 1; ||f|| = 0 -> x = 0, 0 its;
+ * ORC_ENOTCONV at maxiter (x and hist valid).
+ */
+int orc_pcg(orc_hier *h, const double *f, double *x, double tol, int maxiter, int *iters, double *hist)
+{
+    orc_level *v = &h->lv[0];
+    int nx = v->nx, ny = v->ny;
+    size_t np = (size_t)(nx + 2) * (size_t)(ny + 2);
+    *iters = 0;
+    if (h->nu1 != h->nu2 || h->cycle_sym != 1)
+        return ORC_EINVAL;
+    double fn = orc_norm2(nx, ny, f);
+    if (fn == 0.0) {
+        memset(x, 0, sizeof(double) * np);
+        if (hist)
+            hist[0] = 0.0;
+        return ORC_OK;
+    }
+    double *r = (double *)calloc(4 * np, sizeof(double));
+    if (!r)
+        return ORC_ENOMEM;
+    double *z = r + np, *p = z + np, *q = p + np;
+    orc_residual(nx, ny, v->st, f, x, r);
+    double rn = orc_norm2(nx, ny, r);
+    if (hist)
+        hist[0] = rn;
+    int k = 0;
+    if (rn > tol * fn && maxiter > 0) {
+        precondition(h, r, z);
+        memcpy(p, z, sizeof(double) * np);
+        double rho = dot_int(nx, ny, r, z);
+        while (k < maxiter) {
+            apply_A(nx, ny, v->st, p, q);
+            double alpha = rho / dot_int(nx, ny, p, q);
+            for (int j = 1; j <= ny; j++)
+                for (int i = 1; i <= nx; i++) {
+                    size_t t = gidx(nx, i, j);
+                    x[t] += alpha * p[t];
+                    r[t] -= alpha * q[t];
+                }
+            k++;
+            rn = orc_norm2(nx, ny, r);
+            if (hist)
+                hist[k] = rn;
+            if (rn <= tol * fn)
+                break;
+            precondition(h, r, z);
+            double rho1 = dot_int(nx, ny, r, z);
+            double beta = rho1 / rho;
+            for (int j = 1; j <= ny; j++)
+                for (int i = 1; i <= nx; i++) {
+                    size_t t = gidx(nx, i, j);
+                    p[t] = z[t] + beta * p[t];
+                }
+            rho = rho1;
+        }
+    }
+    free(r);
     *iters = k;
     return rn <= tol * fn ? ORC_OK : ORC_ENOTCONV;
 }
