@@ -203,6 +203,8 @@ def main():
     ap.add_argument("--relax", default="point", choices=sorted(RELAX),
                     help="relaxation: point GS (c6, default) or zebra line GS (c11)")
     ap.add_argument("--solve-tol", type=float, default=None, help="tolerance of the timed solve (default per config)")
+    ap.add_argument("--pcg", type=int, default=0, metavar="NU",
+                    help="also time V(NU,NU)-preconditioned CG (symmetric cycle, c12/c13) on the same problem")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -326,6 +328,27 @@ def main():
                  "note": "x0 = 0; ms = wall clock of bmg_solve (norm + stopping test synchronised per cycle); "
                          "setup_ms = wall clock of bmg_setup (S0-S3 + graph-free allocation, synchronised)"}
         del xs
+        if args.pcg > 0:
+            # V-cycle-preconditioned CG (bmg_pcg) with the symmetric V(NU,NU) cycle
+            prm2 = bmg.bmg_params_default()
+            prm2.nu1 = prm2.nu2 = args.pcg
+            prm2.cycle_sym = 1
+            prm2.relax = prm.relax
+            s2 = bmg.Solver(P.workload(wl, nx, ny), prm2)
+            f2 = s2.grid(P.rhs_const(nx, ny))
+            x2 = s2.grid()
+            s2.pcg(f2, x2, tol, 2)  # warm-up: workspace + graph
+            x2.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            it2, h2, rc2 = s2.pcg(f2, x2, tol, SOLVE_MAXIT)
+            dt2 = time.perf_counter() - t0
+            solve["pcg"] = {"preconditioner": f"V({args.pcg},{args.pcg}) symmetric (cycle_sym=1)", "iterations": it2,
+                            "converged": rc2 == 0, "ms": dt2 * 1e3,
+                            "final_rel_residual": float(h2[-1] / fnorm) if len(h2) else None,
+                            "setup_ms": s2.setup_ms}
+            s2.close()
+            del f2, x2
 
     # e2e: the same metric through the public API with HOST buffers (pinned): per step
     # H2D of rhs and x, one V(2,1) cycle, D2H of x; host wall clock, max over ranks

@@ -69,7 +69,11 @@ typedef struct {
     int coarsest;    /* stop coarsening when min(nx,ny) <= coarsest; default 3 */
     int max_levels;  /* 0 = unlimited */
     int agglom_rows; /* multi-GPU: agglomerate below this many rows per rank (default 128) */
-    int cycle_sym;   /* 0 = same colour order on both legs (default); 1 reserved */
+    int cycle_sym;   /* 0 = same colour order on both legs (default); 1 = the post-smoother is
+                        the adjoint of the pre-smoother: colours (and, for alternating
+                        lines, directions) in reverse order (DESIGN §3 c12), so that
+                        V(nu,nu) is a symmetric operator (bmg_pcg's preconditioner).
+                        cycle_sym = 1 runs the per-step kernels on the large levels. */
     int fused;       /* 1 = fused streaming kernels on large levels (default), 0 = one kernel per step */
     int relax;       /* relaxation (fig:vcycle_flowchart's "Relaxation" boxes):
                         BMG_RELAX_POINT (default) multicolour point Gauss-Seidel (DESIGN §3 c6);
@@ -132,6 +136,20 @@ bmg_status_t bmg_vcycle_host(bmg_solver_t h, const double *rhs_host, double *x_h
  */
 bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol, int maxiter, int *iters_out,
                        double *hist_host, void *cuda_stream);
+
+/*
+ * Conjugate gradients preconditioned by one V(nu,nu) cycle from a zero guess
+ * ("V-cycle-preconditioned CG"; Cedar's Krylov use of
+ * BoxMG; DESIGN §3 c13): textbook PCG, r updated recursively,
+ * hist_host[0] = ||rhs - A x0||_2, hist_host[k] = ||r_k||_2; stops when
+ * ||r_k|| <= tol*||rhs|| (||rhs|| = 0: x = 0, 0 iterations).  Needs a
+ * symmetric preconditioner: params nu1 == nu2 and cycle_sym = 1 (EINVAL
+ * otherwise; single-GPU handles only).  Workspace: four level-0 arrays,
+ * allocated on the first call and owned by the handle.  Returns ENOTCONV at
+ * maxiter (x, hist valid).  Synchronises cuda_stream.
+ */
+bmg_status_t bmg_pcg(bmg_solver_t h, const double *rhs, double *x, double tol, int maxiter, int *iters_out,
+                     double *hist_host, void *cuda_stream);
 
 /* ||rhs - A x||_2 over the fine interior ("l2 norm"), deterministic
  * fixed-tree reduction; optional r_out (device, setup pitch, ring untouched)

@@ -21,7 +21,7 @@ BMG_OK, BMG_EINVAL, BMG_ENOMEM, BMG_ECUDA, BMG_ENCCL, BMG_ENOTSPD, BMG_ENOTCONV 
 
 # Every symbol include/bmg.h declares (checked by tests/test_abi.py).
 EXPORTS = (
-    "bmg_params_default", "bmg_setup", "bmg_vcycle", "bmg_vcycle_host", "bmg_solve", "bmg_residual_norm",
+    "bmg_params_default", "bmg_setup", "bmg_vcycle", "bmg_vcycle_host", "bmg_solve", "bmg_pcg", "bmg_residual_norm",
     "bmg_num_levels", "bmg_level_shape", "bmg_level_pitch", "bmg_export_level", "bmg_relax", "bmg_residual",
     "bmg_restrict", "bmg_interp_add", "bmg_smooth_restrict", "bmg_correct_smooth", "bmg_cycle_kernel_count", "bmg_timing",
     "bmg_timing_read", "bmg_destroy", "bmg_strerror",
@@ -76,6 +76,7 @@ def lib():
             "bmg_vcycle": (i, [vp, vp, vp, i, vp]),
             "bmg_vcycle_host": (i, [vp, vp, vp, i, vp]),
             "bmg_solve": (i, [vp, vp, vp, d, i, ip, dp, vp]),
+            "bmg_pcg": (i, [vp, vp, vp, d, i, ip, dp, vp]),
             "bmg_residual_norm": (i, [vp, vp, vp, vp, dp, vp]),
             "bmg_num_levels": (i, [vp, ip]),
             "bmg_level_shape": (i, [vp, i, ip, ip, ip]),
@@ -160,6 +161,16 @@ def bmg_solve(h, rhs, x, tol: float, maxiter: int, stream=None):
     rc = lib().bmg_solve(h, _ptr(rhs), _ptr(x), tol, maxiter, ctypes.byref(it),
                          hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream(stream))
     _check(rc, "bmg_solve", ok=(BMG_OK, BMG_ENOTCONV))
+    return it.value, hist[: it.value + 1], rc
+
+
+def bmg_pcg(h, rhs, x, tol: float, maxiter: int, stream=None):
+    """V-cycle-preconditioned CG.  Returns (iters, hist of iters+1 absolute norms, status)."""
+    it = ctypes.c_int()
+    hist = np.zeros(maxiter + 1)
+    rc = lib().bmg_pcg(h, _ptr(rhs), _ptr(x), tol, maxiter, ctypes.byref(it),
+                       hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream(stream))
+    _check(rc, "bmg_pcg", ok=(BMG_OK, BMG_ENOTCONV))
     return it.value, hist[: it.value + 1], rc
 
 
@@ -333,6 +344,9 @@ class Solver:
 
     def solve(self, rhs, x, tol, maxiter):
         return bmg_solve(self.h, rhs, x, tol, maxiter)
+
+    def pcg(self, rhs, x, tol, maxiter):
+        return bmg_pcg(self.h, rhs, x, tol, maxiter)
 
     def residual_norm(self, rhs, x):
         return bmg_residual_norm(self.h, rhs, x)

@@ -103,6 +103,7 @@ struct bmg_solver {
     long long dist_rows_total = 0;      // doubles of a level-0 rhs/x array of this handle
     int dist_local_ranks = 1;
     double *line_scr = nullptr;       // c11 line relaxation scratch (line modes only)
+    double *pcg_ws = nullptr;         // c13 PCG vectors r, z, p, q (level-0 arrays), lazily
     int tail_l0 = 1 << 30;            // first level of the tail kernel (none: > L)
     TailPlan *tail = nullptr;         // its device-side plan
     bool timing = false;              // bmg_timing: timed graph variant, event pair per launch
@@ -320,6 +321,7 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
             tp.L = h->L;
             tp.nu1 = h->prm.nu1;
             tp.nu2 = h->prm.nu2;
+            tp.cycle_sym = h->prm.cycle_sym;
             tp.chol = h->chol;
             for (int l = l0; l < h->L; l++) {
                 tp.lv[l].A = h->lv[l].op();
@@ -339,7 +341,7 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
     // fused streaming plan + ping-pong partner of u for every fused level above the tail
     for (int l = 0; l + 1 < h->L && l < 32 && l < h->tail_l0; l++) {
         Level &v = h->lv[l];
-        if (!h->prm.fused || h->prm.relax != BMG_RELAX_POINT)
+        if (!h->prm.fused || h->prm.relax != BMG_RELAX_POINT || h->prm.cycle_sym)
             break;
         TRY(fused_plan_level(h->fplan, l, v.nx, v.ny, v.pitch, v.kind, h->prm.nu1, h->prm.nu2, (v.pitch & 1) == 0));
         LevelPlan &lp = h->fplan.lv[l];
@@ -372,7 +374,7 @@ bmg_status_t bmg_setup(const bmg_stencil_t *st, const bmg_params_t *params, void
     else
         bmg_params_default(&h->prm);
     if (h->prm.nu1 < 0 || h->prm.nu2 < 0 || h->prm.coarsest < 1 || h->prm.relax < BMG_RELAX_POINT ||
-        h->prm.relax > BMG_RELAX_ALTLINES) {
+        h->prm.relax > BMG_RELAX_ALTLINES || (h->prm.cycle_sym != 0 && h->prm.cycle_sym != 1)) {
         delete h;
         return fail(BMG_EINVAL, "bad params");
     }
@@ -400,13 +402,15 @@ static bool use_fused(bmg_solver *h, int l, const void *f, const void *uin, cons
     return lp.down && lp.up && al16(f) && al16(uin) && al16(uout) && uin != uout;
 }
 
-// nsweeps sweeps of the handle's relaxation on level l (c6 point or c11 line GS)
-static void relax_level(bmg_solver *h, int l, const double *f, double *u, int nsweeps, cudaStream_t s, int *n)
+// nsweeps sweeps of the handle's relaxation on level l (c6 point or c11 line GS);
+// rev: the adjoint ordering (c12)
+static void relax_level(bmg_solver *h, int l, const double *f, double *u, int nsweeps, cudaStream_t s, int *n,
+                        bool rev = false)
 {
     if (h->prm.relax == BMG_RELAX_POINT)
-        launch_relax(h->lv[l].op(), f, u, nsweeps, s, n);
+        launch_relax(h->lv[l].op(), f, u, nsweeps, s, n, rev);
     else
-        launch_relax_lines(h->lv[l].op(), f, u, nsweeps, h->prm.relax, h->line_scr, s, n);
+        launch_relax_lines(h->lv[l].op(), f, u, nsweeps, h->prm.relax, h->line_scr, s, n, rev);
 }
 
 static void copy_level(bmg_solver *h, int l, double *dst, const double *src, cudaStream_t s)
@@ -440,7 +444,7 @@ static void enqueue_up(bmg_solver *h, int l, bool fused, const double *f, const 
     copy_level(h, l, uout, uin, s);
     launch_interp_add(v.op(), h->civ(l), ec, uout, s);
     *n += 1;
-    relax_level(h, l, f, uout, h->prm.nu2, s, n);
+    relax_level(h, l, f, uout, h->prm.nu2, s, n, h->prm.cycle_sym == 1);
 }
 
 // Enqueue one V(nu1,nu2) cycle (fig:vcycle_flowchart; DESIGN §3 c9) on s.
@@ -691,6 +695,91 @@ bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol,
         if (hist_host)
             hist_host[k] = rn;
     }
+    if (iters_out)
+        *iters_out = k;
+    return rn <= tol * fn ? BMG_OK : fail(BMG_ENOTCONV, "maxiter reached");
+}
+
+/*
+ * c13: conjugate gradients preconditioned by one V(nu,nu) cycle from a zero
+ * guess (symmetric with cycle_sym = 1, c12) -- the textbook PCG recurrences
+ * as DESIGN §3 c13 states them, every vector step a kernel, the scalars
+ * alpha, beta formed on the host from deterministic dot products.
+ */
+bmg_status_t bmg_pcg(bmg_solver_t h, const double *rhs, double *x, double tol, int maxiter, int *iters_out,
+                     double *hist_host, void *cuda_stream)
+{
+    if (!h || !rhs || !x || maxiter < 0 || !(tol >= 0))
+        return fail(BMG_EINVAL, "bad arguments to bmg_pcg");
+    if (h->dist)
+        return fail(BMG_EINVAL, "bmg_pcg: single-GPU handles only");
+    if (h->prm.nu1 != h->prm.nu2 || h->prm.cycle_sym != 1)
+        return fail(BMG_EINVAL, "bmg_pcg: the preconditioner must be symmetric (nu1 == nu2, cycle_sym = 1)");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    if (iters_out)
+        *iters_out = 0;
+    const Level &v = h->lv[0];
+    const Op A = v.op();
+    const size_t np = (size_t)(v.ny + 2) * (size_t)v.pitch;
+    if (!h->pcg_ws) {
+        TRY(dalloc(h, &h->pcg_ws, 4 * np));
+        CK(cudaMemsetAsync(h->pcg_ws, 0, 4 * np * sizeof(double), s));
+    }
+    double *r = h->pcg_ws, *z = r + np, *p = z + np, *q = p + np;
+    auto host_scalar = [&](double *out) -> bmg_status_t {
+        CK(cudaMemcpyAsync(h->h_norm, h->d_norm, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        *out = h->h_norm[0];
+        return BMG_OK;
+    };
+    double fn;
+    launch_norm(A, rhs, h->partials, h->d_norm, s);
+    TRY(host_scalar(&fn));
+    if (fn == 0.0) {
+        launch_zero_interior(A, x, s);
+        CK(cudaStreamSynchronize(s));
+        if (hist_host)
+            hist_host[0] = 0.0;
+        return BMG_OK;
+    }
+    double rn;
+    TRY(bmg_residual_norm(h, rhs, x, r, &rn, cuda_stream));  // r = f - A x0
+    if (hist_host)
+        hist_host[0] = rn;
+    int k = 0;
+    if (rn > tol * fn && maxiter > 0) {
+        auto precondition = [&]() -> bmg_status_t {  // z = one V-cycle on r from z = 0
+            launch_zero_interior(A, z, s);
+            return bmg_vcycle(h, r, z, 1, cuda_stream);
+        };
+        TRY(precondition());
+        CK(cudaMemcpyAsync(p, z, np * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        double rho;
+        launch_dot(A, r, z, h->partials, h->d_norm, s);
+        TRY(host_scalar(&rho));
+        while (k < maxiter) {
+            double pq;
+            launch_matvec(A, p, q, s);
+            launch_dot(A, p, q, h->partials, h->d_norm, s);
+            TRY(host_scalar(&pq));
+            const double alpha = rho / pq;
+            launch_cg_update(A, alpha, p, q, x, r, s);
+            k++;
+            launch_norm(A, r, h->partials, h->d_norm, s);
+            TRY(host_scalar(&rn));
+            if (hist_host)
+                hist_host[k] = rn;
+            if (rn <= tol * fn)
+                break;
+            TRY(precondition());
+            double rho1;
+            launch_dot(A, r, z, h->partials, h->d_norm, s);
+            TRY(host_scalar(&rho1));
+            launch_cg_direction(A, rho1 / rho, z, p, s);
+            rho = rho1;
+        }
+    }
+    CK(cudaGetLastError());
     if (iters_out)
         *iters_out = k;
     return rn <= tol * fn ? BMG_OK : fail(BMG_ENOTCONV, "maxiter reached");

@@ -103,7 +103,9 @@ void launch_assemble_dense(const Op &A, double *M, cudaStream_t s);
 void launch_chol_factor(int n, double *M, int *err, cudaStream_t s);
 void launch_coarse_solve(const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s);
 
-void launch_relax(const Op &A, const double *f, double *u, int nsweeps, cudaStream_t s, int *nlaunch);
+// rev: colours in descending order (the adjoint smoother of the symmetric cycle, c12)
+void launch_relax(const Op &A, const double *f, double *u, int nsweeps, cudaStream_t s, int *nlaunch,
+                  bool rev = false);
 void launch_residual(const Op &A, const double *f, const double *u, double *r, cudaStream_t s);
 void launch_restrict(const Op &A, const CIv &ci, const double *r, double *fc, double *uc, cudaStream_t s);
 void launch_interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s);
@@ -111,13 +113,19 @@ void launch_interp_add(const Op &A, const CIv &ci, const double *ec, double *u, 
 // line_scratch_doubles(nx, ny) doubles.  launch_line_pivots ORs ERR_LINE into
 // *err if a line block has a pivot <= 0.
 void launch_relax_lines(const Op &A, const double *f, double *u, int nsweeps, int mode, double *scr, cudaStream_t s,
-                        int *nlaunch);
+                        int *nlaunch, bool rev = false);
 void launch_line_pivots(const Op &A, int mode, int *err, cudaStream_t s);
 size_t line_scratch_doubles(int nx, int ny);
 void launch_resid_norm(const Op &A, const double *f, const double *u, double *r_out, double *partials,
                        double *result, cudaStream_t s);
 void launch_norm(const Op &A, const double *g, double *partials, double *result, cudaStream_t s);
 void launch_zero_interior(const Op &A, double *x, cudaStream_t s);
+// c13 PCG vector kernels (owned interior rows of A)
+void launch_matvec(const Op &A, const double *p, double *q, cudaStream_t s);
+void launch_dot(const Op &A, const double *a, const double *b, double *partials, double *result, cudaStream_t s);
+void launch_cg_update(const Op &A, double alpha, const double *p, const double *q, double *x, double *r,
+                      cudaStream_t s);
+void launch_cg_direction(const Op &A, double beta, const double *z, double *p, cudaStream_t s);
 
 // Small levels l0..L-1 of the cycle in one single-CTA launch (k_tail).  Lives in
 // device memory (filled once at setup); level 0's f/u are launch arguments.
@@ -128,6 +136,7 @@ struct TailLevel {
 };
 struct TailPlan {
     int l0, L, nu1, nu2;
+    int cycle_sym;         // 1: post-smoother colours reversed (c12)
     const double *chol;    // coarsest Cholesky factor
     TailLevel lv[32];
 };

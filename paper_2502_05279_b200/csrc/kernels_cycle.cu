@@ -80,20 +80,20 @@ __global__ void k_relax9(Op A, const double *__restrict__ f, double *__restrict_
     relax9_pt(A, f, u, i, j);
 }
 
-void launch_relax(const Op &A, const double *f, double *u, int nsweeps, cudaStream_t s, int *nlaunch)
+void launch_relax(const Op &A, const double *f, double *u, int nsweeps, cudaStream_t s, int *nlaunch, bool rev)
 {
     dim3 b(32, 8);
     for (int sw = 0; sw < nsweeps; sw++) {
         if (A.kind == 5) {
             dim3 g((A.nx / 2 + 1 + 31) / 32, (A.ny + 7) / 8);
             for (int c = 0; c < 2; c++)
-                k_relax5<<<g, b, 0, s>>>(A, f, u, c);
+                k_relax5<<<g, b, 0, s>>>(A, f, u, rev ? 1 - c : c);
             if (nlaunch)
                 *nlaunch += 2;
         } else {
             dim3 g((A.nx / 2 + 1 + 31) / 32, (A.ny / 2 + 1 + 7) / 8);
             for (int c = 0; c < 4; c++)
-                k_relax9<<<g, b, 0, s>>>(A, f, u, c);
+                k_relax9<<<g, b, 0, s>>>(A, f, u, rev ? 3 - c : c);
             if (nlaunch)
                 *nlaunch += 4;
         }
@@ -293,6 +293,97 @@ void launch_norm(const Op &A, const double *g, double *partials, double *result,
     k_norm_final<<<1, 1024, 0, s>>>(partials, NORM_BLOCKS, result);
 }
 
+// ---------------------------------------------------------------- PCG vectors (c13)
+// q = A p on the owned interior (ring of q untouched).
+__global__ void k_matvec(Op A, const double *__restrict__ p, double *__restrict__ q)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y + A.ylo;
+    if (i > A.nx || j >= A.yhi)
+        return;
+    const long long P = A.pitch, k = j * P + i;
+    const Row9 a = load_row9(A, k);
+    q[k] = a.o * p[k] + offdiag(a, p, k, P);
+}
+
+// <a, b> over the owned interior: the fixed-tree partials of the norms above.
+__global__ void k_dot_partial(Op A, const double *__restrict__ a, const double *__restrict__ b,
+                              double *__restrict__ partials)
+{
+    double acc = 0.0;
+    const long long P = A.pitch;
+    for (int j = A.ylo + blockIdx.x; j < A.yhi; j += gridDim.x)
+        for (int i = 1 + threadIdx.x; i <= A.nx; i += blockDim.x)
+            acc = fma(a[j * P + i], b[j * P + i], acc);
+    acc = block_sum(acc);
+    if (threadIdx.x == 0)
+        partials[blockIdx.x] = acc;
+}
+
+__global__ void k_sum_final(const double *__restrict__ partials, int n, double *result)
+{
+    double acc = 0.0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x)
+        acc += partials[k];
+    acc = block_sum(acc);
+    if (threadIdx.x == 0)
+        *result = acc;
+}
+
+// x += alpha p; r -= alpha q  (interior)
+__global__ void k_cg_update(Op A, double alpha, const double *__restrict__ p, const double *__restrict__ q,
+                            double *__restrict__ x, double *__restrict__ r)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y + A.ylo;
+    if (i > A.nx || j >= A.yhi)
+        return;
+    const long long k = j * A.pitch + i;
+    x[k] = fma(alpha, p[k], x[k]);
+    r[k] = fma(-alpha, q[k], r[k]);
+}
+
+// p = z + beta p  (interior)
+__global__ void k_cg_direction(Op A, double beta, const double *__restrict__ z, double *__restrict__ p)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y + A.ylo;
+    if (i > A.nx || j >= A.yhi)
+        return;
+    const long long k = j * A.pitch + i;
+    p[k] = fma(beta, p[k], z[k]);
+}
+
+static dim3 interior_grid(const Op &A, dim3 b)
+{
+    return dim3((A.nx + b.x - 1) / b.x, (A.yhi - A.ylo + b.y - 1) / b.y);
+}
+
+void launch_matvec(const Op &A, const double *p, double *q, cudaStream_t s)
+{
+    const dim3 b(32, 8);
+    k_matvec<<<interior_grid(A, b), b, 0, s>>>(A, p, q);
+}
+
+void launch_dot(const Op &A, const double *a, const double *b, double *partials, double *result, cudaStream_t s)
+{
+    k_dot_partial<<<NORM_BLOCKS, 256, 0, s>>>(A, a, b, partials);
+    k_sum_final<<<1, 1024, 0, s>>>(partials, NORM_BLOCKS, result);
+}
+
+void launch_cg_update(const Op &A, double alpha, const double *p, const double *q, double *x, double *r,
+                      cudaStream_t s)
+{
+    const dim3 b(32, 8);
+    k_cg_update<<<interior_grid(A, b), b, 0, s>>>(A, alpha, p, q, x, r);
+}
+
+void launch_cg_direction(const Op &A, double beta, const double *z, double *p, cudaStream_t s)
+{
+    const dim3 b(32, 8);
+    k_cg_direction<<<interior_grid(A, b), b, 0, s>>>(A, beta, z, p);
+}
+
 // ---------------------------------------------------------------- coarsest solve
 // u = A_L^{-1} f with the setup Cholesky factor: forward then backward
 // substitution (fig:vcycle_flowchart "Cholesky"), one CTA, the
@@ -349,13 +440,14 @@ void launch_coarse_solve(const Op &A, const double *Lf, const double *f, double 
 // bitwise that of the per-step path.  Replaces ~4 launches per small level,
 // each bounded by launch latency rather than by its few thousand points.
 template <int KIND>
-__device__ __forceinline__ void tail_relax(const Op &A, const double *f, double *u, int nsweeps)
+__device__ __forceinline__ void tail_relax(const Op &A, const double *f, double *u, int nsweeps, bool rev)
 {
     const int nt = blockDim.x;
     for (int sw = 0; sw < nsweeps; sw++) {
         if (KIND == 5) {
             const int half = A.nx / 2 + 1, cnt = half * A.ny;
-            for (int c = 0; c < 2; c++) {
+            for (int cc = 0; cc < 2; cc++) {
+                const int c = rev ? 1 - cc : cc;
                 for (int k = threadIdx.x; k < cnt; k += nt) {
                     const int j = k / half + 1, i = (((1 + j) & 1) == c ? 1 : 2) + 2 * (k % half);
                     if (i <= A.nx)
@@ -365,7 +457,8 @@ __device__ __forceinline__ void tail_relax(const Op &A, const double *f, double 
             }
         } else {
             const int hx = A.nx / 2 + 1, hy = A.ny / 2 + 1, cnt = hx * hy;
-            for (int c = 0; c < 4; c++) {
+            for (int cc = 0; cc < 4; cc++) {
+                const int c = rev ? 3 - cc : cc;
                 for (int k = threadIdx.x; k < cnt; k += nt) {
                     const int j = 2 * (k / hx) + ((c >> 1) ? 1 : 2), i = 2 * (k % hx) + ((c & 1) ? 1 : 2);
                     if (i <= A.nx && j <= A.ny)
@@ -389,9 +482,9 @@ __global__ void __launch_bounds__(1024, 1) k_tail(const TailPlan *__restrict__ t
         const double *f = F(l);
         double *u = U(l), *r = tp->lv[l].r;
         if (A.kind == 5)
-            tail_relax<5>(A, f, u, tp->nu1);
+            tail_relax<5>(A, f, u, tp->nu1, false);
         else
-            tail_relax<9>(A, f, u, tp->nu1);
+            tail_relax<9>(A, f, u, tp->nu1, false);
         const int wx = A.nx + 2, cnt = wx * (A.ny + 2);
         for (int k = threadIdx.x; k < cnt; k += nt) {
             const int j = k / wx, i = k % wx;
@@ -418,9 +511,9 @@ __global__ void __launch_bounds__(1024, 1) k_tail(const TailPlan *__restrict__ t
         }
         __syncthreads();
         if (A.kind == 5)
-            tail_relax<5>(A, F(l), u, tp->nu2);
+            tail_relax<5>(A, F(l), u, tp->nu2, tp->cycle_sym);
         else
-            tail_relax<9>(A, F(l), u, tp->nu2);
+            tail_relax<9>(A, F(l), u, tp->nu2, tp->cycle_sym);
     }
 }
 

@@ -464,16 +464,21 @@ static void colour_pass(const Op &A, const double *f, double *u, double *scr, in
         *nlaunch += n;
 }
 
+// rev (c12, the adjoint sweep): the (direction, colour) passes in reverse order
 void launch_relax_lines(const Op &A, const double *f, double *u, int nsweeps, int mode, double *scr, cudaStream_t s,
-                        int *nlaunch)
+                        int *nlaunch, bool rev)
 {
+    const bool X = mode == RELAX_XLINES || mode == RELAX_ALTLINES, Yd = mode == RELAX_YLINES || mode == RELAX_ALTLINES;
     for (int sw = 0; sw < nsweeps; sw++) {
-        if (mode == RELAX_XLINES || mode == RELAX_ALTLINES)
-            for (int c = 0; c < 2; c++)
-                colour_pass<0>(A, f, u, scr, c, s, nlaunch);
-        if (mode == RELAX_YLINES || mode == RELAX_ALTLINES)
-            for (int c = 0; c < 2; c++)
-                colour_pass<1>(A, f, u, scr, c, s, nlaunch);
+        for (int pp = 0; pp < 2; pp++) {
+            const int pass = rev ? 1 - pp : pp;
+            if (pass == 0 && X)
+                for (int c = 0; c < 2; c++)
+                    colour_pass<0>(A, f, u, scr, rev ? 1 - c : c, s, nlaunch);
+            if (pass == 1 && Yd)
+                for (int c = 0; c < 2; c++)
+                    colour_pass<1>(A, f, u, scr, rev ? 1 - c : c, s, nlaunch);
+        }
     }
 }
 
