@@ -211,7 +211,8 @@ bmg_status_t bmg_cycle_kernel_count(bmg_solver_t h, int *count);
 
 /* Measurement hook (bench.py's roofline figure).  enable != 0: subsequent
  * bmg_vcycle calls on this single-GPU handle replay a variant of the cycle's
- * graph with two event-record nodes around the level-0 down-leg launch, each
+ * graph with two event-record nodes around the level-0 down-leg launch (or, when
+ * the single-CTA tail kernel starts at level 0, around that launch), each
  * launch re-pointed at a fresh CUDA event pair (timed on the caller's stream);
  * enable == 0 returns to the plain graph.  Either call clears the records.
  * bmg_timing_read waits for the recorded events and returns the summed

@@ -484,6 +484,11 @@ static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream
         if (rec && l == 0)
             cudaEventRecordWithFlags(rec[1], s, cudaEventRecordExternal);
     }
+    // no level-0 down leg of its own (the tail or the coarse solve starts at level 0):
+    // bmg_timing records around that launch instead
+    const bool rec_here = rec && lt == 0;
+    if (rec_here)
+        cudaEventRecordWithFlags(rec[0], s, cudaEventRecordExternal);
     if (h->tail) {
         launch_tail(h->tail, h->nco, F(0), U(0), s);
         n += 1;
@@ -492,6 +497,8 @@ static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream
         launch_coarse_solve(c.op(), h->chol, F(L - 1), U(L - 1), s);
         n += 1;
     }
+    if (rec_here)
+        cudaEventRecordWithFlags(rec[1], s, cudaEventRecordExternal);
     for (int l = lt - 1; l >= 0; l--)
         enqueue_up(h, l, fz[l], F(l), fz[l] ? h->fplan.tmp[l] : U(l), h->lv[l + 1].u, U(l), s, &n);
     return n;
