@@ -474,8 +474,11 @@ def roofline(leg, nx, ny, kind, peak, peak_src, ms_per_step, args):
                 "unit": "GB/s", "frac": None, "traffic": None, "launch_ms": dur_ms, "launches_timed": launches,
                 "share_of_step": dur_ms / ms_per_step}
     s_planes = 3 if kind == 5 else 5
-    # compulsory bytes of the down leg per fine unknown: read u, f and the
-    # s operator planes, write u, read the 2N-double CI planes, write f_c and zero u_c (N/4 each)
+    # algorithmic bytes of the down leg per fine unknown = SURVEY §8(d) model A's
+    # down-leg share: read u, f and the s operator planes, write u, read the
+    # 2N-double CI planes of fig:restrict_kernel, write f_c and zero u_c (N/4 each).
+    # The kernel itself reads only the half of the CI planes whose residual does not
+    # vanish, so this is an effective bandwidth; `traffic` is the real one.
     per_unk = 8.0 * (s_planes + 2 + 1 + 2 + 0.25 + 0.25)
     if args.relax != "point":
         # per-step kernels: every line sweep direction reads the s planes, f and

@@ -430,7 +430,8 @@ static void enqueue_down(bmg_solver *h, int l, bool fused, const double *f, cons
     copy_level(h, l, uout, uin, s);
     relax_level(h, l, f, uout, h->prm.nu1, s, n);
     launch_residual(v.op(), f, uout, v.r, s);
-    launch_restrict(v.op(), h->civ(l), v.r, fc, uc, s);
+    // after nu1 >= 1 point-GS sweeps the last colour's residual vanishes
+    launch_restrict(v.op(), h->civ(l), v.r, fc, uc, s, h->prm.relax == BMG_RELAX_POINT && h->prm.nu1 > 0);
     *n += 2;
 }
 
@@ -869,9 +870,10 @@ bmg_status_t bmg_export_level(bmg_solver_t h, int level, double *stencil_host, d
     if (ci_host && level + 1 < h->L) {
         Level &c = h->lv[level + 1];
         size_t cw = (size_t)c.nx + 2, crows = (size_t)c.ny + 2;
+        const int api_order[8] = {CI_LNE, CI_LA, CI_LNW, CI_LR, CI_LL, CI_LSE, CI_LB, CI_LSW};
         for (int k = 0; k < 8; k++)
-            CK(cudaMemcpy2D(ci_host + k * cw * crows, cw * sizeof(double), v.ci[k], c.pitch * sizeof(double),
-                            cw * sizeof(double), crows, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy2D(ci_host + k * cw * crows, cw * sizeof(double), v.ci[api_order[k]],
+                            c.pitch * sizeof(double), cw * sizeof(double), crows, cudaMemcpyDeviceToHost));
     }
     return BMG_OK;
 }

@@ -14,7 +14,11 @@
 
 namespace bmg {
 
-enum { CI_LNE = 0, CI_LA = 1, CI_LNW = 2, CI_LR = 3, CI_LL = 4, CI_LSE = 5, CI_LB = 6, CI_LSW = 7 };
+// Storage order of the 8 weight planes: the Z-point (corner) weights first, then
+// the X/Y (edge) weights, so that each half is one contiguous block (the fused
+// down legs fetch only the half their restriction needs).
+// bmg_export_level reorders to the API order LNE,LA,LNW,LR,LL,LSE,LB,LSW.
+enum { CI_LNE = 0, CI_LNW = 1, CI_LSE = 2, CI_LSW = 3, CI_LR = 4, CI_LL = 5, CI_LA = 6, CI_LB = 7 };
 
 // error bits raised by setup kernels (device int, OR-ed)
 enum { ERR_DIAG = 1, ERR_DEN = 2, ERR_PIVOT = 4, ERR_LINE = 8 };
@@ -107,7 +111,10 @@ void launch_coarse_solve(const Op &A, const double *Lf, const double *f, double 
 void launch_relax(const Op &A, const double *f, double *u, int nsweeps, cudaStream_t s, int *nlaunch,
                   bool rev = false);
 void launch_residual(const Op &A, const double *f, const double *u, double *r, cudaStream_t s);
-void launch_restrict(const Op &A, const CIv &ci, const double *r, double *fc, double *uc, cudaStream_t s);
+// vanish: r is the residual right after a point-GS sweep; the terms of the colour
+// relaxed last (zero residual) are skipped, as in the fused down leg
+void launch_restrict(const Op &A, const CIv &ci, const double *r, double *fc, double *uc, cudaStream_t s,
+                     bool vanish = false);
 void launch_interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s);
 // c11 zebra line GS (kernels_line.cu): nsweeps sweeps in `mode`; scr holds
 // line_scratch_doubles(nx, ny) doubles.  launch_line_pivots ORs ERR_LINE into

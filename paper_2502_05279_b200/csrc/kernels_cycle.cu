@@ -140,30 +140,61 @@ __device__ __forceinline__ double restrict_pt(const Op &A, const CIv &ci, const 
     return v;
 }
 
-// coarse point (I, J), 0 <= I <= ncx+1, 0 <= J <= ncy+1: qc (0 on the ring) and uc = 0
+// The same listing without the terms whose residual vanishes after a point-GS
+// sweep (the colour relaxed last was solved against its final neighbours, DESIGN
+// §5.2): 5-point levels keep the centre and the Z (corner) terms, 9-point levels
+// the centre and the X/Y terms -- term for term the fused down leg's restriction.
+__device__ __forceinline__ double restrict_pt_vanish(const Op &A, const CIv &ci, const double *__restrict__ q, int I,
+                                                     int J)
+{
+    long long C = ci.pitch, c = J * C + I;
+    long long P = A.pitch, p = (2 * J) * P + 2 * I;
+    double v;
+    if (A.kind == 5) {
+        v = ci.w[CI_LNE][c] * q[p - P - 1];
+        v += ci.w[CI_LNW][c + 1] * q[p - P + 1];
+        v += q[p];
+        v += ci.w[CI_LSE][c + C] * q[p + P - 1];
+        v += ci.w[CI_LSW][c + C + 1] * q[p + P + 1];
+    } else {
+        v = ci.w[CI_LA][c] * q[p - P];
+        v += ci.w[CI_LR][c] * q[p - 1];
+        v += q[p];
+        v += ci.w[CI_LL][c + 1] * q[p + 1];
+        v += ci.w[CI_LB][c + C] * q[p + P];
+    }
+    return v;
+}
+
+// coarse point (I, J), 0 <= I <= ncx+1, 0 <= J <= ncy+1: qc (0 on the ring) and uc = 0;
+// vanish: q is a residual right after a point-GS sweep (restrict_pt_vanish)
 __device__ __forceinline__ void restrict_store(const Op &A, const CIv &ci, const double *__restrict__ q,
-                                               double *__restrict__ qc, double *__restrict__ uc, int I, int J)
+                                               double *__restrict__ qc, double *__restrict__ uc, int I, int J,
+                                               bool vanish = false)
 {
     int ncx = A.nx / 2, ncy = A.ny / 2;
     long long c = J * ci.pitch + I;
     if (uc)
         uc[c] = 0.0;
-    qc[c] = (I == 0 || J == 0 || I > ncx || J > ncy) ? 0.0 : restrict_pt(A, ci, q, I, J);
+    qc[c] = (I == 0 || J == 0 || I > ncx || J > ncy)
+                ? 0.0
+                : (vanish ? restrict_pt_vanish(A, ci, q, I, J) : restrict_pt(A, ci, q, I, J));
 }
 
-__global__ void k_restrict(Op A, CIv ci, const double *__restrict__ q, double *__restrict__ qc, double *__restrict__ uc)
+__global__ void k_restrict(Op A, CIv ci, const double *__restrict__ q, double *__restrict__ qc, double *__restrict__ uc,
+                           bool vanish)
 {
     int I = blockIdx.x * blockDim.x + threadIdx.x;
     int J = blockIdx.y * blockDim.y + threadIdx.y;
     if (I > A.nx / 2 + 1 || J > A.ny / 2 + 1)
         return;
-    restrict_store(A, ci, q, qc, uc, I, J);
+    restrict_store(A, ci, q, qc, uc, I, J, vanish);
 }
 
-void launch_restrict(const Op &A, const CIv &ci, const double *r, double *fc, double *uc, cudaStream_t s)
+void launch_restrict(const Op &A, const CIv &ci, const double *r, double *fc, double *uc, cudaStream_t s, bool vanish)
 {
     dim3 b(32, 8), g((A.nx / 2 + 2 + 31) / 32, (A.ny / 2 + 2 + 7) / 8);
-    k_restrict<<<g, b, 0, s>>>(A, ci, r, fc, uc);
+    k_restrict<<<g, b, 0, s>>>(A, ci, r, fc, uc, vanish);
 }
 
 // (P e) at fine interior point (i, j) (DESIGN §3 c7); e's ring is 0.
@@ -494,7 +525,7 @@ __global__ void __launch_bounds__(1024, 1) k_tail(const TailPlan *__restrict__ t
         __syncthreads();
         const int cx = A.nx / 2 + 2, ccnt = cx * (A.ny / 2 + 2);
         for (int k = threadIdx.x; k < ccnt; k += nt)
-            restrict_store(A, ci, r, tp->lv[l + 1].f, tp->lv[l + 1].u, k % cx, k / cx);
+            restrict_store(A, ci, r, tp->lv[l + 1].f, tp->lv[l + 1].u, k % cx, k / cx, tp->nu1 > 0);
         __syncthreads();
     }
     coarse_solve_cta(tp->lv[L - 1].A, tp->chol, F(L - 1), U(L - 1), b);

@@ -119,6 +119,12 @@ struct Cfg {
     static constexpr int NM = NA + 1;                           // main-ring arrays: + 1/O
     static constexpr int A_DI = NA;                             // main-ring index of 1/O
     static constexpr int CSL = UP ? 4 : 3;                      // coarse-row ring slots
+    // weight planes per coarse row: the up leg interpolates with all 8; the down
+    // leg restricts a residual that vanishes on the colour relaxed last (DESIGN
+    // §5.2), so it needs only the other half: the 4 Z-point weights (5-point
+    // levels) or the 4 X/Y weights (9-point levels), one contiguous block
+    static constexpr int NWP = UP ? 8 : 4;
+    static constexpr int WP0 = UP ? 0 : (KIND == 5 ? CI_LNE : CI_LR);  // first plane fetched
     static constexpr int PASSES = KIND == 5 ? NS : 2 * NS;      // colour passes (x halo shrink)
     static constexpr int H0 = UP ? PASSES : PASSES + 2;         // + residual + restriction
     static constexpr int H = ((H0 < 2 ? 2 : H0) + 1) & ~1;      // even (16-byte TMA alignment)
@@ -135,7 +141,7 @@ struct Cfg {
     static constexpr int NTW = NG * NPG;                       // worker threads
     static constexpr int NT = NTW + 32;                        // + one TMA producer warp
     static constexpr size_t SMEM_DBL =
-        (size_t)NM * AM + (size_t)NA * AS + (UP ? 4 * (size_t)WC : 4 * (size_t)WD) + 8 * CSL * (size_t)WC;
+        (size_t)NM * AM + (size_t)NA * AS + (UP ? 4 * (size_t)WC : 4 * (size_t)WD) + (size_t)NWP * CSL * (size_t)WC;
     static constexpr size_t SMEM = SMEM_DBL * 8 + (SD + 4 + (size_t)NG * NSLOT) * 8;
     static_assert(TX % 4 == 0 && TX > 0, "strip width");
     static_assert(NPG % 32 == 0, "task groups must be whole warps");
@@ -381,7 +387,7 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
     double *smS = sm + C::NM * AM;              // staging ring (natural rows)
     double *sR = smS + NA * AS;                 // residual ring [4][WD], split
     double *sC = sR + 4 * WD;                   // weights ring [4][8][WC]
-    uint64_t *bar = (uint64_t *)(sC + 8 * C::CSL * WC); // SD staging + 4 coarse
+    uint64_t *bar = (uint64_t *)(sC + C::NWP * C::CSL * WC); // SD staging + 4 coarse
 
     const int nx = a.A.nx, ny = a.A.ny, ncx = a.ncx;
     const long long P = a.A.pitch, CP = a.ci.pitch;
@@ -451,8 +457,8 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
                 break;
             const int slot = (Knext - Jlo) % C::CSL;
             uint64_t *b = &bar[SD + slot];
-            mbar_arrive_tx(b, (uint32_t)(8 * WC * 8));
-            tma_3d(sC + slot * 8 * WC, &tmaps.c, cxl, Knext - a.ci.roff, 0, b);
+            mbar_arrive_tx(b, (uint32_t)(C::NWP * WC * 8));
+            tma_3d(sC + slot * C::NWP * WC, &tmaps.c, cxl, Knext - a.ci.roff, C::WP0, b);
             Knext++;
         }
     };
@@ -480,6 +486,11 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
     };
     auto resid_task = [&](int rr, int s0, int sm1, int sp1, int e) {
         if (rr < ya - 1 || rr > yb || rr < 0 || rr > ny + 1)
+            return;
+        // the colour relaxed last has zero residual (each of its points was just
+        // solved against final neighbours of the other colours); the restriction
+        // never reads it: 5-point black (i + rr odd), 9-point colour 3 (i, rr odd)
+        if (KIND == 5 ? ((e + rr) & 1) : (e & rr & 1))
             return;
         if (e)
             resid_par(rr, s0, sm1, sp1, std::integral_constant<int, 1>());
@@ -515,7 +526,8 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
         mbar_wait(&bar[SD + (J + 1 - Jlo) % CS], ((J + 1 - Jlo) / CS) & 1);
         const double *rm = sR + ((2 * J - 1) & 3) * WD, *r0 = sR + ((2 * J) & 3) * WD,
                      *rp = sR + ((2 * J + 1) & 3) * WD;
-        const double *c0 = sC + ((J - Jlo) % CS) * 8 * WC, *c1 = sC + ((J + 1 - Jlo) % CS) * 8 * WC;
+        constexpr int NW = C::NWP, P0 = C::WP0;  // weight planes in the ring slots: [P0, P0 + NW)
+        const double *c0 = sC + ((J - Jlo) % CS) * NW * WC, *c1 = sC + ((J + 1 - Jlo) % CS) * NW * WC;
 #pragma unroll
         for (int p = 0; p < PPT; p++) {
             const int h = m + p * NPG;
@@ -523,16 +535,24 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
             if (I < x0 / 2 || I >= x0 / 2 + TX / 2 || I < 1 || I > ncx)
                 continue;
             const int ic = I - cxl;
-            // split residual rows: column 2h -> [h], 2h-1 -> [HW+h-1], 2h+1 -> [HW+h]
-            double v = c0[CI_LNE * WC + ic] * rm[HW + h - 1];
-            v += c0[CI_LA * WC + ic] * rm[h];
-            v += c0[CI_LNW * WC + ic + 1] * rm[HW + h];
-            v += c0[CI_LR * WC + ic] * r0[HW + h - 1];
-            v += r0[h];
-            v += c0[CI_LL * WC + ic + 1] * r0[HW + h];
-            v += c1[CI_LSE * WC + ic] * rp[HW + h - 1];
-            v += c1[CI_LB * WC + ic] * rp[h];
-            v += c1[CI_LSW * WC + ic + 1] * rp[HW + h];
+            // split residual rows: column 2h -> [h], 2h-1 -> [HW+h-1], 2h+1 -> [HW+h].
+            // fig:restrict_kernel's terms in listing order, without those whose
+            // residual vanishes: 5-point levels keep the centre and the four Z
+            // (corner) terms, 9-point levels the centre and the four X/Y terms.
+            double v;
+            if (KIND == 5) {
+                v = c0[(CI_LNE - P0) * WC + ic] * rm[HW + h - 1];
+                v += c0[(CI_LNW - P0) * WC + ic + 1] * rm[HW + h];
+                v += r0[h];
+                v += c1[(CI_LSE - P0) * WC + ic] * rp[HW + h - 1];
+                v += c1[(CI_LSW - P0) * WC + ic + 1] * rp[HW + h];
+            } else {
+                v = c0[(CI_LA - P0) * WC + ic] * rm[h];
+                v += c0[(CI_LR - P0) * WC + ic] * r0[HW + h - 1];
+                v += r0[h];
+                v += c0[(CI_LL - P0) * WC + ic + 1] * r0[HW + h];
+                v += c1[(CI_LB - P0) * WC + ic] * rp[h];
+            }
             a.fc[(long long)J * CP + I] = v;
             if (a.uc)
                 a.uc[(long long)J * CP + I] = 0.0;
@@ -1046,16 +1066,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
 }
 
 // rank-3 fp64 map over `planes` planes of rows x width elements (row pitch, plane
-// stride in elements); box = bw columns x 1 row x planes.  Rank 2 when planes == 0.
+// stride in elements); box = bw columns x 1 row x bz planes (bz = 0: all planes).
+// Rank 2 when planes == 0.
 static bool make_map(CUtensorMap *m, const double *base, long long width, long long rows, long long pitch,
-                     long long pstride, int planes, int bw)
+                     long long pstride, int planes, int bw, int bz = 0)
 {
     auto fn = encode_fn();
     if (!fn)
         return false;
     cuuint64_t dims[3] = {(cuuint64_t)width, (cuuint64_t)rows, (cuuint64_t)(planes > 0 ? planes : 1)};
     cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)pstride * 8};
-    cuuint32_t box[3] = {(cuuint32_t)bw, 1, (cuuint32_t)(planes > 0 ? planes : 1)};
+    cuuint32_t box[3] = {(cuuint32_t)bw, 1, (cuuint32_t)(planes > 0 ? (bz > 0 ? bz : planes) : 1)};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, planes > 0 ? 3 : 2, (void *)base, dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1081,7 +1102,8 @@ static bool make_maps(TMaps &tm, const FusedGeom &g, const Op &A, const CIv &ci,
     bool ok = make_map(&tm.u, uin + A.roff * A.pitch, A.nx + 2, A.nrows, A.pitch, 0, 0, g.WD) &&
               make_map(&tm.f, f + A.roff * A.pitch, A.nx + 2, A.nrows, A.pitch, 0, 0, g.WD) &&
               make_map(&tm.a, A.O + A.roff * A.pitch, A.nx + 2, A.nrows, A.pitch, np, npl, g.WD) &&
-              make_map(&tm.c, ci.w[0] + ci.roff * ci.pitch, ncx + 2, ci.nrows, ci.pitch, npc, 8, g.WC);
+              // the down leg (ec == nullptr) fetches 4 of the 8 weight planes per coarse row
+              make_map(&tm.c, ci.w[0] + ci.roff * ci.pitch, ncx + 2, ci.nrows, ci.pitch, npc, 8, g.WC, ec ? 8 : 4);
     if (ok && ec)
         ok = make_map(&tm.e, ec + (long long)eroff * ci.pitch, ncx + 2, enrows, ci.pitch, 0, 0, g.WC);
     else
