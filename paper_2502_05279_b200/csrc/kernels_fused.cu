@@ -123,8 +123,11 @@ struct Cfg {
     // leg restricts a residual that vanishes on the colour relaxed last (DESIGN
     // §5.2), so it needs only the other half: the 4 Z-point weights (5-point
     // levels) or the 4 X/Y weights (9-point levels), one contiguous block
-    static constexpr int NWP = UP ? 8 : 4;
-    static constexpr int WP0 = UP ? 0 : (KIND == 5 ? CI_LNE : CI_LR);  // first plane fetched
+    // The up leg's first colour pass recomputes its points from the other colours
+    // only, so their correction is never read: a 5-point up leg corrects only X/Y
+    // points (4 X/Y weight planes); a 9-point one skips the C injection (all 8).
+    static constexpr int NWP = UP ? (KIND == 5 ? 4 : 8) : 4;
+    static constexpr int WP0 = UP ? (KIND == 5 ? CI_LR : 0) : (KIND == 5 ? CI_LNE : CI_LR);  // first plane
     static constexpr int PASSES = KIND == 5 ? NS : 2 * NS;      // colour passes (x halo shrink)
     static constexpr int H0 = UP ? PASSES : PASSES + 2;         // + residual + restriction
     static constexpr int H = ((H0 < 2 ? 2 : H0) + 1) & ~1;      // even (16-byte TMA alignment)
@@ -654,7 +657,7 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
     double *smS = sm + C::NM * AM;              // staging ring
     double *sE = smS + NA * AS;                 // coarse correction ring [4][WC]
     double *sC = sE + 4 * WC;                   // weights ring [4][8][WC]
-    uint64_t *bar = (uint64_t *)(sC + 8 * C::CSL * WC);
+    uint64_t *bar = (uint64_t *)(sC + C::NWP * C::CSL * WC);
 
     const int nx = a.A.nx, ny = a.A.ny;
     const long long P = a.A.pitch;
@@ -720,9 +723,9 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
                 break;
             const int slot = (Knext - Klo) & 3;
             uint64_t *b = &bar[SD + slot];
-            mbar_arrive_tx(b, (uint32_t)(9 * WC * 8));
+            mbar_arrive_tx(b, (uint32_t)((1 + C::NWP) * WC * 8));
             tma_2d(sE + slot * WC, &tmaps.e, cxl, Knext - a.eroff, b);
-            tma_3d(sC + slot * 8 * WC, &tmaps.c, cxl, Knext - a.ci.roff, 0, b);
+            tma_3d(sC + slot * C::NWP * WC, &tmaps.c, cxl, Knext - a.ci.roff, C::WP0, b);
             Knext++;
         }
     };
@@ -732,8 +735,14 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
 
     // u += P e (c7) on row x (main slot sx) at the columns of parity e of this thread's
     // pairs; same operand order as k_interp_add.  Point type is uniform over the group.
+    // Points of the first colour pass (5-point: C and Z; 9-point: C) are skipped:
+    // that pass overwrites them from their neighbours alone, so the result is
+    // bitwise the same as correcting them.
+    constexpr int NW = C::NWP, P0 = C::WP0;
     auto correct_task = [&](int x, int sx, int e) {
         if (x < lo1 || x > hi1)
+            return;
+        if (KIND == 5 ? !((e + x) & 1) : (!e && !(x & 1)))
             return;
         const int Ka = x >> 1, Kb = (x + 1) >> 1;
         mbar_wait(&bar[SD + ((Ka - Klo) & 3)], ((Ka - Klo) >> 2) & 1);
@@ -751,23 +760,23 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
             } else if (e && !rodd) {  // X point (2I-1, 2J)
                 const int I = (c + 1) / 2, Jx = x / 2, ic = I - cxl;
                 const double *ev = sE + ((Jx - Klo) & 3) * WC;
-                const double *w = sC + ((Jx - Klo) & 3) * 8 * WC;
-                s = w[CI_LL * WC + ic] * ev[ic - 1];
-                s += w[CI_LR * WC + ic] * ev[ic];
+                const double *w = sC + ((Jx - Klo) & 3) * NW * WC;
+                s = w[(CI_LL - P0) * WC + ic] * ev[ic - 1];
+                s += w[(CI_LR - P0) * WC + ic] * ev[ic];
             } else if (!e && rodd) {  // Y point (2I, 2J-1)
                 const int I = c / 2, Jy = (x + 1) / 2, ic = I - cxl;
                 const double *e0 = sE + ((Jy - 1 - Klo) & 3) * WC, *e1 = sE + ((Jy - Klo) & 3) * WC;
-                const double *w = sC + ((Jy - Klo) & 3) * 8 * WC;
-                s = w[CI_LB * WC + ic] * e0[ic];
-                s += w[CI_LA * WC + ic] * e1[ic];
+                const double *w = sC + ((Jy - Klo) & 3) * NW * WC;
+                s = w[(CI_LB - P0) * WC + ic] * e0[ic];
+                s += w[(CI_LA - P0) * WC + ic] * e1[ic];
             } else {  // Z point (2I-1, 2J-1)
                 const int I = (c + 1) / 2, Jz = (x + 1) / 2, ic = I - cxl;
                 const double *e0 = sE + ((Jz - 1 - Klo) & 3) * WC, *e1 = sE + ((Jz - Klo) & 3) * WC;
-                const double *w = sC + ((Jz - Klo) & 3) * 8 * WC;
-                s = w[CI_LSW * WC + ic] * e0[ic - 1];
-                s += w[CI_LSE * WC + ic] * e0[ic];
-                s += w[CI_LNW * WC + ic] * e1[ic - 1];
-                s += w[CI_LNE * WC + ic] * e1[ic];
+                const double *w = sC + ((Jz - Klo) & 3) * NW * WC;
+                s = w[(CI_LSW - P0) * WC + ic] * e0[ic - 1];
+                s += w[(CI_LSE - P0) * WC + ic] * e0[ic];
+                s += w[(CI_LNW - P0) * WC + ic] * e1[ic - 1];
+                s += w[(CI_LNE - P0) * WC + ic] * e1[ic];
             }
             u0[h] += s;
         }
@@ -1102,8 +1111,9 @@ static bool make_maps(TMaps &tm, const FusedGeom &g, const Op &A, const CIv &ci,
     bool ok = make_map(&tm.u, uin + A.roff * A.pitch, A.nx + 2, A.nrows, A.pitch, 0, 0, g.WD) &&
               make_map(&tm.f, f + A.roff * A.pitch, A.nx + 2, A.nrows, A.pitch, 0, 0, g.WD) &&
               make_map(&tm.a, A.O + A.roff * A.pitch, A.nx + 2, A.nrows, A.pitch, np, npl, g.WD) &&
-              // the down leg (ec == nullptr) fetches 4 of the 8 weight planes per coarse row
-              make_map(&tm.c, ci.w[0] + ci.roff * ci.pitch, ncx + 2, ci.nrows, ci.pitch, npc, 8, g.WC, ec ? 8 : 4);
+              // the down leg (ec == nullptr) and the 5-point up leg fetch 4 of the 8 weight planes
+              make_map(&tm.c, ci.w[0] + ci.roff * ci.pitch, ncx + 2, ci.nrows, ci.pitch, npc, 8, g.WC,
+                       ec && A.kind == 9 ? 8 : 4);
     if (ok && ec)
         ok = make_map(&tm.e, ec + (long long)eroff * ci.pitch, ncx + 2, enrows, ci.pitch, 0, 0, g.WC);
     else
