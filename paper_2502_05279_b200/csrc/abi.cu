@@ -421,13 +421,17 @@ static void copy_level(bmg_solver *h, int l, double *dst, const double *src, cud
 }
 
 // Down leg of level l: u_out = relax^nu1(u_in); fc = P^T (f - A u_out); uc = 0 (if non-null).
+// u_in == nullptr: a zero start (c9) that is not read.
 static void enqueue_down(bmg_solver *h, int l, bool fused, const double *f, const double *uin, double *uout,
                          double *fc, double *uc, cudaStream_t s, int *n)
 {
     Level &v = h->lv[l];
     if (fused && fused_down(h->fplan, l, v.op(), h->civ(l), f, uin, uout, fc, uc, s, n))
         return;
-    copy_level(h, l, uout, uin, s);
+    if (uin)
+        copy_level(h, l, uout, uin, s);
+    else
+        launch_zero_interior(v.op(), uout, s);
     relax_level(h, l, f, uout, h->prm.nu1, s, n);
     launch_residual(v.op(), f, uout, v.r, s);
     // after nu1 >= 1 point-GS sweeps the last colour's residual vanishes
@@ -479,9 +483,16 @@ static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream
     for (int l = 0; l < lt; l++) {
         double *T = l < 32 ? h->fplan.tmp[l] : nullptr;
         fz[l] = T && use_fused(h, l, F(l), U(l), T);
+    }
+    for (int l = 0; l < lt; l++) {
+        double *T = l < 32 ? h->fplan.tmp[l] : nullptr;
+        // a coarse level's down leg starts from zero (c9): a fused one does not read it,
+        // so the level above need not write that zero start either
+        const bool uz = l > 0 && fz[l];
+        double *uc = (l + 1 < lt && fz[l + 1]) ? nullptr : h->lv[l + 1].u;
         if (rec && l == 0)
             cudaEventRecordWithFlags(rec[0], s, cudaEventRecordExternal);
-        enqueue_down(h, l, fz[l], F(l), U(l), fz[l] ? T : U(l), h->lv[l + 1].f, h->lv[l + 1].u, s, &n);
+        enqueue_down(h, l, fz[l], F(l), uz ? nullptr : U(l), fz[l] ? T : U(l), h->lv[l + 1].f, uc, s, &n);
         if (rec && l == 0)
             cudaEventRecordWithFlags(rec[1], s, cudaEventRecordExternal);
     }

@@ -45,6 +45,7 @@ bmg_status_t fused_plan_level(FusedPlan &fp, int l, int nx, int ny, long long pi
                               bool aligned);
 
 // Down leg of level l: nu1 sweeps on (f, uin) -> uout, fc = P^T(f - A uout), uc = 0 (if non-null).
+// uin == nullptr: a zero start (the correction scheme's coarse levels, c9) that is not read.
 // Returns false if level l is not fused.
 bool fused_down(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const double *f, const double *uin,
                 double *uout, double *fc, double *uc, cudaStream_t s, int *nlaunch);

@@ -204,6 +204,7 @@ struct FArgs {
     double *uout, *fc, *uc;
     int nstrips, chunk, ncx, ncy;
     int eroff;  // stored-row offset of the coarse correction e (up leg)
+    int uzero;  // down leg: u_in == 0 (a coarse level's zero start, c9) -- not read
 };
 
 // TMA descriptors of one launch (kernel parameter, __grid_constant__):
@@ -426,6 +427,9 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
     static_assert(NR <= C::NG, "ring space");
     const Rings rg{smem_u32(bar + SD + 4), lo};
 
+    if (a.uzero)  // the zero start is never read from HBM: its staging rows stay 0
+        for (int i = tid; i < SD * WD; i += C::NT)
+            smS[(i / WD) * (NA * WD) + A_U * WD + i % WD] = 0.0;
     if (tid == 0) {
         for (int i = 0; i < SD + 4; i++)
             mbar_init(&bar[i], 1);
@@ -447,9 +451,10 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
     auto issue_row = [&](int row) {
         const int slot = (row - lo) % SD;
         uint64_t *b = &bar[slot];
-        mbar_arrive_tx(b, (uint32_t)(NA * WD * 8));
+        mbar_arrive_tx(b, (uint32_t)((a.uzero ? NA - 1 : NA) * WD * 8));
         double *d = smS + slot * (NA * WD);
-        tma_2d(d + A_U * WD, &tmaps.u, xl, row - a.A.roff, b);
+        if (!a.uzero)
+            tma_2d(d + A_U * WD, &tmaps.u, xl, row - a.A.roff, b);
         tma_2d(d + A_F * WD, &tmaps.f, xl, row - a.A.roff, b);
         tma_3d(d + A_O * WD, &tmaps.a, xl, row - a.A.roff, 0, b);
     };
@@ -1147,6 +1152,7 @@ static FArgs make_args(const FusedGeom &g, const Op &A, const CIv &ci)
     a.ncx = A.nx / 2;
     a.ncy = A.ny / 2;
     a.eroff = 0;
+    a.uzero = 0;
     return a;
 }
 
@@ -1162,8 +1168,9 @@ bool fused_down(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const do
     a.uout = uout;
     a.fc = fc;
     a.uc = uc;
+    a.uzero = uin == nullptr;
     TMaps tm;
-    if (!make_maps(tm, g, A, ci, uin, f, nullptr, 0, 0))
+    if (!make_maps(tm, g, A, ci, uin ? uin : f, f, nullptr, 0, 0))  // uzero: u map unused
         return false;
     if (A.kind == 5)
         g.NS == 2 ? launch_down<5, 2>(g, a, tm, s) : launch_down<5, 4>(g, a, tm, s);
