@@ -62,6 +62,8 @@ def lib():
             "orc_residual": (None, [c_int, c_int, _dp, _dp, _dp, _dp]),
             "orc_restrict": (None, [c_int, c_int, _dp, _dp, _dp]),
             "orc_interp_add": (None, [c_int, c_int, _dp, _dp, _dp]),
+            "orc_interp_add_affine": (None, [c_int, c_int, _dp, _dp, _dp, _dp, _dp]),
+            "orc_set_affine": (None, [c_void_p, c_int]),
             "orc_chol_factor": (c_int, [c_int, _dp]),
             "orc_chol_solve": (None, [c_int, _dp, _dp]),
             "orc_assemble_dense": (None, [c_int, c_int, _dp, _dp]),
@@ -196,6 +198,15 @@ def interp_add(ci, e, u) -> np.ndarray:
     return u
 
 
+def interp_add_affine(ci, e, st, r, u) -> np.ndarray:
+    """c14: u += P e + r/a_O at the non-coarse fine points."""
+    ny, nx = u.shape[0] - 2, u.shape[1] - 2
+    u = np.array(u, dtype=np.float64, copy=True, order="C")
+    lib().orc_interp_add_affine(nx, ny, _p(np.ascontiguousarray(ci)), _p(np.ascontiguousarray(e)),
+                                _p(np.ascontiguousarray(st)), _p(np.ascontiguousarray(r)), _p(u))
+    return u
+
+
 def chol_factor(A) -> np.ndarray:
     A = np.array(A, dtype=np.float64, copy=True, order="C")
     rc = lib().orc_chol_factor(A.shape[0], _p(A))
@@ -225,7 +236,7 @@ def norm2(g) -> float:
 class Hierarchy:
     """Oracle BoxMG hierarchy (setup c0-c4, c8) with V-cycle / solve (c9)."""
 
-    def __init__(self, stencil, nu1=2, nu2=1, coarsest=3, max_levels=0, relax="point", cycle_sym=0):
+    def __init__(self, stencil, nu1=2, nu2=1, coarsest=3, max_levels=0, relax="point", cycle_sym=0, affine=0):
         nx, ny = stencil.nx, stencil.ny
         self.nx, self.ny = nx, ny
         planes = [np.ascontiguousarray(p, dtype=np.float64) for p in stencil.plane_list()]
@@ -237,6 +248,8 @@ class Hierarchy:
         if rc != OK:
             raise ValueError(f"orc_setup: status {rc}")
         self._h = h
+        if affine:
+            lib().orc_set_affine(h, 1)
 
     def __del__(self):
         h = getattr(self, "_h", None)

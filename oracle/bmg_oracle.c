@@ -471,6 +471,29 @@ void orc_restrict(int nx, int ny, const double *ci, const double *q, double *qc)
         }
 }
 
+void orc_interp_add(int nx, int ny, const double *ci, const double *e, double *u);
+
+/*
+ * c14: BoxMG's affine interpolation-correction (the
+ * "r_F/a_O term" of BoxMG's interp_add): u += P e as in c7, plus, at every
+ * fine point that is not coincident with a coarse point (X, Y, Z), the
+ * residual r (the one restricted on the down leg) divided by the diagonal:
+ *   u(F) += (P e)(F) + r(F) / a_O(F),     u(C) += e(C).
+ * st: the level's full stencil (a_O at entry O_).
+ */
+void orc_interp_add_affine(int nx, int ny, const double *ci, const double *e, const double *st, const double *r,
+                           double *u)
+{
+    orc_interp_add(nx, ny, ci, e, u);
+    for (int j = 1; j <= ny; j++)
+        for (int i = 1; i <= nx; i++) {
+            if (!(i & 1) && !(j & 1))
+                continue; /* C point */
+            size_t p = gidx(nx, i, j);
+            u[p] += r[p] / st[9 * p + O_];
+        }
+}
+
 /*
  * c7: interpolation + correction (fig:vcycle_flowchart "Interpolate",
  * P:152; index map of fig:loop_indices P:382-403): u += P e over the fine
@@ -577,7 +600,7 @@ typedef struct {
 } orc_level;
 
 typedef struct {
-    int L, nu1, nu2, relax, cycle_sym;
+    int L, nu1, nu2, relax, cycle_sym, affine;
     orc_level lv[ORC_MAXLEV];
     double *chol; /* coarsest L factor, n*n */
     int nco;
@@ -683,6 +706,9 @@ int orc_setup(int nx, int ny, int kind, long pitch, const double *O, const doubl
 
 int orc_num_levels(const orc_hier *h) { return h->L; }
 
+/* c14: switch the cycle's interpolation to the affine BoxMG form (on = 1). */
+void orc_set_affine(orc_hier *h, int on) { h->affine = on != 0; }
+
 void orc_level_shape(const orc_hier *h, int l, int *nx, int *ny, int *kind)
 {
     *nx = h->lv[l].nx;
@@ -733,7 +759,10 @@ static void vcycle_level(orc_hier *h, int l)
     orc_restrict(v->nx, v->ny, v->ci, v->r, c->f);
     memset(c->u, 0, sizeof(double) * (size_t)(c->nx + 2) * (size_t)(c->ny + 2));
     vcycle_level(h, l + 1);
-    orc_interp_add(v->nx, v->ny, v->ci, c->u, v->u);
+    if (h->affine) /* c14: r still holds the residual restricted above */
+        orc_interp_add_affine(v->nx, v->ny, v->ci, c->u, v->st, v->r, v->u);
+    else
+        orc_interp_add(v->nx, v->ny, v->ci, c->u, v->u);
     relax_mode(h->relax, v->nx, v->ny, v->kind, v->st, v->f, v->u, h->nu2, h->cycle_sym);
 }
 

@@ -280,3 +280,26 @@ def test_leg_parity_level0(orc, wl, nx, ny, fused):
     assert_iterate_close(got, ref, rtol=1e-13)
     assert np.all(got[0, :] == 0) and np.all(got[:, 0] == 0) and np.all(got[-1, :] == 0) and np.all(got[:, -1] == 0)
     s.close()
+
+
+def test_random_shapes_vcycle_parity(orc):
+    """Seeded sweep over shapes the fixed cases miss (odd/even, thin rectangles, sizes
+    straddling the fused / tail / per-step thresholds and the strip width): one fused
+    V(2,1) cycle against the oracle at the DESIGN §7 tolerance."""
+    rng = np.random.default_rng(2025)
+    for _ in range(16):
+        nx, ny = (int(v) for v in rng.integers(4, 420, size=2))
+        wl = ["lognormal", "random9", "checker_off3", "aniso"][int(rng.integers(0, 4))]
+        st = P.workload(wl, nx, ny)
+        s = bmg.Solver(st)
+        h = orc.Hierarchy(st)
+        f = P.field_uniform(nx, ny, seed=int(rng.integers(1 << 30)))
+        x0 = P.field_uniform(nx, ny, seed=int(rng.integers(1 << 30)))
+        x = s.grid(x0)
+        s.vcycle(s.grid(f), x, 1)
+        torch.cuda.synchronize()
+        ref = h.vcycle(f, x0, 1)
+        got = bmg.from_device(x, nx)
+        tol = 1e-12 * np.maximum(np.abs(ref), np.abs(ref).max())
+        assert np.all(np.abs(got - ref) <= tol), (wl, nx, ny, np.abs(got - ref).max())
+        s.close()
