@@ -83,6 +83,11 @@ typedef struct {
                         BMG_RELAX_ALTLINES one sweep = an x-line then a y-line sweep.
                         Line modes run the per-step kernels (fused ignored) and need
                         nx, ny <= 32768 (EINVAL otherwise). */
+    int affine;      /* 0 (default): u += P e (DESIGN §3 c7); 1: BoxMG's affine
+                        interpolation-correction u(F) += (P e)(F) + r(F)/a_O(F) at the
+                        non-coarse points, r the residual restricted on the down leg
+                        (c14).  Runs the per-step kernels on the
+                        large levels (the fused down legs do not store r). */
 } bmg_params_t;
 
 #define BMG_RELAX_POINT 0

@@ -42,7 +42,7 @@ class bmg_stencil_t(ctypes.Structure):
 class bmg_params_t(ctypes.Structure):
     _fields_ = [("nu1", ctypes.c_int), ("nu2", ctypes.c_int), ("coarsest", ctypes.c_int),
                 ("max_levels", ctypes.c_int), ("agglom_rows", ctypes.c_int), ("cycle_sym", ctypes.c_int),
-                ("fused", ctypes.c_int), ("relax", ctypes.c_int)]
+                ("fused", ctypes.c_int), ("relax", ctypes.c_int), ("affine", ctypes.c_int)]
 
 
 class bmg_comm_t(ctypes.Structure):

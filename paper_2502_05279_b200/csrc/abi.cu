@@ -150,6 +150,7 @@ void bmg_params_default(bmg_params_t *p)
     p->cycle_sym = 0;
     p->fused = 1;
     p->relax = BMG_RELAX_POINT;
+    p->affine = 0;
 }
 
 const char *bmg_strerror(bmg_status_t s)
@@ -322,6 +323,7 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
             tp.nu1 = h->prm.nu1;
             tp.nu2 = h->prm.nu2;
             tp.cycle_sym = h->prm.cycle_sym;
+            tp.affine = h->prm.affine;
             tp.chol = h->chol;
             for (int l = l0; l < h->L; l++) {
                 tp.lv[l].A = h->lv[l].op();
@@ -341,7 +343,7 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
     // fused streaming plan + ping-pong partner of u for every fused level above the tail
     for (int l = 0; l + 1 < h->L && l < 32 && l < h->tail_l0; l++) {
         Level &v = h->lv[l];
-        if (!h->prm.fused || h->prm.relax != BMG_RELAX_POINT || h->prm.cycle_sym)
+        if (!h->prm.fused || h->prm.relax != BMG_RELAX_POINT || h->prm.cycle_sym || h->prm.affine)
             break;
         TRY(fused_plan_level(h->fplan, l, v.nx, v.ny, v.pitch, v.kind, h->prm.nu1, h->prm.nu2, (v.pitch & 1) == 0));
         LevelPlan &lp = h->fplan.lv[l];
@@ -374,7 +376,8 @@ bmg_status_t bmg_setup(const bmg_stencil_t *st, const bmg_params_t *params, void
     else
         bmg_params_default(&h->prm);
     if (h->prm.nu1 < 0 || h->prm.nu2 < 0 || h->prm.coarsest < 1 || h->prm.relax < BMG_RELAX_POINT ||
-        h->prm.relax > BMG_RELAX_ALTLINES || (h->prm.cycle_sym != 0 && h->prm.cycle_sym != 1)) {
+        h->prm.relax > BMG_RELAX_ALTLINES || (h->prm.cycle_sym != 0 && h->prm.cycle_sym != 1) ||
+        (h->prm.affine != 0 && h->prm.affine != 1)) {
         delete h;
         return fail(BMG_EINVAL, "bad params");
     }
@@ -447,7 +450,8 @@ static void enqueue_up(bmg_solver *h, int l, bool fused, const double *f, const 
     if (fused && fused_up(h->fplan, l, v.op(), h->civ(l), f, uin, ec, 0, h->lv[l + 1].ny + 2, uout, s, n))
         return;
     copy_level(h, l, uout, uin, s);
-    launch_interp_add(v.op(), h->civ(l), ec, uout, s);
+    // c14: v.r still holds the residual restricted on this level's down leg
+    launch_interp_add(v.op(), h->civ(l), ec, uout, s, h->prm.affine ? v.r : nullptr);
     *n += 1;
     relax_level(h, l, f, uout, h->prm.nu2, s, n, h->prm.cycle_sym == 1);
 }

@@ -115,7 +115,9 @@ void launch_residual(const Op &A, const double *f, const double *u, double *r, c
 // relaxed last (zero residual) are skipped, as in the fused down leg
 void launch_restrict(const Op &A, const CIv &ci, const double *r, double *fc, double *uc, cudaStream_t s,
                      bool vanish = false);
-void launch_interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s);
+// r != nullptr: BoxMG's affine term r/a_O at the non-coarse points (c14)
+void launch_interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s,
+                       const double *r = nullptr);
 // c11 zebra line GS (kernels_line.cu): nsweeps sweeps in `mode`; scr holds
 // line_scratch_doubles(nx, ny) doubles.  launch_line_pivots ORs ERR_LINE into
 // *err if a line block has a pivot <= 0.
@@ -144,6 +146,7 @@ struct TailLevel {
 struct TailPlan {
     int l0, L, nu1, nu2;
     int cycle_sym;         // 1: post-smoother colours reversed (c12)
+    int affine;            // 1: affine interpolation-correction with the level's r (c14)
     const double *chol;    // coarsest Cholesky factor
     TailLevel lv[32];
 };

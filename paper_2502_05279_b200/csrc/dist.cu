@@ -425,9 +425,9 @@ bmg_status_t dist_setup(const bmg_stencil_t *st, const bmg_comm_t *cm, const bmg
     d->nx = st->nx;
     d->ny = st->ny;
     d->kind0 = st->kind;
-    if (!d->prm.fused || d->prm.relax != BMG_RELAX_POINT || d->prm.cycle_sym != 0 || (d->prm.nu1 != 1 && d->prm.nu1 != 2) ||
+    if (!d->prm.fused || d->prm.relax != BMG_RELAX_POINT || d->prm.cycle_sym != 0 || d->prm.affine != 0 || (d->prm.nu1 != 1 && d->prm.nu1 != 2) ||
         (d->prm.nu2 != 1 && d->prm.nu2 != 2)) {
-        err = "distributed solver needs the fused point-GS kernels (params.fused = 1, relax = BMG_RELAX_POINT, cycle_sym = 0, "
+        err = "distributed solver needs the fused point-GS kernels (params.fused = 1, relax = BMG_RELAX_POINT, cycle_sym = 0, affine = 0, "
               "nu1, nu2 in {1, 2})";
         return fail(BMG_EINVAL);
     }

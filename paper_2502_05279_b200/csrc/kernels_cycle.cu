@@ -223,20 +223,33 @@ __device__ __forceinline__ double interp_pt(const CIv &ci, const double *__restr
     return s;
 }
 
-// u += P e, one thread per fine interior point.
-__global__ void k_interp_add(Op A, CIv ci, const double *__restrict__ e, double *__restrict__ u)
+// c14 affine term at a non-coarse fine point: r / a_O (0 at C points and without r)
+__device__ __forceinline__ double affine_pt(const Op &A, const double *__restrict__ r, int i, int j)
+{
+    if (!r || (!(i & 1) && !(j & 1)))
+        return 0.0;
+    const long long p = j * A.pitch + i;
+    return r[p] / A.O[p];
+}
+
+// u += P e (+ r/a_O at F points if r != nullptr, c14), one thread per fine interior point.
+__global__ void k_interp_add(Op A, CIv ci, const double *__restrict__ e, const double *__restrict__ r,
+                             double *__restrict__ u)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x + 1;
     int j = blockIdx.y * blockDim.y + threadIdx.y + 1;
     if (i > A.nx || j > A.ny)
         return;
-    u[j * A.pitch + i] += interp_pt(ci, e, i, j);
+    double s = interp_pt(ci, e, i, j);
+    if (r)
+        s += affine_pt(A, r, i, j);
+    u[j * A.pitch + i] += s;
 }
 
-void launch_interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s)
+void launch_interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s, const double *r)
 {
     dim3 b(32, 8), g((A.nx + 31) / 32, (A.ny + 7) / 8);
-    k_interp_add<<<g, b, 0, s>>>(A, ci, ec, u);
+    k_interp_add<<<g, b, 0, s>>>(A, ci, ec, r, u);
 }
 
 // zero the interior (and ring) of a level grid function
@@ -538,7 +551,10 @@ __global__ void __launch_bounds__(1024, 1) k_tail(const TailPlan *__restrict__ t
         const int cnt = A.nx * A.ny;
         for (int k = threadIdx.x; k < cnt; k += nt) {
             const int j = k / A.nx + 1, i = k % A.nx + 1;
-            u[(long long)j * A.pitch + i] += interp_pt(ci, e, i, j);
+            double s = interp_pt(ci, e, i, j);
+            if (tp->affine)
+                s += affine_pt(A, tp->lv[l].r, i, j);
+            u[(long long)j * A.pitch + i] += s;
         }
         __syncthreads();
         if (A.kind == 5)

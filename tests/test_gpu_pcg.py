@@ -109,3 +109,29 @@ def test_pcg_config2_true_residual():
     assert abs(true_rn - hist[-1]) <= 1e-9 * fn
     assert true_rn <= 1e-9 * fn
     s.close()
+
+
+@pytest.mark.parametrize("wl,nx,ny", [("lognormal", 63, 63), ("checker_off3", 95, 47), ("random9", 33, 33),
+                                      ("aniso", 63, 63), ("lognormal", 300, 257)])
+def test_affine_cycle_parity(orc, wl, nx, ny):
+    """BoxMG's affine interpolation-correction (DESIGN §3 c14): one V(2,1) cycle and a
+    solve against the oracle."""
+    st = P.workload(wl, nx, ny)
+    prm = bmg.bmg_params_default()
+    prm.affine = 1
+    s = bmg.Solver(st, prm)
+    h = orc.Hierarchy(st, affine=1)
+    f = P.field_uniform(nx, ny, seed=91)
+    x0 = P.field_uniform(nx, ny, seed=92)
+    x = s.grid(x0)
+    s.vcycle(s.grid(f), x, 1)
+    torch.cuda.synchronize()
+    assert_iterate_close(bmg.from_device(x, nx), h.vcycle(f, x0, 1))
+    if nx * ny <= 10000:
+        fr = P.rhs_const(nx, ny)
+        x = s.grid()
+        it, hist, rc = s.solve(s.grid(fr), x, 1e-9, 200)
+        uo, ito, histo, rco = h.solve(fr, np.zeros_like(fr), 1e-9, 200)
+        assert rc == rco and it == ito
+        assert np.all(np.abs(hist - histo) <= 1e-10 * histo + 1e-12 * histo[0])
+    s.close()
