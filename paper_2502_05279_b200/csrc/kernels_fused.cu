@@ -102,6 +102,31 @@ __device__ __forceinline__ void tma_3d(void *dst, const CUtensorMap *m, int x, i
         : "memory");
 }
 
+// L2 prefetch of one tensor box (no shared memory, no completion): the rows far
+// ahead of the shared-memory ring are pulled into L2 so that the ring's TMA loads
+// hit L2 -- the ring's depth (bytes in flight per SM) is bounded by shared memory.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *m, int x, int y)
+{
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(x), "r"(y)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *m, int x, int y, int z)
+{
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(x), "r"(y), "r"(z)
+                 : "memory");
+}
+
+// rows beyond the ring's prefetch depth D that are prefetched into L2 (0: none; measured no
+// gain at 4..32 rows, DESIGN §10 -- kept as a tuning knob)
+#ifndef BMG_L2PF
+#define BMG_L2PF 0
+#endif
+
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
 // ------------------------------------------------------------------ configuration
@@ -581,6 +606,13 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
             // the TMA (async proxy) overwrites them, ordered by the mbarrier wait above.
             if (t + D <= hi)
                 issue_row(t + D);
+            if (BMG_L2PF > 0 && t + D + BMG_L2PF <= hi) {
+                const int row = t + D + BMG_L2PF - a.A.roff;
+                if (!a.uzero)
+                    tma_prefetch_2d(&tmaps.u, xl, row);
+                tma_prefetch_2d(&tmaps.f, xl, row);
+                tma_prefetch_3d(&tmaps.a, xl, row, 0);
+            }
             issue_coarse(t);
         }
         return;
@@ -603,18 +635,37 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
     }
     int tm = 0, tsd = 0;  // main / staging ring slots of row t
     for (int t = lo; t <= tend; t++, tm = (tm + 1 == RM) ? 0 : tm + 1, tsd = (tsd + 1 == SD) ? 0 : tsd + 1) {
+// Timing experiments only (tools_variants.py -D...): drop one task's work to find
+// the pipeline's bottleneck; results are wrong when any is set.
+#ifndef BMG_X_NOSPLIT
+#define BMG_X_NOSPLIT 0
+#endif
+#ifndef BMG_X_NOSTAGE
+#define BMG_X_NOSTAGE 0
+#endif
+#ifndef BMG_X_NORES
+#define BMG_X_NORES 0
+#endif
+#ifndef BMG_X_NORESTR
+#define BMG_X_NORESTR 0
+#endif
+#ifndef BMG_X_NOSTORE
+#define BMG_X_NOSTORE 0
+#endif
         if (grp >= G_SPLIT) {
             rg.wait(R_SPLIT, t - 1 - E);
             if (t <= hi) {
                 mbar_wait(&bar[tsd], ((t - lo) / SD) & 1);
-                if (grp == G_SPLIT)
+                if (BMG_X_NOSPLIT) {
+                } else if (grp == G_SPLIT)
                     split_row<NA, AM, WD, PPT, NPG, false>(sm, smS, tsd, tm, 0, QSPLIT, m);
                 else
                     split_row<NA, AM, WD, PPT, NPG, true>(sm, smS, tsd, tm, QSPLIT, NA, m);
             }
         } else if (grp < NSG) {
             rg.wait(grp, t - 1);
-            if (KIND == 5) {
+            if (BMG_X_NOSTAGE) {
+            } else if (KIND == 5) {
                 const int k = grp + 1, d = 2 * k, r = t - d;
                 if (r > lo && r < hi && r >= 1 && r <= ny)
                     colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1),
@@ -635,15 +686,17 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
         } else if (grp < G_STORE) {
             rg.wait(R_RES, t - 1);
             const int d = 2 * NS + 2;
-            resid_task(t - d, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), grp - G_RES);
+            if (!BMG_X_NORES)
+                resid_task(t - d, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), grp - G_RES);
         } else if (grp == G_STORE) {
             rg.wait(R_STORE, t - 3);
-            store_task(t - 2 * NS - 3, back<RM>(tm, 2 * NS + 3));
+            if (!BMG_X_NOSTORE)
+                store_task(t - 2 * NS - 3, back<RM>(tm, 2 * NS + 3));
         } else {
             rg.wait(R_RESTR, t - 1);
             const int jr = t - 2 * NS - 4;
             const int J = jr >> 1;
-            if (jr >= 0 && !(jr & 1) && J >= Jlo && J <= Jhi)
+            if (!BMG_X_NORESTR && jr >= 0 && !(jr & 1) && J >= Jlo && J <= Jhi)
                 restrict_task(J);
         }
         rg.done(t, a0, a1, a2);
@@ -819,6 +872,12 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
             rg.wait(R_PROD, t - 1);
             if (t + D <= hi)
                 issue_row(t + D);
+            if (BMG_L2PF > 0 && t + D + BMG_L2PF <= hi) {
+                const int row = t + D + BMG_L2PF - a.A.roff;
+                tma_prefetch_2d(&tmaps.u, xl, row);
+                tma_prefetch_2d(&tmaps.f, xl, row);
+                tma_prefetch_3d(&tmaps.a, xl, row, 0);
+            }
             issue_coarse(t);
         }
         return;
