@@ -958,12 +958,16 @@ static void device_limits()
 
 // Deepest TMA prefetch (rows, <= 4) whose shared-memory footprint fits a CTA.
 constexpr size_t SMEM_CTA_MAX = 232448;  // 227 KB opt-in
-template <int KIND, int NS, int WD, bool UP, int PPT, int E>
+#ifndef BMG_DMAX
+#define BMG_DMAX 4
+#endif
+template <int KIND, int NS, int WD, bool UP, int PPT, int E, int DM = BMG_DMAX>
 constexpr int pick_D()
 {
-    return Cfg<KIND, NS, WD, 4, UP, PPT, E>::SMEM <= SMEM_CTA_MAX   ? 4
-           : Cfg<KIND, NS, WD, 3, UP, PPT, E>::SMEM <= SMEM_CTA_MAX ? 3
-                                                                    : 2;
+    if constexpr (DM <= 2)
+        return 2;
+    else
+        return Cfg<KIND, NS, WD, DM, UP, PPT, E>::SMEM <= SMEM_CTA_MAX ? DM : pick_D<KIND, NS, WD, UP, PPT, E, DM - 1>();
 }
 
 // Kernel instances: (kind, NS) -> (WD, D, pairs per thread).  WD = smem row width.
