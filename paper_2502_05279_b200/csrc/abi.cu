@@ -6,6 +6,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <chrono>
 #include <map>
 #include <string>
 #include <utility>
@@ -107,6 +108,7 @@ struct bmg_solver {
     int tail_l0 = 1 << 30;            // first level of the tail kernel (none: > L)
     TailPlan *tail = nullptr;         // its device-side plan
     bool timing = false;              // bmg_timing: timed graph variant, event pair per launch
+    bool cycle_err = false;           // a planned fused leg was rejected while enqueuing a cycle
     std::vector<cudaEvent_t> tev;     // event pairs (start, end) per recorded launch
     size_t tev_used = 0;
 
@@ -200,9 +202,25 @@ bmg_status_t bmg_destroy(bmg_solver_t h)
     return BMG_OK;
 }
 
+// BMG_SETUP_TRACE=1: host wall-clock of the setup phases on stderr (tuning aid)
+static void setup_trace(const char *what, cudaStream_t s)
+{
+    static const bool on = getenv("BMG_SETUP_TRACE") != nullptr;
+    if (!on)
+        return;
+    static std::chrono::steady_clock::time_point t0;
+    cudaStreamSynchronize(s);
+    auto now = std::chrono::steady_clock::now();
+    if (strcmp(what, "start") != 0)
+        fprintf(stderr, "bmg_setup %-16s %8.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(now - t0).count());
+    t0 = now;
+}
+
 static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStream_t s)
 {
     const bmg_params_t &pr = h->prm;
+    setup_trace("start", s);
     // level ladder (c1): n_{l+1} = floor(n_l/2) until min(nx,ny) <= coarsest
     {
         int nx = st->nx, ny = st->ny;
@@ -220,32 +238,43 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
         v.ny = l == 0 ? st->ny : h->lv[l - 1].ny / 2;
         v.kind = l == 0 ? st->kind : 9;
         v.pitch = l == 0 ? st->pitch : round_pitch(v.nx);
-        size_t np = (size_t)(v.ny + 2) * (size_t)v.pitch;
-        int npl = v.kind == 9 ? 5 : 3;
-        {  // the planes of a level form one block (plane stride np): one 3-D TMA box per row
-            double *blk = nullptr;
-            TRY(dalloc(h, &blk, np * npl));
-            for (int k = 0; k < npl; k++)
-                v.pl[k] = blk + k * np;
-        }
-        TRY(dalloc(h, &v.r, np));
-        if (l > 0) {
-            TRY(dalloc(h, &v.u, np));
-            TRY(dalloc(h, &v.f, np));
-            for (int k = 0; k < npl; k++)
-                CK(cudaMemsetAsync(v.pl[k], 0, np * sizeof(double), s));
-            CK(cudaMemsetAsync(v.u, 0, np * sizeof(double), s));
-            CK(cudaMemsetAsync(v.f, 0, np * sizeof(double), s));
-        }
     }
-    for (int l = 0; l + 1 < h->L; l++) {
-        Level &c = h->lv[l + 1];
-        size_t np = (size_t)(c.ny + 2) * (size_t)c.pitch;
-        double *blk = nullptr;  // the 8 weight planes form one block (plane stride np)
-        TRY(dalloc(h, &blk, np * 8));
-        CK(cudaMemsetAsync(blk, 0, 8 * np * sizeof(double), s));
-        for (int k = 0; k < 8; k++)
-            h->lv[l].ci[k] = blk + k * np;
+    // Every level array lives in ONE zeroed device block (one cudaMalloc: a few
+    // large allocations cost ~1 ms, a dozen separate ones ~7-10 ms).  Pass 0 sizes
+    // the arena, pass 1 carves it (256-B aligned pieces).
+    double *arena = nullptr;
+    size_t used = 0;
+    auto take = [&](size_t n) {
+        double *p = arena ? arena + used : nullptr;
+        used += (n + 31) / 32 * 32;
+        return p;
+    };
+    for (int pass = 0; pass < 2; pass++) {
+        if (pass == 1) {
+            TRY(dalloc(h, &arena, used));
+            CK(cudaMemsetAsync(arena, 0, used * sizeof(double), s));
+            used = 0;
+        }
+        for (int l = 0; l < h->L; l++) {
+            Level &v = h->lv[l];
+            size_t np = (size_t)(v.ny + 2) * (size_t)v.pitch;
+            int npl = v.kind == 9 ? 5 : 3;
+            double *blk = take(np * npl);  // the planes of a level form one block (plane
+            for (int k = 0; k < npl; k++)  // stride np): one 3-D TMA box per row
+                v.pl[k] = blk ? blk + k * np : nullptr;
+            v.r = take(np);
+            if (l > 0) {
+                v.u = take(np);
+                v.f = take(np);
+            }
+        }
+        for (int l = 0; l + 1 < h->L; l++) {
+            Level &c = h->lv[l + 1];
+            size_t np = (size_t)(c.ny + 2) * (size_t)c.pitch;
+            double *blk = take(np * 8);  // the 8 weight planes form one block (plane stride np)
+            for (int k = 0; k < 8; k++)
+                h->lv[l].ci[k] = blk ? blk + k * np : nullptr;
+        }
     }
     {
         void *q;
@@ -258,6 +287,7 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
     TRY(dalloc(h, &h->d_norm, 8));
     CK(cudaMallocHost(&h->h_norm, 8 * sizeof(double)));
 
+    setup_trace("allocate", s);
     // S0 ingest
     {
         Level &v = h->lv[0];
@@ -265,6 +295,7 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
         launch_ingest(v.nx, v.ny, v.kind, v.pitch, src, v.pl, h->d_err, s, 0, v.ny + 2);
         CK(cudaGetLastError());
     }
+    setup_trace("ingest", s);
     // S1 + S2 per level
     for (int l = 0; l + 1 < h->L; l++) {
         Level &v = h->lv[l], &c = h->lv[l + 1];
@@ -273,6 +304,7 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
         launch_setup_rap(v.op(), h->civ(l), c.nx, c.ny, c.pitch, c.pl, s, 1, c.ny);
         CK(cudaGetLastError());
     }
+    setup_trace("interp+rap", s);
     // S3 coarsest dense Cholesky
     {
         Level &c = h->lv[h->L - 1];
@@ -293,6 +325,7 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
         return fail(BMG_EINVAL, "interpolation denominator <= 0 (operator not suited to BoxMG collapse)");
     if (herr & ERR_PIVOT)
         return fail(BMG_ENOTSPD, "coarsest-level Cholesky pivot <= 0");
+    setup_trace("cholesky+check", s);
     // c11 line relaxation: scratch sized for level 0, line pivots of every relaxed level
     if (pr.relax != BMG_RELAX_POINT) {
         if (h->lv[0].nx > LINE_NMAX || h->lv[0].ny > LINE_NMAX)
@@ -351,11 +384,15 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
             lp.down = lp.up = false;
             continue;
         }
+        // the ping-pong partner T is the level's residual array: a fused level never
+        // stores r (its down leg restricts from shared memory), and T lives only
+        // within one cycle; its ring must be 0
         size_t np = (size_t)(v.ny + 2) * (size_t)v.pitch;
-        TRY(dalloc(h, &h->fplan.tmp[l], np));
-        CK(cudaMemsetAsync(h->fplan.tmp[l], 0, np * sizeof(double), s));
+        h->fplan.tmp[l] = v.r;
+        CK(cudaMemsetAsync(v.r, 0, np * sizeof(double), s));
     }
     CK(cudaStreamSynchronize(s));
+    setup_trace("lines/tail/fused", s);
     return BMG_OK;
 }
 
@@ -431,6 +468,10 @@ static void enqueue_down(bmg_solver *h, int l, bool fused, const double *f, cons
     Level &v = h->lv[l];
     if (fused && fused_down(h->fplan, l, v.op(), h->civ(l), f, uin, uout, fc, uc, s, n))
         return;
+    if (fused && uout == v.r) {  // the per-step path would need r, which is T here
+        h->cycle_err = true;
+        return;
+    }
     if (uin)
         copy_level(h, l, uout, uin, s);
     else
@@ -537,10 +578,15 @@ static bmg_status_t get_graph(bmg_solver *h, const double *f, double *x, bool ti
     }
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+    h->cycle_err = false;
     int n = enqueue_cycle(h, f, x, h->cap, timed ? h->cev : nullptr);
     cudaError_t e = cudaStreamEndCapture(h->cap, &g);
     if (e != cudaSuccess)
         return fail(BMG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    if (h->cycle_err) {
+        cudaGraphDestroy(g);
+        return fail(BMG_ECUDA, "a fused leg was rejected while capturing the cycle (tensor-map encode?)");
+    }
     GraphRec gr;
     gr.g = g;
     if (timed) {
