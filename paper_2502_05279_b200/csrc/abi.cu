@@ -252,7 +252,9 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
     for (int pass = 0; pass < 2; pass++) {
         if (pass == 1) {
             TRY(dalloc(h, &arena, used));
+            setup_trace("cudaMalloc", s);
             CK(cudaMemsetAsync(arena, 0, used * sizeof(double), s));
+            setup_trace("memset", s);
             used = 0;
         }
         for (int l = 0; l < h->L; l++) {
