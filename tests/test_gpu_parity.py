@@ -307,3 +307,44 @@ def test_random_shapes_vcycle_parity(orc):
         tol = 1e-12 * np.maximum(np.abs(ref), np.abs(ref).max())
         assert np.all(np.abs(got - ref) <= tol), (wl, nx, ny, np.abs(got - ref).max())
         s.close()
+
+
+@pytest.mark.parametrize("nu1,nu2,coarsest,max_levels", [(1, 1, 3, 0), (2, 2, 3, 0), (0, 1, 3, 0), (1, 0, 3, 0),
+                                                          (3, 2, 3, 0), (2, 1, 7, 0), (2, 1, 3, 2), (2, 1, 3, 3)])
+def test_params_vcycle_parity(orc, nu1, nu2, coarsest, max_levels):
+    """Cycle shapes other than the default V(2,1): nu1/nu2 from 0 to 3 (nu = 0 and 3 run
+    the per-step kernels on the large levels; no vanishing-residual restriction after
+    nu1 = 0), a larger coarsest grid, and a truncated hierarchy (bigger Cholesky)."""
+    nx, ny = 150, 97
+    st = P.workload("lognormal", nx, ny)
+    prm = bmg.bmg_params_default()
+    prm.nu1, prm.nu2, prm.coarsest, prm.max_levels = nu1, nu2, coarsest, max_levels
+    s = bmg.Solver(st, prm)
+    h = orc.Hierarchy(st, nu1=nu1, nu2=nu2, coarsest=coarsest, max_levels=max_levels)
+    assert s.L == h.num_levels
+    f = P.field_uniform(nx, ny, seed=101)
+    x0 = P.field_uniform(nx, ny, seed=102)
+    x = s.grid(x0)
+    s.vcycle(s.grid(f), x, 1)
+    torch.cuda.synchronize()
+    assert_iterate_close(bmg.from_device(x, nx), h.vcycle(f, x0, 1))
+    s.close()
+
+
+@pytest.mark.parametrize("extra", [1, 3, 40])
+def test_user_pitch_vcycle_parity(orc, extra):
+    """A caller pitch other than the library's (odd: the fused level-0 legs need an even
+    pitch, so level 0 runs the per-step kernels; padded: fused) gives the same cycle."""
+    nx, ny = 131, 90
+    st = P.workload("random9", nx, ny)
+    s = bmg.Solver(st, pitch=nx + 2 + extra)
+    h = orc.Hierarchy(st)
+    f = P.field_uniform(nx, ny, seed=103)
+    x0 = P.field_uniform(nx, ny, seed=104)
+    x = s.grid(x0)
+    s.vcycle(s.grid(f), x, 2)
+    torch.cuda.synchronize()
+    assert_iterate_close(bmg.from_device(x, nx), h.vcycle(f, x0, 2))
+    xg = x.cpu().numpy()
+    assert np.all(xg[:, nx + 1:] == 0)  # padding and ring untouched
+    s.close()
