@@ -27,6 +27,7 @@ struct FusedGeom {
     int threads = 0;
     size_t smem = 0;
     bool ok = false;
+    bool wave = false;  // 5-point down leg: the register-wavefront kernel (k_wave_down5)
 };
 
 struct LevelPlan {
