@@ -272,6 +272,28 @@ static bmg_status_t exchange(DistSolver *d, int l, Field fd, cudaStream_t s, std
 // All-gather the owned level-K rows [ylo, yhi) into the full array `full` (global
 // rows, pitch pitchK, `nplanes` planes of stride npk) on every rank.  which = 0:
 // the rows come from the slab's planes; which = 1: they are already in `full`.
+// Two exchanges as ONE NCCL group (nested groups launch at the outermost end):
+// one communication kernel per leg instead of one per field.
+static bmg_status_t exchange2(DistSolver *d, int l1, Field f1, int l2, Field f2, cudaStream_t s, std::string &err)
+{
+    if (d->P == 1)
+        return BMG_OK;
+    if (d->loopback) {
+        bmg_status_t rc = exchange(d, l1, f1, s, err);
+        return rc == BMG_OK ? exchange(d, l2, f2, s, err) : rc;
+    }
+    ncclResult_t r = d->nccl.groupStart();
+    bmg_status_t rc = r == ncclSuccess ? exchange(d, l1, f1, s, err) : BMG_ENCCL;
+    if (rc == BMG_OK)
+        rc = exchange(d, l2, f2, s, err);
+    ncclResult_t r2 = d->nccl.groupEnd();
+    if (rc == BMG_OK && (r != ncclSuccess || r2 != ncclSuccess)) {
+        err = std::string("NCCL exchange group: ") + d->nccl.errstr(r != ncclSuccess ? r : r2);
+        return BMG_ENCCL;
+    }
+    return rc;
+}
+
 static bmg_status_t allgather_rows(DistSolver *d, double *full, long long npk, int nplanes, int which,
                                    cudaStream_t s, std::string &err)
 {
@@ -631,14 +653,18 @@ static bmg_status_t one_cycle(DistSolver *d, cudaStream_t s, std::string &err)
     const int K = d->K;
     int n = 0;
     for (int l = 0; l < K; l++) {
-        DTRY(exchange(d, l, F_U, s, err));
-        DTRY(exchange(d, l, F_F, s, err));
+        // level 0: u and f in one group; a coarse level starts from zero (c9), which
+        // its fused down leg does not read -- only f's ghost rows move
+        if (l == 0)
+            DTRY(exchange2(d, 0, F_U, 0, F_F, s, err));
+        else
+            DTRY(exchange(d, l, F_F, s, err));
         for (auto &R : d->ranks) {
             SLevel &v = R.lv[l];
             const bool last = l + 1 == K;
             double *fc = last ? d->fK : R.lv[l + 1].f;
-            double *uc = last ? nullptr : R.lv[l + 1].u;
-            if (!fused_down(R.fp, l, v.op(), civ_of(R, l), v.f, v.u, v.T, fc, uc, s, &n)) {
+            if (!fused_down(R.fp, l, v.op(), civ_of(R, l), v.f, l == 0 ? v.u : nullptr, v.T, fc, nullptr, s,
+                            &n)) {
                 err = "fused down leg rejected a slab level";
                 return BMG_EINVAL;
             }
@@ -652,9 +678,10 @@ static bmg_status_t one_cycle(DistSolver *d, cudaStream_t s, std::string &err)
     cudaMemsetAsync(d->xK, 0, sizeof(double) * (size_t)(d->nyK + 2) * d->pitchK, s);
     DTRY(bmg_vcycle(d->inner, d->fK, d->xK, 1, s));
     for (int l = K - 1; l >= 0; l--) {
-        DTRY(exchange(d, l, F_T, s, err));
         if (l + 1 < K)
-            DTRY(exchange(d, l + 1, F_U, s, err));
+            DTRY(exchange2(d, l, F_T, l + 1, F_U, s, err));
+        else
+            DTRY(exchange(d, l, F_T, s, err));
         for (auto &R : d->ranks) {
             SLevel &v = R.lv[l];
             const bool last = l + 1 == K;

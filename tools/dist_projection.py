@@ -1,0 +1,66 @@
+"""Multi-GPU evidence on ONE GPU: the row-slab solver with the loopback
+transport runs all P slabs of the 8191^2 problem on this GPU, one after another.
+
+  T_lb(P)   = loopback cycle time (every slab's legs + the replicated inner cycle
+              once + device-to-device ghost-row copies)
+  T_inner   = the replicated inner hierarchy's cycle (a single-GPU solver on the
+              level-K operator, measured on its own)
+  slabs(P)  = T_lb(P) - T_inner  (all slabs' work, summed)
+
+On P GPUs each rank runs its slab concurrently, so the per-cycle time is about
+  T_P ~ slabs(P)/P * imbalance + T_inner + T_exch,
+T_exch = 2K grouped NCCL ghost-row exchanges (8191^2, P=8: K levels; each a
+one-row-per-neighbour send/recv over NVLink) + one all-gather of level K's rhs --
+NOT measured here (one GPU); the printed projection takes them as a parameter.
+Prints one JSON line.
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2502_05279_b200 import bmg, dist as D, problems as P  # noqa: E402
+
+N = int(os.environ.get("N", "8191"))
+EXCH_US = float(os.environ.get("EXCH_US", "25"))  # assumed latency of one grouped NCCL exchange
+
+
+def time_cycles(fn, ncyc=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(ncyc):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / ncyc
+
+
+st = P.workload("poisson", N, N)
+f_np = P.rhs_const(N, N)
+out = {"n": N, "exch_us_assumed": EXCH_US}
+s = bmg.Solver(st)
+f, x = s.grid(f_np), s.grid()
+out["single_ms"] = time_cycles(lambda: s.vcycle(f, x, 1))
+s.close()
+for nr in (2, 4, 8):
+    yb, K = bmg.bmg_partition(N, N, nr)
+    d = D.DistSolver(st, nr, 0, None, loopback=True)
+    f, x = d.local(f_np), d.local()
+    t_lb = time_cycles(lambda: d.vcycle(f, x, 1))
+    d.close()
+    nK = N >> K
+    si = bmg.Solver(P.workload("poisson", nK, nK))  # the replicated inner hierarchy
+    fi, xi = si.grid(P.rhs_const(nK, nK)), si.grid()
+    t_in = time_cycles(lambda: si.vcycle(fi, xi, 1))
+    si.close()
+    slabs = t_lb - t_in
+    t_p = slabs / nr + t_in + (2 * K + 1) * EXCH_US / 1e3
+    out[f"p{nr}"] = {"kdist": K, "loopback_ms": t_lb, "inner_ms": t_in, "slabs_ms": slabs,
+                     "slab_overhead_vs_single": slabs / (out["single_ms"] - t_in) if out["single_ms"] > t_in else None,
+                     "projected_ms": t_p, "projected_efficiency": out["single_ms"] / (nr * t_p)}
+print(json.dumps(out))
