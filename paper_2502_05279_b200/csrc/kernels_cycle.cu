@@ -462,6 +462,32 @@ __device__ __forceinline__ void coarse_solve_cta(const Op &A, const double *__re
         u[(p / A.nx + 1) * A.pitch + p % A.nx + 1] = b[p];
 }
 
+// The same two substitutions by ONE warp for n <= 32 unknowns (lane i holds b_i;
+// x_k is broadcast by a shuffle): the CTA version pays two __syncthreads per
+// unknown.  Identical operations in identical order, so bitwise the same result.
+__device__ __forceinline__ void coarse_solve_warp(const Op &A, const double *__restrict__ Lf,
+                                                  const double *__restrict__ f, double *__restrict__ u)
+{
+    const int n = A.nx * A.ny, i = threadIdx.x & 31;
+    double b = i < n ? f[(i / A.nx + 1) * A.pitch + i % A.nx + 1] : 0.0;
+    for (int k = 0; k < n; k++) {  // L y = b
+        const double bk = __shfl_sync(0xffffffffu, b, k) / Lf[(long long)k * n + k];
+        if (i == k)
+            b = bk;
+        else if (i > k && i < n)
+            b -= Lf[(long long)i * n + k] * bk;
+    }
+    for (int k = n - 1; k >= 0; k--) {  // L^T x = y
+        const double bk = __shfl_sync(0xffffffffu, b, k) / Lf[(long long)k * n + k];
+        if (i == k)
+            b = bk;
+        else if (i < k)
+            b -= Lf[(long long)k * n + i] * bk;
+    }
+    if (i < n)
+        u[(i / A.nx + 1) * A.pitch + i % A.nx + 1] = b;
+}
+
 __global__ void k_coarse_solve(Op A, const double *__restrict__ Lf, const double *__restrict__ f, double *__restrict__ u)
 {
     extern __shared__ double b[];
@@ -541,7 +567,12 @@ __global__ void __launch_bounds__(1024, 1) k_tail(const TailPlan *__restrict__ t
             restrict_store(A, ci, r, tp->lv[l + 1].f, tp->lv[l + 1].u, k % cx, k / cx, tp->nu1 > 0);
         __syncthreads();
     }
-    coarse_solve_cta(tp->lv[L - 1].A, tp->chol, F(L - 1), U(L - 1), b);
+    if (tp->lv[L - 1].A.nx * tp->lv[L - 1].A.ny <= 32) {
+        if (threadIdx.x < 32)
+            coarse_solve_warp(tp->lv[L - 1].A, tp->chol, F(L - 1), U(L - 1));
+    } else {
+        coarse_solve_cta(tp->lv[L - 1].A, tp->chol, F(L - 1), U(L - 1), b);
+    }
     __syncthreads();
     for (int l = L - 2; l >= l0; l--) {
         const Op A = tp->lv[l].A;
