@@ -190,7 +190,7 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "cycles/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / val,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "nx": nx, "ny": ny, "cycle": "V(2,1)"},
         "munknowns_per_s": val * nx * ny / 1e6,
         "cpu_baseline": {"value": val, "unit": "cycles/s", "cores": 1, "kind": "oracle", "sample": sample,
