@@ -244,3 +244,21 @@ def test_operator_induced_beats_bilinear_at_jump(orc):
     s = P.stencil5_from_D(P.d_node_jump(n, n, 21))
     fac = asymptotic_factor(orc, s, ncyc=12)
     assert fac < 0.08, fac
+
+
+@pytest.mark.parametrize("wl,kind,n", [("lognormal", 5, 31), ("checker", 5, 31), ("random9", 9, 30), ("aniso", 9, 31)])
+def test_last_colour_residual_vanishes(orc, wl, kind, n):
+    """The identity behind DESIGN §3 c5a: after a multicolour GS sweep the residual is
+    zero (to rounding) at every point of the colour relaxed last -- 5-point: black
+    ((i+j) odd), 9-point: colour 3 (i, j odd) -- and not at the others."""
+    stc = P.workload(wl, n, n)
+    st = orc.expand_stencil(stc)
+    f = P.field_uniform(n, n, seed=11)
+    u = orc.relax(st, kind, f, P.field_uniform(n, n, seed=12), 1)
+    r = orc.residual(st, f, u)
+    J, I = np.meshgrid(np.arange(n + 2), np.arange(n + 2), indexing="ij")
+    inside = (I >= 1) & (I <= n) & (J >= 1) & (J <= n)
+    last = inside & (((I + J) % 2 == 1) if kind == 5 else ((I % 2 == 1) & (J % 2 == 1)))
+    scale = np.abs(f).max() + np.abs(u).max() * np.abs(st).sum(-1).max()
+    assert np.abs(r[last]).max() <= 1e-15 * scale
+    assert np.abs(r[inside & ~last]).max() > 1e-6 * np.abs(r).max()
