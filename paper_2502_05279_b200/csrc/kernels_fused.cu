@@ -1294,7 +1294,10 @@ struct Inst {
 #ifndef BMG_PPT5
 #define BMG_PPT5 2
 #endif
-    static constexpr int PPT_DN = KIND == 5 ? BMG_PPT5 : 1;
+#ifndef BMG_PPT9DN
+#define BMG_PPT9DN 1
+#endif
+    static constexpr int PPT_DN = KIND == 5 ? BMG_PPT5 : BMG_PPT9DN;
     static constexpr int WD_UP = KIND == 5 ? BMG_WD5 : (NS == 4 ? 192 : BMG_WD9UP);
 
     static constexpr int PPT_UP = KIND == 5 ? BMG_PPT5 : (NS == 4 ? 1 : 2);
