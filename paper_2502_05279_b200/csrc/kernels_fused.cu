@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
 }
 
 // ------------------------------------------------------------------ register wavefront
-// 5-point down leg without the shared-memory main ring: a warp
+// 5-point down leg without the shared-memory main ring (off by default): a warp
 // owns a 64-column window (lane h: the column pair 2h, 2h+1) and marches up the
 // rows keeping the last NS+3 rows of u and NS+2 rows of coefficients in
 // REGISTERS.  Step t: the row t arrives (TMA staging ring, natural layout, read
