@@ -378,9 +378,10 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
     // fused streaming plan + ping-pong partner of u for every fused level above the tail
     for (int l = 0; l + 1 < h->L && l < 32 && l < h->tail_l0; l++) {
         Level &v = h->lv[l];
-        if (!h->prm.fused || h->prm.relax != BMG_RELAX_POINT || h->prm.cycle_sym || h->prm.affine)
+        if (!h->prm.fused || h->prm.relax != BMG_RELAX_POINT || h->prm.affine)
             break;
-        TRY(fused_plan_level(h->fplan, l, v.nx, v.ny, v.pitch, v.kind, h->prm.nu1, h->prm.nu2, (v.pitch & 1) == 0));
+        TRY(fused_plan_level(h->fplan, l, v.nx, v.ny, v.pitch, v.kind, h->prm.nu1, h->prm.nu2, (v.pitch & 1) == 0,
+                             h->prm.cycle_sym == 1));
         LevelPlan &lp = h->fplan.lv[l];
         if (!(lp.down && lp.up)) {
             lp.down = lp.up = false;

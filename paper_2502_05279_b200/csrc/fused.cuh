@@ -28,6 +28,7 @@ struct FusedGeom {
     size_t smem = 0;
     bool ok = false;
     bool wave = false;  // 5-point down leg: the register-wavefront kernel (k_wave_down5)
+    bool rev = false;   // up leg: colours in reverse order (cycle_sym, c12)
 };
 
 struct LevelPlan {
@@ -42,8 +43,9 @@ struct FusedPlan {
 };
 
 // Decide per level whether the fused kernels run and with which geometry.
+// rev: the up legs run the colours in reverse order (cycle_sym = 1, c12)
 bmg_status_t fused_plan_level(FusedPlan &fp, int l, int nx, int ny, long long pitch, int kind, int nu1, int nu2,
-                              bool aligned);
+                              bool aligned, bool rev = false);
 
 // Down leg of level l: nu1 sweeps on (f, uin) -> uout, fc = P^T(f - A uout), uc = 0 (if non-null).
 // uin == nullptr: a zero start (the correction scheme's coarse levels, c9) that is not read.

@@ -1011,11 +1011,16 @@ __global__ void __launch_bounds__(32 * WV_WARPS, 2) k_wave_down5(FArgs a, const 
 }
 
 // ------------------------------------------------------------------ up kernel
-template <int KIND, int NS, int WD, int D, int PPT, int E>
+// REV (the symmetric cycle's adjoint post-smoother, c12): colours in reverse
+// order -- 5-point black before red, 9-point 3, 2, 1, 0 (odd rows first, odd
+// columns first) -- and the correction skips the points of that first pass.
+template <int KIND, int NS, int WD, int D, int PPT, int E, bool REV = false>
 __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
     k_fused_up(FArgs a, const __grid_constant__ TMaps tmaps)
 {
     using C = Cfg<KIND, NS, WD, D, true, PPT, E>;
+    // weight planes fetched: 5-point forward -> X/Y half, reversed -> Z half; 9-point all
+    constexpr int P0 = (KIND == 5 && REV) ? CI_LNE : C::WP0;
     constexpr int NA = C::NA, H = C::H, TX = C::TX, WC = C::WC, HW = C::HW, NPG = C::NPG;
     constexpr int RM = C::RM, SD = C::SD, AM = C::AM, AS = C::AS;
     extern __shared__ __align__(128) double sm[];
@@ -1090,7 +1095,7 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
             uint64_t *b = &bar[SD + slot];
             mbar_arrive_tx(b, (uint32_t)((1 + C::NWP) * WC * 8));
             tma_2d(sE + slot * WC, &tmaps.e, cxl, Knext - a.eroff, b);
-            tma_3d(sC + slot * C::NWP * WC, &tmaps.c, cxl, Knext - a.ci.roff, C::WP0, b);
+            tma_3d(sC + slot * C::NWP * WC, &tmaps.c, cxl, Knext - a.ci.roff, P0, b);
             Knext++;
         }
     };
@@ -1103,11 +1108,13 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
     // Points of the first colour pass (5-point: C and Z; 9-point: C) are skipped:
     // that pass overwrites them from their neighbours alone, so the result is
     // bitwise the same as correcting them.
-    constexpr int NW = C::NWP, P0 = C::WP0;
+    constexpr int NW = C::NWP;
     auto correct_task = [&](int x, int sx, int e) {
         if (x < lo1 || x > hi1)
             return;
-        if (KIND == 5 ? !((e + x) & 1) : (!e && !(x & 1)))
+        const bool first_pass = KIND == 5 ? (REV ? ((e + x) & 1) : !((e + x) & 1))
+                                          : (REV ? (e && (x & 1)) : (!e && !(x & 1)));
+        if (first_pass)
             return;
         const int Ka = x >> 1, Kb = (x + 1) >> 1;
         mbar_wait(&bar[SD + ((Ka - Klo) & 3)], ((Ka - Klo) >> 2) & 1);
@@ -1221,20 +1228,22 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
             rg.wait(grp - G_ST0, t - 1);
             if (KIND == 5) {
                 const int k = grp - G_ST0 + 1, d = 2 * k + 1, r = t - d;
+                const int col = REV ? (k & 1) : ((k - 1) & 1);  // stage k's colour
                 if (r > lo && r < hi && r >= 1 && r <= ny)
                     colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1),
-                                                   (((k - 1) & 1) - r) & 1, kc);
+                                                   (col - r) & 1, kc);
             } else {
                 // active 9-point row stage(s): k with (t-1-2k) & 1 == (k-1) & 1, i.e. (t + k) even
-                const int k = ((t & 1) ? 1 : 2) + 2 * grp, d = 2 * k + 1, r = t - d;
+                // (REV: (t + k) odd -- odd rows first -- and odd columns before even)
+                const int k = ((t & 1) ? (REV ? 2 : 1) : (REV ? 1 : 2)) + 2 * grp, d = 2 * k + 1, r = t - d;
                 const bool act = k <= NS && r > lo && r < hi && r >= 1 && r <= ny;
                 if (act)
-                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), 0,
-                                                   kc);
+                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1),
+                                                   REV ? 1 : 0, kc);
                 group_sync(1 + grp, NPG);
                 if (act)
-                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), 1,
-                                                   kc);
+                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1),
+                                                   REV ? 0 : 1, kc);
                 group_sync(1 + grp, NPG);
             }
         } else {
@@ -1349,6 +1358,8 @@ static void set_attrs()
     if (su <= g_smem_optin)
         cudaFuncSetAttribute(k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)su);
+        cudaFuncSetAttribute(k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)su);
     cudaGetLastError();  // an unsupported instance is simply not planned (plan_grid checks the size)
 }
 
@@ -1385,7 +1396,7 @@ static void plan_grid(FusedGeom &g, int nx, int ny, int warm)
 }
 
 bmg_status_t fused_plan_level(FusedPlan &fp, int l, int nx, int ny, long long pitch, int kind, int nu1, int nu2,
-                              bool aligned)
+                              bool aligned, bool rev)
 {
     LevelPlan &lp = fp.lv[l];
     lp.down = lp.up = false;
@@ -1417,6 +1428,7 @@ bmg_status_t fused_plan_level(FusedPlan &fp, int l, int nx, int ny, long long pi
         nsu == 2 ? fill_geom<5, 2>(lp.gu, true) : fill_geom<5, 4>(lp.gu, true);
         plan_grid(lp.gd, nx, ny, 2 * nsd + 3);
         plan_grid(lp.gu, nx, ny, 2 * nsu + 2);
+        lp.gu.rev = rev;
         lp.down = lp.gd.ok;
         lp.up = lp.gu.ok;
         return BMG_OK;
@@ -1430,6 +1442,7 @@ bmg_status_t fused_plan_level(FusedPlan &fp, int l, int nx, int ny, long long pi
     }
     plan_grid(lp.gd, nx, ny, 2 * nsd + 4);
     plan_grid(lp.gu, nx, ny, 2 * nsu + 2);
+    lp.gu.rev = rev;
     lp.down = lp.gd.ok;
     lp.up = lp.gu.ok;
     return BMG_OK;
@@ -1533,7 +1546,12 @@ template <int KIND, int NS>
 static void launch_up(const FusedGeom &g, const FArgs &a, const TMaps &tm, cudaStream_t s)
 {
     using I = Inst<KIND, NS>;
-    k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a, tm);
+    if (g.rev)
+        k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP, true><<<g.nstrips * g.nchunks, g.threads, g.smem,
+                                                                            s>>>(a, tm);
+    else
+        k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a,
+                                                                                                                   tm);
 }
 
 static FArgs make_args(const FusedGeom &g, const Op &A, const CIv &ci)

@@ -282,6 +282,33 @@ def test_leg_parity_level0(orc, wl, nx, ny, fused):
     s.close()
 
 
+@pytest.mark.parametrize("wl,nx,ny", [("lognormal", 63, 63), ("checker", 127, 127), ("random9", 200, 131),
+                                      ("lognormal", 300, 257), ("checker_off3", 95, 47), ("random9", 33, 33)])
+@pytest.mark.parametrize("nu2", [1, 2])
+@pytest.mark.parametrize("fused", [1, 0])
+def test_up_leg_sym_parity(orc, wl, nx, ny, nu2, fused):
+    """cycle_sym = 1 (c12): the up leg's post-smoother is the adjoint sweep (colours
+    in reverse order; on the fused path the REV instance of the up kernel, whose
+    correction skips the reversed first colour)."""
+    st = P.workload(wl, nx, ny)
+    prm = bmg.bmg_params_default()
+    prm.fused, prm.cycle_sym, prm.nu1, prm.nu2 = fused, 1, nu2, nu2
+    s = bmg.Solver(st, prm)
+    if s.L < 2:
+        pytest.skip("single level")
+    st9 = orc.expand_stencil(st)
+    _, ci = orc.Hierarchy(st).export_level(0)
+    f = P.field_uniform(nx, ny, seed=51)
+    u0 = P.field_uniform(nx, ny, seed=52)
+    ec = P.field_uniform(nx // 2, ny // 2, seed=53)
+    uout = s.grid()
+    bmg.bmg_correct_smooth(s.h, 0, s.grid(f), s.grid(u0), s.level_grid(1, ec), uout)
+    torch.cuda.synchronize()
+    ref = orc.relax_adjoint(st9, st.kind, f, orc.interp_add(ci, ec, u0), nu2)
+    assert_iterate_close(bmg.from_device(uout, nx), ref, rtol=1e-13)
+    s.close()
+
+
 def test_random_shapes_vcycle_parity(orc):
     """Seeded sweep over shapes the fixed cases miss (odd/even, thin rectangles, sizes
     straddling the fused / tail / per-step thresholds and the strip width): one fused

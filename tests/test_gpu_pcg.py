@@ -43,7 +43,9 @@ def assert_iterate_close(g, o, rtol=1e-12):
 
 @pytest.mark.parametrize("wl,nx,ny,nu,mode", [("lognormal", 63, 63, 1, "point"), ("random9", 33, 47, 1, "point"),
                                               ("checker", 127, 127, 2, "point"), ("lognormal", 300, 257, 2, "point"),
-                                              ("aniso", 63, 63, 1, "yline"), ("lognormal", 40, 33, 1, "altline")])
+                                              ("aniso", 63, 63, 1, "yline"), ("lognormal", 40, 33, 1, "altline"),
+                                              ("random9", 161, 130, 1, "point"), ("random9", 200, 211, 2, "point"),
+                                              ("checker_off3", 255, 190, 1, "point")])
 def test_symmetric_cycle_parity(orc, wl, nx, ny, nu, mode):
     st = P.workload(wl, nx, ny)
     s = bmg.Solver(st, params(nu, nu, mode))
@@ -58,7 +60,8 @@ def test_symmetric_cycle_parity(orc, wl, nx, ny, nu, mode):
 
 
 @pytest.mark.parametrize("wl,n,mode,tol", [("lognormal", 63, "point", 1e-10), ("checker", 127, "point", 1e-10),
-                                           ("random9", 65, "point", 1e-10), ("aniso", 63, "yline", 1e-9)])
+                                           ("random9", 65, "point", 1e-10), ("aniso", 63, "yline", 1e-9),
+                                           ("checker", 511, "point", 1e-10), ("random9", 257, "point", 1e-10)])
 def test_pcg_parity(orc, wl, n, mode, tol):
     st = P.workload(wl, n, n)
     s = bmg.Solver(st, params(1, 1, mode))
