@@ -77,6 +77,7 @@ def lib():
             "orc_vcycle": (None, [c_void_p, _dp, _dp, c_int]),
             "orc_residual_norm": (c_double, [c_void_p, _dp, _dp]),
             "orc_solve": (c_int, [c_void_p, _dp, _dp, c_double, c_int, _ip, _dp]),
+            "orc_solve_block": (c_int, [c_void_p, c_int, _dp, _dp, c_double, c_int, _ip, _dp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -295,3 +296,14 @@ class Hierarchy:
         it = ctypes.c_int()
         rc = lib().orc_solve(self._h, _p(np.ascontiguousarray(f)), _p(u), tol, maxiter, ctypes.byref(it), _p(hist))
         return u, it.value, hist[: it.value + 1], rc
+
+    def solve_block(self, F, U, tol, maxiter):
+        """c15 block multi-RHS solve: F, U of shape (nrhs, ny+2, nx+2).  Returns
+        (U, block steps, hist (steps+1, nrhs) absolute norms, status)."""
+        F = np.ascontiguousarray(F, dtype=np.float64)
+        U = np.array(U, dtype=np.float64, copy=True, order="C")
+        K = F.shape[0]
+        hist = np.zeros((maxiter + 1, K))
+        it = ctypes.c_int()
+        rc = lib().orc_solve_block(self._h, K, _p(F), _p(U), tol, maxiter, ctypes.byref(it), _p(hist))
+        return U, it.value, hist[: it.value + 1], rc

@@ -819,6 +819,63 @@ int orc_solve(orc_hier *h, const double *f, double *u, double tol, int maxiter, 
 }
 
 /* ------------------------------------------------------------------------
+ * c15: block multi-RHS solve (§5, "solve
+ * several initial vectors in block fashion").  nrhs independent systems
+ * A x_c = f_c share the hierarchy; each block step applies one V-cycle (c9)
+ * to every column, then measures every column's residual.  The block stops
+ * when EVERY column meets its own test ||r_c|| <= tol ||f_c|| (a column that
+ * met it earlier keeps being cycled), or after maxiter block steps.  A column
+ * with f_c = 0 is set to x_c = 0 and counts as converged.
+ * f, u: nrhs grid functions one after another ((ny+2)(nx+2) each);
+ * hist: (maxiter+1) rows of nrhs norms, row k after k block steps.
+ * ---------------------------------------------------------------------- */
+int orc_solve_block(orc_hier *h, int nrhs, const double *f, double *u, double tol, int maxiter, int *iters,
+                    double *hist)
+{
+    orc_level *v = &h->lv[0];
+    size_t np = (size_t)(v->nx + 2) * (size_t)(v->ny + 2);
+    double *fn = malloc(sizeof(double) * (size_t)nrhs), *rn = malloc(sizeof(double) * (size_t)nrhs);
+    if (!fn || !rn) {
+        free(fn);
+        free(rn);
+        return ORC_ENOMEM;
+    }
+    for (int c = 0; c < nrhs; c++) {
+        fn[c] = orc_norm2(v->nx, v->ny, f + c * np);
+        if (fn[c] == 0.0)
+            memset(u + c * np, 0, sizeof(double) * np);
+        rn[c] = orc_residual_norm(h, f + c * np, u + c * np);
+        if (hist)
+            hist[c] = rn[c];
+    }
+    int k = 0;
+    for (;;) {
+        int done = 1;
+        for (int c = 0; c < nrhs; c++)
+            if (rn[c] > tol * fn[c])
+                done = 0;
+        if (done || k >= maxiter)
+            break;
+        for (int c = 0; c < nrhs; c++)
+            orc_vcycle(h, f + c * np, u + c * np, 1);
+        k++;
+        for (int c = 0; c < nrhs; c++) {
+            rn[c] = orc_residual_norm(h, f + c * np, u + c * np);
+            if (hist)
+                hist[(size_t)k * nrhs + c] = rn[c];
+        }
+    }
+    int ok = 1;
+    for (int c = 0; c < nrhs; c++)
+        if (rn[c] > tol * fn[c])
+            ok = 0;
+    *iters = k;
+    free(fn);
+    free(rn);
+    return ok ? ORC_OK : ORC_ENOTCONV;
+}
+
+/* ------------------------------------------------------------------------
  * c13: V-cycle-preconditioned conjugate gradients (the
  * Krylov acceleration Cedar offers around BoxMG)
  * ---------------------------------------------------------------------- */
