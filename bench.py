@@ -217,6 +217,8 @@ def main():
     ap.add_argument("--solve-tol", type=float, default=None, help="tolerance of the timed solve (default per config)")
     ap.add_argument("--pcg", type=int, default=0, metavar="NU",
                     help="also time V(NU,NU)-preconditioned CG (symmetric cycle, c12/c13) on the same problem")
+    ap.add_argument("--nrhs", type=int, default=0, metavar="K",
+                    help="also time the block multi-RHS cycle (c15, bmg_vcycle_block) with K right-hand sides")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -371,6 +373,39 @@ def main():
             s2.close()
             del f2, x2
 
+    # block multi-RHS (c15): K right-hand sides per cycle, every kernel
+    # reading the operator / weights once for all K; device-timed block cycles from the
+    # same rhs in every column, then a block solve from x0 = 0
+    block = None
+    if args.nrhs > 0 and not distributed and args.relax == "point":
+        K = args.nrhs
+        fb = solver.block_grid(K)
+        fb.copy_(f.unsqueeze(-1).expand(-1, -1, K))
+        xb = solver.block_grid(K)
+        solver.vcycle_block(fb, xb, args.warmup)
+        nb = max(10, args.steps // 4)
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        b0.record(stream)
+        solver.vcycle_block(fb, xb, nb)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        bms = b0.elapsed_time(b1) / nb
+        xb.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        itb, hb, rcb = solver.solve_block(fb, xb, args.solve_tol or SOLVE_TOL.get(args.config, 1e-10), SOLVE_MAXIT)
+        dtb = time.perf_counter() - t0
+        block = {"nrhs": K, "ms_per_block_cycle": bms, "ms_per_rhs_cycle": bms / K,
+                 "rhs_cycles_per_s": K * 1e3 / bms, "vs_single_rhs_cycle": ms_per_step / (bms / K),
+                 "solve": {"steps": itb, "converged": rcb == 0, "ms": dtb * 1e3,
+                           "final_rel_residual": float(hb[-1].max() / fnorm) if len(hb) else None},
+                 "note": ("K columns interleaved per point; per-step block kernels (one read of the stencil and "
+                          "weights per block), CUDA-graph replay, device-timed; vs_single_rhs_cycle = the "
+                          "single-RHS cycle time of this line / the block cycle time per right-hand side")}
+        del fb, xb
+        torch.cuda.empty_cache()
+
     # e2e: the same metric through the public API with HOST buffers (pinned): per step
     # H2D of rhs and x, one V(2,1) cycle, D2H of x; host wall clock, max over ranks
     e2e = None
@@ -448,6 +483,8 @@ def main():
         "solve": solve,
         "cpu_baseline": cpu,
     }
+    if block is not None:
+        line["block"] = block
     if rank == 0:
         print(json.dumps(line), flush=True)
     solver.close()

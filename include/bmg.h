@@ -156,6 +156,44 @@ bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol,
 bmg_status_t bmg_pcg(bmg_solver_t h, const double *rhs, double *x, double tol, int maxiter, int *iters_out,
                      double *hist_host, void *cuda_stream);
 
+/*
+ * Block multi-RHS V-cycles (§5 "solve
+ * several initial vectors in block fashion"; DESIGN §3 c15): nrhs systems
+ * A x_c = rhs_c on the same hierarchy, every kernel of the cycle applying one
+ * read of the operator / interpolation weights to all nrhs columns.
+ *   rhs, x: DEVICE arrays of (ny+2) * pitch * nrhs doubles, INTERLEAVED:
+ *           column c of point (i, j) at ((size_t)j * pitch + i) * nrhs + c
+ *           (16-byte aligned when nrhs is even); ring as in bmg_vcycle.
+ *   nrhs:   1 .. BMG_MAX_NRHS.
+ * Column c after ncycles block cycles is bmg_vcycle(rhs_c, x_c, ncycles): the
+ * same per-point operations in the same order (up to the FMA contraction the
+ * compiler picks in the single-RHS kernels: a few ulp).  Point relaxation only
+ * (params.relax != POINT: EINVAL); cycle_sym and affine apply.  Single-GPU
+ * handles only.  Workspace (per level r, and f, u below level 0, nrhs columns
+ * each) is allocated on the first call for a given nrhs and owned by the
+ * handle; a call with another nrhs reallocates it.  Asynchronous on cuda_stream.
+ */
+#define BMG_MAX_NRHS 8
+bmg_status_t bmg_vcycle_block(bmg_solver_t h, int nrhs, const double *rhs, double *x, int ncycles,
+                              void *cuda_stream);
+
+/* ||rhs_c - A x_c||_2 for every column into norms_host[0..nrhs) (host);
+ * synchronises cuda_stream.  Layout and limits as bmg_vcycle_block. */
+bmg_status_t bmg_residual_norm_block(bmg_solver_t h, int nrhs, const double *rhs, const double *x,
+                                     double *norms_host, void *cuda_stream);
+
+/*
+ * Block solve (c15): hist row 0 = the nrhs initial residual norms; each block
+ * step is one block V-cycle followed by the nrhs residual norms (row k).  Stops
+ * when EVERY column has ||r_c|| <= tol*||rhs_c|| (a column that met its test
+ * earlier keeps being cycled) or after maxiter steps.  A column with
+ * ||rhs_c|| = 0 is set to x_c = 0 and counts as converged.
+ * hist_host: (maxiter+1) * nrhs doubles (row-major, may be NULL); iters_out:
+ * block steps taken (may be NULL).  Returns ENOTCONV if maxiter was reached.
+ */
+bmg_status_t bmg_solve_block(bmg_solver_t h, int nrhs, const double *rhs, double *x, double tol, int maxiter,
+                             int *iters_out, double *hist_host, void *cuda_stream);
+
 /* ||rhs - A x||_2 over the fine interior ("l2 norm"), deterministic
  * fixed-tree reduction; optional r_out (device, setup pitch, ring untouched)
  * receives the residual.  *norm_host is a host double.  Synchronises. */

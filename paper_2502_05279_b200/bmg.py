@@ -25,8 +25,11 @@ EXPORTS = (
     "bmg_num_levels", "bmg_level_shape", "bmg_level_pitch", "bmg_export_level", "bmg_relax", "bmg_residual",
     "bmg_restrict", "bmg_interp_add", "bmg_smooth_restrict", "bmg_correct_smooth", "bmg_cycle_kernel_count", "bmg_timing",
     "bmg_timing_read", "bmg_destroy", "bmg_strerror",
-    "bmg_last_error_detail", "bmg_partition", "bmg_setup_dist", "bmg_local_rows",
+    "bmg_last_error_detail", "bmg_partition", "bmg_setup_dist", "bmg_local_rows", "bmg_vcycle_block",
+    "bmg_residual_norm_block", "bmg_solve_block",
 )
+
+BMG_MAX_NRHS = 8
 
 BMG_HALO = 6
 
@@ -77,6 +80,9 @@ def lib():
             "bmg_vcycle_host": (i, [vp, vp, vp, i, vp]),
             "bmg_solve": (i, [vp, vp, vp, d, i, ip, dp, vp]),
             "bmg_pcg": (i, [vp, vp, vp, d, i, ip, dp, vp]),
+            "bmg_vcycle_block": (i, [vp, i, vp, vp, i, vp]),
+            "bmg_residual_norm_block": (i, [vp, i, vp, vp, dp, vp]),
+            "bmg_solve_block": (i, [vp, i, vp, vp, d, i, ip, dp, vp]),
             "bmg_residual_norm": (i, [vp, vp, vp, vp, dp, vp]),
             "bmg_num_levels": (i, [vp, ip]),
             "bmg_level_shape": (i, [vp, i, ip, ip, ip]),
@@ -171,6 +177,28 @@ def bmg_pcg(h, rhs, x, tol: float, maxiter: int, stream=None):
     rc = lib().bmg_pcg(h, _ptr(rhs), _ptr(x), tol, maxiter, ctypes.byref(it),
                        hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream(stream))
     _check(rc, "bmg_pcg", ok=(BMG_OK, BMG_ENOTCONV))
+    return it.value, hist[: it.value + 1], rc
+
+
+def bmg_vcycle_block(h, nrhs: int, rhs, x, ncycles: int = 1, stream=None):
+    """rhs, x: device tensors (ny+2, pitch, nrhs) -- the interleaved block layout."""
+    _check(lib().bmg_vcycle_block(h, nrhs, _ptr(rhs), _ptr(x), ncycles, _stream(stream)), "bmg_vcycle_block")
+
+
+def bmg_residual_norm_block(h, nrhs: int, rhs, x, stream=None) -> np.ndarray:
+    out = np.zeros(nrhs)
+    _check(lib().bmg_residual_norm_block(h, nrhs, _ptr(rhs), _ptr(x), out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                         _stream(stream)), "bmg_residual_norm_block")
+    return out
+
+
+def bmg_solve_block(h, nrhs: int, rhs, x, tol: float, maxiter: int, stream=None):
+    """Returns (block steps, hist (steps+1, nrhs) absolute norms, status)."""
+    it = ctypes.c_int()
+    hist = np.zeros((maxiter + 1, nrhs))
+    rc = lib().bmg_solve_block(h, nrhs, _ptr(rhs), _ptr(x), tol, maxiter, ctypes.byref(it),
+                               hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream(stream))
+    _check(rc, "bmg_solve_block", ok=(BMG_OK, BMG_ENOTCONV))
     return it.value, hist[: it.value + 1], rc
 
 
@@ -310,6 +338,21 @@ def from_device(t, nx: int) -> np.ndarray:
     return t[:, : nx + 2].cpu().numpy().copy()
 
 
+def to_device_block(arrays, pitch: int, device="cuda"):
+    """nrhs (ny+2, nx+2) host arrays -> (ny+2, pitch, nrhs) device tensor (block layout)."""
+    import torch
+
+    a = np.stack([np.asarray(x, dtype=np.float64) for x in arrays], axis=-1)
+    t = torch.zeros((a.shape[0], pitch, a.shape[2]), dtype=torch.float64, device=device)
+    t[:, : a.shape[1], :] = torch.from_numpy(np.ascontiguousarray(a)).to(device)
+    return t
+
+
+def from_device_block(t, nx: int) -> np.ndarray:
+    """(ny+2, pitch, nrhs) device tensor -> (nrhs, ny+2, nx+2) host array."""
+    return np.ascontiguousarray(np.moveaxis(t[:, : nx + 2, :].cpu().numpy(), -1, 0))
+
+
 class Solver:
     """Convenience owner of a bmg_solver_t for a problems.Stencil (device copies kept)."""
 
@@ -339,8 +382,23 @@ class Solver:
             return torch.zeros((ny + 2, p), dtype=torch.float64, device=self.device)
         return to_device(a, p, self.device)
 
+    def block_grid(self, nrhs: int, arrays=None):
+        """(ny+2, pitch, nrhs) device tensor in the block layout (zeros or the given arrays)."""
+        import torch
+
+        if arrays is None:
+            return torch.zeros((self.ny + 2, self.pitch, nrhs), dtype=torch.float64, device=self.device)
+        assert len(arrays) == nrhs
+        return to_device_block(arrays, self.pitch, self.device)
+
     def vcycle(self, rhs, x, ncycles=1):
         bmg_vcycle(self.h, rhs, x, ncycles)
+
+    def vcycle_block(self, rhs, x, ncycles=1):
+        bmg_vcycle_block(self.h, rhs.shape[-1], rhs, x, ncycles)
+
+    def solve_block(self, rhs, x, tol, maxiter):
+        return bmg_solve_block(self.h, rhs.shape[-1], rhs, x, tol, maxiter)
 
     def solve(self, rhs, x, tol, maxiter):
         return bmg_solve(self.h, rhs, x, tol, maxiter)

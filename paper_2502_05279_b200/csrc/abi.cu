@@ -111,6 +111,13 @@ struct bmg_solver {
     bool cycle_err = false;           // a planned fused leg was rejected while enqueuing a cycle
     std::vector<cudaEvent_t> tev;     // event pairs (start, end) per recorded launch
     size_t tev_used = 0;
+    // c15 block multi-RHS workspace (bmg_vcycle_block) for blk_K columns: per level
+    // r (all but the coarsest), f and u (below level 0), K-interleaved, one arena
+    int blk_K = 0;
+    void *blk_arena = nullptr;
+    std::vector<double *> blk_f, blk_u, blk_r;
+    double *blk_partials = nullptr, *blk_norm = nullptr;
+    std::map<std::pair<const void *, const void *>, cudaGraphExec_t> bgraphs;  // block cycle graphs (blk_K)
 
     CIv civ(int l) const
     {
@@ -194,6 +201,10 @@ bmg_status_t bmg_destroy(bmg_solver_t h)
             cudaEventDestroy(e);
     for (void *p : h->allocs)
         cudaFree(p);
+    for (auto &kv : h->bgraphs)
+        cudaGraphExecDestroy(kv.second);
+    if (h->blk_arena)
+        cudaFree(h->blk_arena);
     if (h->h_norm)
         cudaFreeHost(h->h_norm);
     if (h->cap)
@@ -855,6 +866,201 @@ bmg_status_t bmg_pcg(bmg_solver_t h, const double *rhs, double *x, double tol, i
     if (iters_out)
         *iters_out = k;
     return rn <= tol * fn ? BMG_OK : fail(BMG_ENOTCONV, "maxiter reached");
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- c15 block multi-RHS
+// The block workspace for K columns (reallocated when K changes; block graphs
+// hold its pointers, so they go with it).
+static bmg_status_t block_workspace(bmg_solver *h, int K, cudaStream_t s)
+{
+    if (h->blk_K == K)
+        return BMG_OK;
+    CK(cudaStreamSynchronize(s));
+    CK(cudaDeviceSynchronize());
+    for (auto &kv : h->bgraphs)
+        cudaGraphExecDestroy(kv.second);
+    h->bgraphs.clear();
+    if (h->blk_arena)
+        cudaFree(h->blk_arena);
+    h->blk_arena = nullptr;
+    h->blk_K = 0;
+    const int L = h->L;
+    h->blk_f.assign(L, nullptr);
+    h->blk_u.assign(L, nullptr);
+    h->blk_r.assign(L, nullptr);
+    size_t used = 0;
+    double *arena = nullptr;
+    auto take = [&](size_t n) {
+        double *p = arena ? arena + used : nullptr;
+        used += (n + 31) / 32 * 32;
+        return p;
+    };
+    for (int pass = 0; pass < 2; pass++) {
+        if (pass == 1) {
+            CK(cudaMalloc(&h->blk_arena, used * sizeof(double)));
+            arena = (double *)h->blk_arena;
+            CK(cudaMemsetAsync(arena, 0, used * sizeof(double), s));
+            used = 0;
+        }
+        for (int l = 0; l < L; l++) {
+            const size_t np = (size_t)(h->lv[l].ny + 2) * (size_t)h->lv[l].pitch * (size_t)K;
+            if (l + 1 < L)
+                h->blk_r[l] = take(np);
+            if (l > 0) {
+                h->blk_f[l] = take(np);
+                h->blk_u[l] = take(np);
+            }
+        }
+        h->blk_partials = take((size_t)K * NORM_BLOCKS);
+        h->blk_norm = take(K);
+    }
+    h->blk_K = K;
+    return BMG_OK;
+}
+
+// One block V(nu1,nu2) cycle on s: the per-step path of enqueue_cycle (fused = 0)
+// with every step's kernel in its K-column form.
+static int enqueue_cycle_block(bmg_solver *h, int K, const double *f0, double *u0, cudaStream_t s)
+{
+    int n = 0;
+    const int L = h->L;
+    auto F = [&](int l) { return l == 0 ? f0 : (const double *)h->blk_f[l]; };
+    auto U = [&](int l) { return l == 0 ? u0 : h->blk_u[l]; };
+    for (int l = 0; l + 1 < L; l++) {
+        const Op A = h->lv[l].op();
+        launch_relax_block(K, A, F(l), U(l), h->prm.nu1, s, &n);
+        if (h->prm.nu1 > 0 && !h->prm.affine) {  // the vanishing restriction, residual fused in (r not stored)
+            launch_resid_restrict_block(K, A, h->civ(l), F(l), U(l), h->blk_f[l + 1], h->blk_u[l + 1], s);
+            n += 1;
+        } else {  // c14 needs r on the up leg; nu1 = 0 restricts every residual
+            launch_residual_block(K, A, F(l), U(l), h->blk_r[l], s);
+            launch_restrict_block(K, A, h->civ(l), h->blk_r[l], h->blk_f[l + 1], h->blk_u[l + 1], s, h->prm.nu1 > 0);
+            n += 2;
+        }
+    }
+    launch_coarse_solve_block(K, h->lv[L - 1].op(), h->chol, F(L - 1), U(L - 1), s);
+    n += 1;
+    for (int l = L - 2; l >= 0; l--) {
+        const Op A = h->lv[l].op();
+        launch_interp_add_block(K, A, h->civ(l), U(l + 1), U(l), s, h->prm.affine ? h->blk_r[l] : nullptr);
+        n += 1;
+        launch_relax_block(K, A, F(l), U(l), h->prm.nu2, s, &n, h->prm.cycle_sym == 1);
+    }
+    return n;
+}
+
+static bmg_status_t block_args(bmg_solver *h, int K, const void *rhs, const void *x, const char *who)
+{
+    if (!h || !rhs || !x || K < 1 || K > BMG_MAX_NRHS)
+        return fail(BMG_EINVAL, std::string("bad arguments to ") + who + " (nrhs in 1.." +
+                                    std::to_string(BMG_MAX_NRHS) + ")");
+    if (h->dist)
+        return fail(BMG_EINVAL, std::string(who) + ": single-GPU handles only");
+    if (h->prm.relax != BMG_RELAX_POINT)
+        return fail(BMG_EINVAL, std::string(who) + ": point relaxation only");
+    if (K % 2 == 0 && (!al16(rhs) || !al16(x)))
+        return fail(BMG_EINVAL, std::string(who) + ": rhs/x must be 16-byte aligned for even nrhs");
+    return BMG_OK;
+}
+
+static bmg_status_t block_norms(bmg_solver *h, int K, const double *rhs, const double *x, double *out,
+                                cudaStream_t s)
+{
+    if (x)
+        launch_resid_norm_block(K, h->lv[0].op(), rhs, x, h->blk_partials, h->blk_norm, s);
+    else
+        launch_norm_block(K, h->lv[0].op(), rhs, h->blk_partials, h->blk_norm, s);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h->h_norm, h->blk_norm, K * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    memcpy(out, h->h_norm, K * sizeof(double));
+    return BMG_OK;
+}
+
+extern "C" {
+
+bmg_status_t bmg_vcycle_block(bmg_solver_t h, int nrhs, const double *rhs, double *x, int ncycles, void *cuda_stream)
+{
+    TRY(block_args(h, nrhs, rhs, x, "bmg_vcycle_block"));
+    if (ncycles < 0)
+        return fail(BMG_EINVAL, "bmg_vcycle_block: ncycles < 0");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    TRY(block_workspace(h, nrhs, s));
+    auto key = std::make_pair((const void *)rhs, (const void *)x);
+    auto it = h->bgraphs.find(key);
+    if (it == h->bgraphs.end()) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+        enqueue_cycle_block(h, nrhs, rhs, x, h->cap);
+        cudaError_t e = cudaStreamEndCapture(h->cap, &g);
+        if (e != cudaSuccess)
+            return fail(BMG_ECUDA, std::string("block graph capture: ") + cudaGetErrorString(e));
+        cudaGraphExec_t ex;
+        e = cudaGraphInstantiate(&ex, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess)
+            return fail(BMG_ECUDA, std::string("block graph instantiate: ") + cudaGetErrorString(e));
+        if (h->bgraphs.size() > 16) {
+            for (auto &kv : h->bgraphs)
+                cudaGraphExecDestroy(kv.second);
+            h->bgraphs.clear();
+        }
+        it = h->bgraphs.emplace(key, ex).first;
+    }
+    for (int k = 0; k < ncycles; k++)
+        CK(cudaGraphLaunch(it->second, s));
+    return BMG_OK;
+}
+
+bmg_status_t bmg_residual_norm_block(bmg_solver_t h, int nrhs, const double *rhs, const double *x,
+                                     double *norms_host, void *cuda_stream)
+{
+    TRY(block_args(h, nrhs, rhs, x, "bmg_residual_norm_block"));
+    if (!norms_host)
+        return fail(BMG_EINVAL, "bmg_residual_norm_block: null norms_host");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    TRY(block_workspace(h, nrhs, s));
+    return block_norms(h, nrhs, rhs, x, norms_host, s);
+}
+
+bmg_status_t bmg_solve_block(bmg_solver_t h, int nrhs, const double *rhs, double *x, double tol, int maxiter,
+                             int *iters_out, double *hist_host, void *cuda_stream)
+{
+    TRY(block_args(h, nrhs, rhs, x, "bmg_solve_block"));
+    if (maxiter < 0 || !(tol >= 0))
+        return fail(BMG_EINVAL, "bad arguments to bmg_solve_block");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    TRY(block_workspace(h, nrhs, s));
+    if (iters_out)
+        *iters_out = 0;
+    const int K = nrhs;
+    double fn[BMG_MAX_NRHS], rn[BMG_MAX_NRHS];
+    TRY(block_norms(h, K, rhs, nullptr, fn, s));
+    for (int c = 0; c < K; c++)
+        if (fn[c] == 0.0)  // SPEC S:444 per column
+            launch_zero_col_block(K, h->lv[0].op(), x, c, s);
+    TRY(block_norms(h, K, rhs, x, rn, s));
+    if (hist_host)
+        memcpy(hist_host, rn, K * sizeof(double));
+    auto done = [&]() {
+        for (int c = 0; c < K; c++)
+            if (rn[c] > tol * fn[c])
+                return false;
+        return true;
+    };
+    int k = 0;
+    while (!done() && k < maxiter) {
+        TRY(bmg_vcycle_block(h, K, rhs, x, 1, cuda_stream));
+        k++;
+        TRY(block_norms(h, K, rhs, x, rn, s));
+        if (hist_host)
+            memcpy(hist_host + (size_t)k * K, rn, K * sizeof(double));
+    }
+    if (iters_out)
+        *iters_out = k;
+    return done() ? BMG_OK : fail(BMG_ENOTCONV, "maxiter reached");
 }
 
 bmg_status_t bmg_num_levels(bmg_solver_t h, int *L)

@@ -96,6 +96,26 @@ __device__ __forceinline__ double rcp_pos(double b)
     return fma(r, fma(-b, r, 1.0), r);
 }
 
+// CTA-wide sum in a fixed tree (warp shuffles, then one warp over the warp
+// sums): the deterministic reduction of the norms and dot products.
+__device__ __forceinline__ double block_sum(double v)
+{
+    __shared__ double sh[32];
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_down_sync(0xffffffffu, v, o);
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0)
+        sh[wid] = v;
+    __syncthreads();
+    int nw = blockDim.x >> 5;
+    v = (threadIdx.x < nw) ? sh[threadIdx.x] : 0.0;
+    if (wid == 0)
+        for (int o = 16; o > 0; o >>= 1)
+            v += __shfl_down_sync(0xffffffffu, v, o);
+    __syncthreads();
+    return v;
+}
+
 // ---- launchers (kernels.cu) ----
 void launch_ingest(int nx, int ny, int kind, long long pitch, const double *const src[5], double *const dst[5],
                    int *err, cudaStream_t s, int j0, int j1);
@@ -135,6 +155,27 @@ void launch_dot(const Op &A, const double *a, const double *b, double *partials,
 void launch_cg_update(const Op &A, double alpha, const double *p, const double *q, double *x, double *r,
                       cudaStream_t s);
 void launch_cg_direction(const Op &A, double beta, const double *z, double *p, cudaStream_t s);
+
+// c15 block multi-RHS kernels (kernels_block.cu): K = 1..BMG_MAX_NRHS columns
+// stored interleaved, element (j, i, c) at (j*pitch + i)*K + c; per column the
+// per-step kernels' arithmetic.  The norm launchers leave K results in result[0..K)
+// and need K*NORM_BLOCKS partials.
+void launch_relax_block(int K, const Op &A, const double *f, double *u, int nsweeps, cudaStream_t s, int *nlaunch,
+                        bool rev = false);
+void launch_residual_block(int K, const Op &A, const double *f, const double *u, double *r, cudaStream_t s);
+void launch_restrict_block(int K, const Op &A, const CIv &ci, const double *r, double *fc, double *uc,
+                           cudaStream_t s, bool vanish);
+// residual + vanishing restriction fused (after nu1 >= 1 point-GS sweeps; r never stored)
+void launch_resid_restrict_block(int K, const Op &A, const CIv &ci, const double *f, const double *u, double *fc,
+                                 double *uc, cudaStream_t s);
+void launch_interp_add_block(int K, const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s,
+                             const double *r = nullptr);
+void launch_coarse_solve_block(int K, const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s);
+void launch_resid_norm_block(int K, const Op &A, const double *f, const double *u, double *partials, double *result,
+                             cudaStream_t s);
+void launch_norm_block(int K, const Op &A, const double *g, double *partials, double *result, cudaStream_t s);
+void launch_zero_block(int K, const Op &A, double *x, cudaStream_t s);
+void launch_zero_col_block(int K, const Op &A, double *x, int col, cudaStream_t s);
 
 // Small levels l0..L-1 of the cycle in one single-CTA launch (k_tail).  Lives in
 // device memory (filled once at setup); level 0's f/u are launch arguments.

@@ -1,0 +1,667 @@
+// kernels_block.cu -- block multi-RHS V-cycle kernels (DESIGN §3 c15; SURVEY
+// §8(f) row 2; §5: "solve several initial vectors in block
+// fashion").
+//
+// K right-hand sides (and K iterates) are stored interleaved: element (j, i, c)
+// at (j*pitch + i)*K + c.  A thread loads the operator row / interpolation
+// weights of its point ONCE and applies them to the K columns, whose values
+// sit in K consecutive doubles (16-byte vector loads for even K).  The stencil
+// and weight planes -- the dominant bytes of a cycle -- are thus read
+// once per block instead of once per right-hand side.
+//
+// Per column every kernel performs the per-step kernels' operations
+// (kernels_cycle.cu) in the same source order, with every product-sum pinned
+// to that order (__dmul_rn/__fma_rn); column c of a block cycle is the
+// single-RHS cycle on column c up to the FMA contractions nvcc picks there.
+#include "bmg_internal.cuh"
+
+namespace bmg {
+
+namespace {
+
+// K consecutive doubles (16-byte aligned for even K: cudaMalloc'd bases and an
+// even element offset)
+template <int K>
+__device__ __forceinline__ void ldk(const double *__restrict__ p, double (&v)[K])
+{
+    if constexpr (K % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < K / 2; c++) {
+            const double2 t = reinterpret_cast<const double2 *>(p)[c];
+            v[2 * c] = t.x;
+            v[2 * c + 1] = t.y;
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < K; c++)
+            v[c] = p[c];
+    }
+}
+
+template <int K>
+__device__ __forceinline__ void stk(double *__restrict__ p, const double (&v)[K])
+{
+    if constexpr (K % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < K / 2; c++)
+            reinterpret_cast<double2 *>(p)[c] = make_double2(v[2 * c], v[2 * c + 1]);
+    } else {
+#pragma unroll
+        for (int c = 0; c < K; c++)
+            p[c] = v[c];
+    }
+}
+
+template <int K>
+__device__ __forceinline__ void setk(double *__restrict__ p, double x)
+{
+    double v[K];
+#pragma unroll
+    for (int c = 0; c < K; c++)
+        v[c] = x;
+    stk<K>(p, v);
+}
+
+// Work split: a thread owns W = 2 columns of its point (one 16-byte access per
+// neighbour) for even K, W = 1 for odd K, and TP = K / W threads share a point
+// (consecutive lanes: a warp touches 32/TP points' contiguous column blocks).
+// The operator row / weights are loaded by each of the TP threads (same address,
+// one L1 transaction).
+template <int K>
+struct Split {
+    static constexpr int W = (K % 2 == 0) ? 2 : 1;
+    static constexpr int TP = K / W;
+};
+
+// (off-diagonal part of A u)_p for W columns at element stride K (u already
+// offset to the first of them), fig:stencil_operator order SW,S,SE,W,E,NW,N,NE
+// (offdiag() of kernels_cycle.cu per column)
+template <int W, int K>
+__device__ __forceinline__ void offdiag_w(const Row9 &a, const double *__restrict__ u, long long p, long long P,
+                                          double (&s)[W])
+{
+    double t[W];
+    ldk<W>(u + (p - P - 1) * K, t);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        s[c] = __dmul_rn(a.sw, t[c]);
+    ldk<W>(u + (p - P) * K, t);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        s[c] = __fma_rn(a.s, t[c], s[c]);
+    ldk<W>(u + (p - P + 1) * K, t);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        s[c] = __fma_rn(a.se, t[c], s[c]);
+    ldk<W>(u + (p - 1) * K, t);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        s[c] = __fma_rn(a.w, t[c], s[c]);
+    ldk<W>(u + (p + 1) * K, t);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        s[c] = __fma_rn(a.e, t[c], s[c]);
+    ldk<W>(u + (p + P - 1) * K, t);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        s[c] = __fma_rn(a.nw, t[c], s[c]);
+    ldk<W>(u + (p + P) * K, t);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        s[c] = __fma_rn(a.n, t[c], s[c]);
+    ldk<W>(u + (p + P + 1) * K, t);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        s[c] = __fma_rn(a.ne, t[c], s[c]);
+}
+
+// v[c] = w * q[c] / v[c] += w * q[c] / v[c] += q[c].  Every product-sum chain in
+// this file is written with __dmul_rn / __fma_rn in source order: left to the
+// compiler, a*b + c*d may contract to either fma(c,d,a*b) or fma(a,b,c*d), and
+// the block kernels' rounding is pinned to the source order instead.
+template <int W, int K>
+__device__ __forceinline__ void wset(double (&v)[W], double w, const double *__restrict__ q, long long qi)
+{
+    double t[W];
+    ldk<W>(q + qi * K, t);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        v[c] = __dmul_rn(w, t[c]);
+}
+
+template <int W, int K>
+__device__ __forceinline__ void wadd(double (&v)[W], double w, const double *__restrict__ q, long long qi)
+{
+    double t[W];
+    ldk<W>(q + qi * K, t);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        v[c] = __fma_rn(w, t[c], v[c]);
+}
+
+template <int W, int K>
+__device__ __forceinline__ void add1(double (&v)[W], const double *__restrict__ q, long long qi)
+{
+    double t[W];
+    ldk<W>(q + qi * K, t);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        v[c] += t[c];
+}
+
+// ------------------------------------------------------------------ relaxation (c6)
+template <int K>
+__global__ void kb_relax5(Op A, const double *__restrict__ f, double *__restrict__ u, int colour)
+{
+    constexpr int W = Split<K>::W, TP = Split<K>::TP;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y + 1;
+    if (j > A.ny)
+        return;
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x, sub = gx % TP;
+    const int i = ((((1 + j) & 1) == colour) ? 1 : 2) + 2 * (gx / TP);
+    if (i > A.nx)
+        return;
+    const long long P = A.pitch, p = j * P + i;
+    const double o = A.O[p], w = A.W[p], e = A.W[p + 1], s = A.S[p], n = A.S[p + P];
+    const double rc = rcp_pos(o);
+    const double *ub = u + sub * W;
+    double us[W], uw[W], ue[W], un[W], fp[W], out[W];
+    ldk<W>(ub + (p - P) * K, us);
+    ldk<W>(ub + (p - 1) * K, uw);
+    ldk<W>(ub + (p + 1) * K, ue);
+    ldk<W>(ub + (p + P) * K, un);
+    ldk<W>(f + sub * W + p * K, fp);
+#pragma unroll
+    for (int c = 0; c < W; c++) {
+        double acc = __dmul_rn(s, us[c]);
+        acc = __fma_rn(w, uw[c], acc);
+        acc = __fma_rn(e, ue[c], acc);
+        acc = __fma_rn(n, un[c], acc);
+        out[c] = (fp[c] - acc) * rc;
+    }
+    stk<W>(u + sub * W + p * K, out);
+}
+
+template <int K>
+__global__ void kb_relax9(Op A, const double *__restrict__ f, double *__restrict__ u, int colour)
+{
+    constexpr int W = Split<K>::W, TP = Split<K>::TP;
+    const int j = 2 * (blockIdx.y * blockDim.y + threadIdx.y) + ((colour >> 1) ? 1 : 2);
+    if (j > A.ny)
+        return;
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x, sub = gx % TP;
+    const int i = 2 * (gx / TP) + ((colour & 1) ? 1 : 2);
+    if (i > A.nx)
+        return;
+    const long long P = A.pitch, p = j * P + i;
+    const Row9 a = load_row9(A, p);
+    const double rc = rcp_pos(a.o);
+    double sm[W], fp[W];
+    offdiag_w<W, K>(a, u + sub * W, p, P, sm);
+    ldk<W>(f + sub * W + p * K, fp);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        sm[c] = (fp[c] - sm[c]) * rc;
+    stk<W>(u + sub * W + p * K, sm);
+}
+
+// ------------------------------------------------------------------ residual
+template <int K>
+__global__ void kb_residual(Op A, const double *__restrict__ f, const double *__restrict__ u, double *__restrict__ r)
+{
+    constexpr int W = Split<K>::W, TP = Split<K>::TP;
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x, sub = gx % TP, i = gx / TP;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    if (i > A.nx + 1 || j > A.ny + 1)
+        return;
+    const long long P = A.pitch, p = j * P + i;
+    if (i == 0 || j == 0 || i > A.nx || j > A.ny) {
+        setk<W>(r + sub * W + p * K, 0.0);
+        return;
+    }
+    const Row9 a = load_row9(A, p);
+    double sm[W], up[W], fp[W];
+    offdiag_w<W, K>(a, u + sub * W, p, P, sm);
+    ldk<W>(u + sub * W + p * K, up);
+    ldk<W>(f + sub * W + p * K, fp);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        sm[c] = fp[c] - __fma_rn(a.o, up[c], sm[c]);
+    stk<W>(r + sub * W + p * K, sm);
+}
+
+// ------------------------------------------------------------------ restriction (fig:restrict_kernel)
+template <int K>
+__global__ void kb_restrict(Op A, CIv ci, const double *__restrict__ q, double *__restrict__ qc,
+                            double *__restrict__ uc, bool vanish)
+{
+    constexpr int W = Split<K>::W, TP = Split<K>::TP;
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x, sub = gx % TP, I = gx / TP;
+    const int J = blockIdx.y * blockDim.y + threadIdx.y;
+    if (I > A.nx / 2 + 1 || J > A.ny / 2 + 1)
+        return;
+    const long long C = ci.pitch, c = J * C + I;
+    if (uc)
+        setk<W>(uc + sub * W + c * K, 0.0);
+    if (I == 0 || J == 0 || I > A.nx / 2 || J > A.ny / 2) {
+        setk<W>(qc + sub * W + c * K, 0.0);
+        return;
+    }
+    const long long P = A.pitch, p = (2 * J) * P + 2 * I;
+    const double *qb = q + sub * W;
+    double v[W];
+    if (vanish && A.kind == 5) {  // restrict_pt_vanish, 5-point: centre + Z terms
+        wset<W, K>(v, ci.w[CI_LNE][c], qb, p - P - 1);
+        wadd<W, K>(v, ci.w[CI_LNW][c + 1], qb, p - P + 1);
+        add1<W, K>(v, qb, p);
+        wadd<W, K>(v, ci.w[CI_LSE][c + C], qb, p + P - 1);
+        wadd<W, K>(v, ci.w[CI_LSW][c + C + 1], qb, p + P + 1);
+    } else if (vanish) {  // 9-point: centre + X/Y terms
+        wset<W, K>(v, ci.w[CI_LA][c], qb, p - P);
+        wadd<W, K>(v, ci.w[CI_LR][c], qb, p - 1);
+        add1<W, K>(v, qb, p);
+        wadd<W, K>(v, ci.w[CI_LL][c + 1], qb, p + 1);
+        wadd<W, K>(v, ci.w[CI_LB][c + C], qb, p + P);
+    } else {  // restrict_pt
+        wset<W, K>(v, ci.w[CI_LNE][c], qb, p - P - 1);
+        wadd<W, K>(v, ci.w[CI_LA][c], qb, p - P);
+        wadd<W, K>(v, ci.w[CI_LNW][c + 1], qb, p - P + 1);
+        wadd<W, K>(v, ci.w[CI_LR][c], qb, p - 1);
+        add1<W, K>(v, qb, p);
+        wadd<W, K>(v, ci.w[CI_LL][c + 1], qb, p + 1);
+        wadd<W, K>(v, ci.w[CI_LSE][c + C], qb, p + P - 1);
+        wadd<W, K>(v, ci.w[CI_LB][c + C], qb, p + P);
+        wadd<W, K>(v, ci.w[CI_LSW][c + C + 1], qb, p + P + 1);
+    }
+    stk<W>(qc + sub * W + c * K, v);
+}
+
+// Residual and vanishing restriction in one pass (after nu1 >= 1 point-GS sweeps,
+// DESIGN §5.2): each coarse point evaluates r = f - A u at exactly the fine points
+// its restriction keeps -- 5-point: the centre and the 4 Z corners; 9-point: the
+// centre and the 4 X/Y edge points -- so r is never stored.  Per column the
+// residual is the per-step one (f - fma(a_O, u, offdiag)) and the sum is
+// restrict_pt_vanish's, in source order.
+template <int W, int K>
+__device__ __forceinline__ void resid_w(const Op &A, const double *__restrict__ f, const double *__restrict__ u,
+                                        int i, int j, double (&r)[W])
+{
+    const long long P = A.pitch, p = (long long)j * P + i;
+    double sm[W], up[W], fp[W];
+    if (A.kind == 5) {  // the zero corner terms of offdiag() contribute exact zeros
+        const double o = A.O[p], w = A.W[p], e = A.W[p + 1], s = A.S[p], n = A.S[p + P];
+        double t[W];
+        ldk<W>(u + (p - P) * K, t);
+#pragma unroll
+        for (int c = 0; c < W; c++)
+            sm[c] = __dmul_rn(s, t[c]);
+        ldk<W>(u + (p - 1) * K, t);
+#pragma unroll
+        for (int c = 0; c < W; c++)
+            sm[c] = __fma_rn(w, t[c], sm[c]);
+        ldk<W>(u + (p + 1) * K, t);
+#pragma unroll
+        for (int c = 0; c < W; c++)
+            sm[c] = __fma_rn(e, t[c], sm[c]);
+        ldk<W>(u + (p + P) * K, t);
+#pragma unroll
+        for (int c = 0; c < W; c++)
+            sm[c] = __fma_rn(n, t[c], sm[c]);
+        ldk<W>(u + p * K, up);
+        ldk<W>(f + p * K, fp);
+#pragma unroll
+        for (int c = 0; c < W; c++)
+            r[c] = fp[c] - __fma_rn(o, up[c], sm[c]);
+    } else {
+        const Row9 a = load_row9(A, p);
+        offdiag_w<W, K>(a, u, p, P, sm);
+        ldk<W>(u + p * K, up);
+        ldk<W>(f + p * K, fp);
+#pragma unroll
+        for (int c = 0; c < W; c++)
+            r[c] = fp[c] - __fma_rn(a.o, up[c], sm[c]);
+    }
+}
+
+template <int W>
+__device__ __forceinline__ void racc(double (&v)[W], double w, const double (&r)[W], bool first)
+{
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        v[c] = first ? __dmul_rn(w, r[c]) : __fma_rn(w, r[c], v[c]);
+}
+
+template <int K>
+__global__ void kb_resid_restrict(Op A, CIv ci, const double *__restrict__ f, const double *__restrict__ u,
+                                  double *__restrict__ qc, double *__restrict__ uc)
+{
+    constexpr int W = Split<K>::W, TP = Split<K>::TP;
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x, sub = gx % TP, I = gx / TP;
+    const int J = blockIdx.y * blockDim.y + threadIdx.y;
+    if (I > A.nx / 2 + 1 || J > A.ny / 2 + 1)
+        return;
+    const long long C = ci.pitch, c = J * C + I;
+    if (uc)
+        setk<W>(uc + sub * W + c * K, 0.0);
+    if (I == 0 || J == 0 || I > A.nx / 2 || J > A.ny / 2) {
+        setk<W>(qc + sub * W + c * K, 0.0);
+        return;
+    }
+    const double *fb = f + sub * W, *ub = u + sub * W;
+    const int i = 2 * I, j = 2 * J;
+    double v[W], r[W];
+    if (A.kind == 5) {  // centre + Z terms
+        resid_w<W, K>(A, fb, ub, i - 1, j - 1, r);
+        racc<W>(v, ci.w[CI_LNE][c], r, true);
+        resid_w<W, K>(A, fb, ub, i + 1, j - 1, r);
+        racc<W>(v, ci.w[CI_LNW][c + 1], r, false);
+        resid_w<W, K>(A, fb, ub, i, j, r);
+#pragma unroll
+        for (int k = 0; k < W; k++)
+            v[k] = __dadd_rn(v[k], r[k]);
+        resid_w<W, K>(A, fb, ub, i - 1, j + 1, r);
+        racc<W>(v, ci.w[CI_LSE][c + C], r, false);
+        resid_w<W, K>(A, fb, ub, i + 1, j + 1, r);
+        racc<W>(v, ci.w[CI_LSW][c + C + 1], r, false);
+    } else {  // centre + X/Y terms
+        resid_w<W, K>(A, fb, ub, i, j - 1, r);
+        racc<W>(v, ci.w[CI_LA][c], r, true);
+        resid_w<W, K>(A, fb, ub, i - 1, j, r);
+        racc<W>(v, ci.w[CI_LR][c], r, false);
+        resid_w<W, K>(A, fb, ub, i, j, r);
+#pragma unroll
+        for (int k = 0; k < W; k++)
+            v[k] = __dadd_rn(v[k], r[k]);
+        resid_w<W, K>(A, fb, ub, i + 1, j, r);
+        racc<W>(v, ci.w[CI_LL][c + 1], r, false);
+        resid_w<W, K>(A, fb, ub, i, j + 1, r);
+        racc<W>(v, ci.w[CI_LB][c + C], r, false);
+    }
+    stk<W>(qc + sub * W + c * K, v);
+}
+
+// ------------------------------------------------------------------ interpolation + correction (c7, c14)
+template <int K>
+__global__ void kb_interp_add(Op A, CIv ci, const double *__restrict__ e, const double *__restrict__ r,
+                              double *__restrict__ u)
+{
+    constexpr int W = Split<K>::W, TP = Split<K>::TP;
+    // the parity of i alternates with blockIdx.x, so that a warp (one j) takes one
+    // branch below while the two parities of a strip run side by side (u read once)
+    const int gx = (blockIdx.x >> 1) * blockDim.x + threadIdx.x, sub = gx % TP;
+    const int i = 2 * (gx / TP) + 1 + (blockIdx.x & 1);
+    const int j = blockIdx.y * blockDim.y + threadIdx.y + 1;
+    if (i > A.nx || j > A.ny)
+        return;
+    const long long C = ci.pitch;
+    const int I = (i + 1) >> 1, J = (j + 1) >> 1;
+    const double *eb = e + sub * W;
+    double s[W];
+    if (!(i & 1) && !(j & 1)) {  // C point
+        ldk<W>(eb + ((j >> 1) * C + (i >> 1)) * K, s);
+    } else if ((i & 1) && !(j & 1)) {  // X
+        const long long c = (j >> 1) * C + I;
+        wset<W, K>(s, ci.w[CI_LL][c], eb, c - 1);
+        wadd<W, K>(s, ci.w[CI_LR][c], eb, c);
+    } else if (!(i & 1) && (j & 1)) {  // Y
+        const long long c = J * C + (i >> 1);
+        wset<W, K>(s, ci.w[CI_LB][c], eb, c - C);
+        wadd<W, K>(s, ci.w[CI_LA][c], eb, c);
+    } else {  // Z
+        const long long c = J * C + I;
+        wset<W, K>(s, ci.w[CI_LSW][c], eb, c - C - 1);
+        wadd<W, K>(s, ci.w[CI_LSE][c], eb, c - C);
+        wadd<W, K>(s, ci.w[CI_LNW][c], eb, c - 1);
+        wadd<W, K>(s, ci.w[CI_LNE][c], eb, c);
+    }
+    const long long p = j * A.pitch + i;
+    if (r && ((i & 1) || (j & 1))) {  // c14 affine term r / a_O at the non-coarse points
+        double rp[W];
+        ldk<W>(r + sub * W + p * K, rp);
+        const double o = A.O[p];
+#pragma unroll
+        for (int c = 0; c < W; c++)
+            s[c] += rp[c] / o;
+    } else if (r) {  // affine_pt() is 0 at C points: s += 0.0, as the per-step kernel
+#pragma unroll
+        for (int c = 0; c < W; c++)
+            s[c] += 0.0;
+    }
+    double up[W];
+    ldk<W>(u + sub * W + p * K, up);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        up[c] += s[c];
+    stk<W>(u + sub * W + p * K, up);
+}
+
+// ------------------------------------------------------------------ coarsest solve (c8)
+// CTA c: column c, the substitutions of coarse_solve_cta.
+template <int K>
+__global__ void kb_coarse_solve(Op A, const double *__restrict__ Lf, const double *__restrict__ f,
+                                double *__restrict__ u)
+{
+    extern __shared__ double b[];
+    const int n = A.nx * A.ny, col = blockIdx.x;
+    for (int p = threadIdx.x; p < n; p += blockDim.x)
+        b[p] = f[((p / A.nx + 1) * A.pitch + p % A.nx + 1) * K + col];
+    __syncthreads();
+    for (int k = 0; k < n; k++) {  // L y = b
+        double bk = b[k] / Lf[(long long)k * n + k];
+        __syncthreads();
+        if (threadIdx.x == 0)
+            b[k] = bk;
+        for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x)
+            b[i] -= Lf[(long long)i * n + k] * bk;
+        __syncthreads();
+    }
+    for (int k = n - 1; k >= 0; k--) {  // L^T x = y
+        double bk = b[k] / Lf[(long long)k * n + k];
+        __syncthreads();
+        if (threadIdx.x == 0)
+            b[k] = bk;
+        for (int i = threadIdx.x; i < k; i += blockDim.x)
+            b[i] -= Lf[(long long)k * n + i] * bk;
+        __syncthreads();
+    }
+    for (int p = threadIdx.x; p < n; p += blockDim.x)
+        u[((p / A.nx + 1) * A.pitch + p % A.nx + 1) * K + col] = b[p];
+}
+
+// ------------------------------------------------------------------ norms (per column, fixed trees)
+template <int K, bool RESID>
+__global__ void kb_norm_partial(Op A, const double *__restrict__ f, const double *__restrict__ u,
+                                double *__restrict__ partials)
+{
+    double acc[K];
+#pragma unroll
+    for (int c = 0; c < K; c++)
+        acc[c] = 0.0;
+    const long long P = A.pitch;
+    for (int j = A.ylo + blockIdx.x; j < A.yhi; j += gridDim.x) {
+        for (int i = 1 + threadIdx.x; i <= A.nx; i += blockDim.x) {
+            const long long p = j * P + i;
+            double v[K];
+            ldk<K>(f + p * K, v);
+            if (RESID) {
+                const Row9 a = load_row9(A, p);
+                double s[K], up[K];
+                offdiag_w<K, K>(a, u, p, P, s);
+                ldk<K>(u + p * K, up);
+#pragma unroll
+                for (int c = 0; c < K; c++)
+                    v[c] = v[c] - __fma_rn(a.o, up[c], s[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < K; c++)
+                acc[c] = __fma_rn(v[c], v[c], acc[c]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < K; c++) {
+        const double t = block_sum(acc[c]);
+        if (threadIdx.x == 0)
+            partials[c * NORM_BLOCKS + blockIdx.x] = t;
+    }
+}
+
+// CTA c: column c's partials, the tree of k_norm_final
+__global__ void kb_norm_final(const double *__restrict__ partials, double *__restrict__ result)
+{
+    double acc = 0.0;
+    const double *pc = partials + blockIdx.x * NORM_BLOCKS;
+    for (int k = threadIdx.x; k < NORM_BLOCKS; k += blockDim.x)
+        acc += pc[k];
+    acc = block_sum(acc);
+    if (threadIdx.x == 0)
+        result[blockIdx.x] = sqrt(acc);
+}
+
+__global__ void kb_zero(long long n, double *x)
+{
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t < n)
+        x[t] = 0.0;
+}
+
+// ------------------------------------------------------------------ launchers
+template <int K>
+struct Launch {
+    static constexpr int TP = Split<K>::TP;
+    static void relax(const Op &A, const double *f, double *u, int nsweeps, cudaStream_t s, int *nlaunch, bool rev)
+    {
+        const dim3 b(32, 8);
+        for (int sw = 0; sw < nsweeps; sw++) {
+            if (A.kind == 5) {
+                const dim3 g(((A.nx / 2 + 1) * TP + 31) / 32, (A.ny + 7) / 8);
+                for (int c = 0; c < 2; c++)
+                    kb_relax5<K><<<g, b, 0, s>>>(A, f, u, rev ? 1 - c : c);
+                if (nlaunch)
+                    *nlaunch += 2;
+            } else {
+                const dim3 g(((A.nx / 2 + 1) * TP + 31) / 32, (A.ny / 2 + 1 + 7) / 8);
+                for (int c = 0; c < 4; c++)
+                    kb_relax9<K><<<g, b, 0, s>>>(A, f, u, rev ? 3 - c : c);
+                if (nlaunch)
+                    *nlaunch += 4;
+            }
+        }
+    }
+    static void residual(const Op &A, const double *f, const double *u, double *r, cudaStream_t s)
+    {
+        const dim3 b(32, 8), g(((A.nx + 2) * TP + 31) / 32, (A.ny + 2 + 7) / 8);
+        kb_residual<K><<<g, b, 0, s>>>(A, f, u, r);
+    }
+    static void restrict_(const Op &A, const CIv &ci, const double *r, double *fc, double *uc, cudaStream_t s,
+                          bool vanish)
+    {
+        const dim3 b(32, 8), g(((A.nx / 2 + 2) * TP + 31) / 32, (A.ny / 2 + 2 + 7) / 8);
+        kb_restrict<K><<<g, b, 0, s>>>(A, ci, r, fc, uc, vanish);
+    }
+    static void resid_restrict(const Op &A, const CIv &ci, const double *f, const double *u, double *fc, double *uc,
+                               cudaStream_t s)
+    {
+        const dim3 b(32, 8), g(((A.nx / 2 + 2) * TP + 31) / 32, (A.ny / 2 + 2 + 7) / 8);
+        kb_resid_restrict<K><<<g, b, 0, s>>>(A, ci, f, u, fc, uc);
+    }
+    static void interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s, const double *r)
+    {
+        const dim3 b(32, 8), g(2 * (((A.nx + 1) / 2 * TP + 31) / 32), (A.ny + 7) / 8);
+        kb_interp_add<K><<<g, b, 0, s>>>(A, ci, ec, r, u);
+    }
+    static void coarse(const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s)
+    {
+        const int n = A.nx * A.ny;
+        const int threads = n < 32 ? 32 : (n < 1024 ? ((n + 31) / 32) * 32 : 1024);
+        kb_coarse_solve<K><<<K, threads, sizeof(double) * n, s>>>(A, Lf, f, u);
+    }
+    static void norm(const Op &A, const double *f, const double *u, double *partials, double *result, cudaStream_t s)
+    {
+        if (u)
+            kb_norm_partial<K, true><<<NORM_BLOCKS, 256, 0, s>>>(A, f, u, partials);
+        else
+            kb_norm_partial<K, false><<<NORM_BLOCKS, 256, 0, s>>>(A, f, nullptr, partials);
+        kb_norm_final<<<K, 1024, 0, s>>>(partials, result);
+    }
+};
+
+#define BMG_BLOCK_DISPATCH(K, call)           \
+    switch (K) {                              \
+    case 1: Launch<1>::call; break;           \
+    case 2: Launch<2>::call; break;           \
+    case 3: Launch<3>::call; break;           \
+    case 4: Launch<4>::call; break;           \
+    case 5: Launch<5>::call; break;           \
+    case 6: Launch<6>::call; break;           \
+    case 7: Launch<7>::call; break;           \
+    case 8: Launch<8>::call; break;           \
+    default: break;                           \
+    }
+
+}  // namespace
+
+void launch_relax_block(int K, const Op &A, const double *f, double *u, int nsweeps, cudaStream_t s, int *nlaunch,
+                        bool rev)
+{
+    BMG_BLOCK_DISPATCH(K, relax(A, f, u, nsweeps, s, nlaunch, rev));
+}
+
+void launch_residual_block(int K, const Op &A, const double *f, const double *u, double *r, cudaStream_t s)
+{
+    BMG_BLOCK_DISPATCH(K, residual(A, f, u, r, s));
+}
+
+void launch_restrict_block(int K, const Op &A, const CIv &ci, const double *r, double *fc, double *uc,
+                           cudaStream_t s, bool vanish)
+{
+    BMG_BLOCK_DISPATCH(K, restrict_(A, ci, r, fc, uc, s, vanish));
+}
+
+void launch_resid_restrict_block(int K, const Op &A, const CIv &ci, const double *f, const double *u, double *fc,
+                                 double *uc, cudaStream_t s)
+{
+    BMG_BLOCK_DISPATCH(K, resid_restrict(A, ci, f, u, fc, uc, s));
+}
+
+void launch_interp_add_block(int K, const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s,
+                             const double *r)
+{
+    BMG_BLOCK_DISPATCH(K, interp_add(A, ci, ec, u, s, r));
+}
+
+void launch_coarse_solve_block(int K, const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s)
+{
+    BMG_BLOCK_DISPATCH(K, coarse(A, Lf, f, u, s));
+}
+
+void launch_resid_norm_block(int K, const Op &A, const double *f, const double *u, double *partials, double *result,
+                             cudaStream_t s)
+{
+    BMG_BLOCK_DISPATCH(K, norm(A, f, u, partials, result, s));
+}
+
+void launch_norm_block(int K, const Op &A, const double *g, double *partials, double *result, cudaStream_t s)
+{
+    BMG_BLOCK_DISPATCH(K, norm(A, g, nullptr, partials, result, s));
+}
+
+__global__ void kb_zero_col(long long n, int K, int col, double *x)
+{
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t < n)
+        x[t * K + col] = 0.0;
+}
+
+void launch_zero_col_block(int K, const Op &A, double *x, int col, cudaStream_t s)
+{
+    const long long n = (A.ny + 2) * A.pitch;
+    kb_zero_col<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, K, col, x);
+}
+
+void launch_zero_block(int K, const Op &A, double *x, cudaStream_t s)
+{
+    const long long n = (A.ny + 2) * A.pitch * K;
+    kb_zero<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, x);
+}
+
+}  // namespace bmg

@@ -268,26 +268,8 @@ void launch_zero_interior(const Op &A, double *x, cudaStream_t s)
 
 // ---------------------------------------------------------------- norms
 // Deterministic two-pass l2 norm: NORM_BLOCKS fixed blocks each reduce a
-// fixed row set (warp shuffle tree + fixed smem tree), then one block sums
-// the partials in a fixed tree.  Bitwise run-to-run reproducible.
-__device__ __forceinline__ double block_sum(double v)
-{
-    __shared__ double sh[32];
-    for (int o = 16; o > 0; o >>= 1)
-        v += __shfl_down_sync(0xffffffffu, v, o);
-    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0)
-        sh[wid] = v;
-    __syncthreads();
-    int nw = blockDim.x >> 5;
-    v = (threadIdx.x < nw) ? sh[threadIdx.x] : 0.0;
-    if (wid == 0)
-        for (int o = 16; o > 0; o >>= 1)
-            v += __shfl_down_sync(0xffffffffu, v, o);
-    __syncthreads();
-    return v;
-}
-
+// fixed row set (block_sum, bmg_internal.cuh), then one block sums the
+// partials in a fixed tree.  Bitwise run-to-run reproducible.
 template <bool RESID>
 __global__ void k_norm_partial(Op A, const double *__restrict__ f, const double *__restrict__ u,
                                double *__restrict__ r_out, double *__restrict__ partials)
