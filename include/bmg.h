@@ -151,7 +151,10 @@ bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol,
  * symmetric preconditioner: params nu1 == nu2 and cycle_sym = 1 (EINVAL
  * otherwise; single-GPU handles only).  Workspace: four level-0 arrays,
  * allocated on the first call and owned by the handle.  Returns ENOTCONV at
- * maxiter (x, hist valid).  Synchronises cuda_stream.
+ * maxiter (x, hist valid).  The host waits once per iteration (for ||r_k||);
+ * alpha and beta are formed on the device.  On return x and hist are final;
+ * the next iteration's preconditioner, enqueued speculatively before the last
+ * wait, may still be running on cuda_stream (it writes only the workspace).
  */
 bmg_status_t bmg_pcg(bmg_solver_t h, const double *rhs, double *x, double tol, int maxiter, int *iters_out,
                      double *hist_host, void *cuda_stream);

@@ -104,7 +104,8 @@ struct bmg_solver {
     long long dist_rows_total = 0;      // doubles of a level-0 rhs/x array of this handle
     int dist_local_ranks = 1;
     double *line_scr = nullptr;       // c11 line relaxation scratch (line modes only)
-    double *pcg_ws = nullptr;         // c13 PCG vectors r, z, p, q (level-0 arrays), lazily
+    double *pcg_ws = nullptr;         // c13 PCG vectors r, z, p, q (level-0 arrays) + scalars, lazily
+    cudaEvent_t pcg_ev = nullptr;     // marks the residual norm's arrival in h_norm
     int tail_l0 = 1 << 30;            // first level of the tail kernel (none: > L)
     TailPlan *tail = nullptr;         // its device-side plan
     bool timing = false;              // bmg_timing: timed graph variant, event pair per launch
@@ -199,6 +200,8 @@ bmg_status_t bmg_destroy(bmg_solver_t h)
     for (cudaEvent_t e : h->cev)
         if (e)
             cudaEventDestroy(e);
+    if (h->pcg_ev)
+        cudaEventDestroy(h->pcg_ev);
     for (void *p : h->allocs)
         cudaFree(p);
     for (auto &kv : h->bgraphs)
@@ -786,8 +789,12 @@ bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol,
 /*
  * c13: conjugate gradients preconditioned by one V(nu,nu) cycle from a zero
  * guess (symmetric with cycle_sym = 1, c12) -- the textbook PCG recurrences
- * as DESIGN §3 c13 states them, every vector step a kernel, the scalars
- * alpha, beta formed on the host from deterministic dot products.
+ * as DESIGN §3 c13 states them, every vector step a kernel.  The scalars
+ * alpha = rho/(p.q) and beta = rho'/rho are formed on the device from the
+ * deterministic dot products (slots of sc[]), so the host waits once per
+ * iteration, for ||r|| (the stopping test); the next iteration's
+ * preconditioner, rho' and direction -- which touch only z, p and sc -- are
+ * enqueued before that wait, so the GPU does not idle during it.
  */
 bmg_status_t bmg_pcg(bmg_solver_t h, const double *rhs, double *x, double tol, int maxiter, int *iters_out,
                      double *hist_host, void *cuda_stream)
@@ -805,19 +812,17 @@ bmg_status_t bmg_pcg(bmg_solver_t h, const double *rhs, double *x, double tol, i
     const Op A = v.op();
     const size_t np = (size_t)(v.ny + 2) * (size_t)v.pitch;
     if (!h->pcg_ws) {
-        TRY(dalloc(h, &h->pcg_ws, 4 * np));
-        CK(cudaMemsetAsync(h->pcg_ws, 0, 4 * np * sizeof(double), s));
+        TRY(dalloc(h, &h->pcg_ws, 4 * np + 32));
+        CK(cudaMemsetAsync(h->pcg_ws, 0, (4 * np + 32) * sizeof(double), s));
+        CK(cudaEventCreateWithFlags(&h->pcg_ev, cudaEventDisableTiming));
     }
-    double *r = h->pcg_ws, *z = r + np, *p = z + np, *q = p + np;
-    auto host_scalar = [&](double *out) -> bmg_status_t {
-        CK(cudaMemcpyAsync(h->h_norm, h->d_norm, sizeof(double), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        *out = h->h_norm[0];
-        return BMG_OK;
-    };
+    double *r = h->pcg_ws, *z = r + np, *p = z + np, *q = p + np, *sc = q + np;
+    enum { PQ = 1, RN = 2 };  // sc slots; rho alternates between slots 0 and 3
     double fn;
     launch_norm(A, rhs, h->partials, h->d_norm, s);
-    TRY(host_scalar(&fn));
+    CK(cudaMemcpyAsync(h->h_norm, h->d_norm, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    fn = h->h_norm[0];
     if (fn == 0.0) {
         launch_zero_interior(A, x, s);
         CK(cudaStreamSynchronize(s));
@@ -835,31 +840,31 @@ bmg_status_t bmg_pcg(bmg_solver_t h, const double *rhs, double *x, double tol, i
             launch_zero_interior(A, z, s);
             return bmg_vcycle(h, r, z, 1, cuda_stream);
         };
+        int cur = 0;  // slot of the current rho
         TRY(precondition());
         CK(cudaMemcpyAsync(p, z, np * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        double rho;
-        launch_dot(A, r, z, h->partials, h->d_norm, s);
-        TRY(host_scalar(&rho));
+        launch_dot(A, r, z, h->partials, sc + cur, s);
         while (k < maxiter) {
-            double pq;
             launch_matvec(A, p, q, s);
-            launch_dot(A, p, q, h->partials, h->d_norm, s);
-            TRY(host_scalar(&pq));
-            const double alpha = rho / pq;
-            launch_cg_update(A, alpha, p, q, x, r, s);
+            launch_dot(A, p, q, h->partials, sc + PQ, s);
+            launch_cg_update(A, sc, cur, PQ, p, q, x, r, s);  // alpha = rho / (p.q)
             k++;
-            launch_norm(A, r, h->partials, h->d_norm, s);
-            TRY(host_scalar(&rn));
+            launch_norm(A, r, h->partials, sc + RN, s);
+            CK(cudaMemcpyAsync(h->h_norm, sc + RN, sizeof(double), cudaMemcpyDeviceToHost, s));
+            CK(cudaEventRecord(h->pcg_ev, s));
+            // the next direction, speculatively (z, p and sc only; x and r are final)
+            const int nxt = 3 - cur;
+            TRY(precondition());
+            launch_dot(A, r, z, h->partials, sc + nxt, s);
+            launch_cg_direction(A, sc, nxt, cur, z, p, s);  // beta = rho' / rho
+            CK(cudaGetLastError());
+            CK(cudaEventSynchronize(h->pcg_ev));
+            rn = h->h_norm[0];
             if (hist_host)
                 hist_host[k] = rn;
             if (rn <= tol * fn)
                 break;
-            TRY(precondition());
-            double rho1;
-            launch_dot(A, r, z, h->partials, h->d_norm, s);
-            TRY(host_scalar(&rho1));
-            launch_cg_direction(A, rho1 / rho, z, p, s);
-            rho = rho1;
+            cur = nxt;
         }
     }
     CK(cudaGetLastError());

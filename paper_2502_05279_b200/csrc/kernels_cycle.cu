@@ -356,26 +356,30 @@ __global__ void k_sum_final(const double *__restrict__ partials, int n, double *
         *result = acc;
 }
 
-// x += alpha p; r -= alpha q  (interior)
-__global__ void k_cg_update(Op A, double alpha, const double *__restrict__ p, const double *__restrict__ q,
-                            double *__restrict__ x, double *__restrict__ r)
+// x += alpha p; r -= alpha q  (interior); alpha = sc[inum] / sc[iden] formed on the
+// device from the dot products (the same IEEE division the host would do)
+__global__ void k_cg_update(Op A, const double *__restrict__ sc, int inum, int iden, const double *__restrict__ p,
+                            const double *__restrict__ q, double *__restrict__ x, double *__restrict__ r)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x + 1;
     const int j = blockIdx.y * blockDim.y + threadIdx.y + A.ylo;
     if (i > A.nx || j >= A.yhi)
         return;
+    const double alpha = sc[inum] / sc[iden];
     const long long k = j * A.pitch + i;
     x[k] = fma(alpha, p[k], x[k]);
     r[k] = fma(-alpha, q[k], r[k]);
 }
 
-// p = z + beta p  (interior)
-__global__ void k_cg_direction(Op A, double beta, const double *__restrict__ z, double *__restrict__ p)
+// p = z + beta p  (interior); beta = sc[inum] / sc[iden]
+__global__ void k_cg_direction(Op A, const double *__restrict__ sc, int inum, int iden, const double *__restrict__ z,
+                               double *__restrict__ p)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x + 1;
     const int j = blockIdx.y * blockDim.y + threadIdx.y + A.ylo;
     if (i > A.nx || j >= A.yhi)
         return;
+    const double beta = sc[inum] / sc[iden];
     const long long k = j * A.pitch + i;
     p[k] = fma(beta, p[k], z[k]);
 }
@@ -397,17 +401,18 @@ void launch_dot(const Op &A, const double *a, const double *b, double *partials,
     k_sum_final<<<1, 1024, 0, s>>>(partials, NORM_BLOCKS, result);
 }
 
-void launch_cg_update(const Op &A, double alpha, const double *p, const double *q, double *x, double *r,
-                      cudaStream_t s)
+void launch_cg_update(const Op &A, const double *sc, int inum, int iden, const double *p, const double *q, double *x,
+                      double *r, cudaStream_t s)
 {
     const dim3 b(32, 8);
-    k_cg_update<<<interior_grid(A, b), b, 0, s>>>(A, alpha, p, q, x, r);
+    k_cg_update<<<interior_grid(A, b), b, 0, s>>>(A, sc, inum, iden, p, q, x, r);
 }
 
-void launch_cg_direction(const Op &A, double beta, const double *z, double *p, cudaStream_t s)
+void launch_cg_direction(const Op &A, const double *sc, int inum, int iden, const double *z, double *p,
+                         cudaStream_t s)
 {
     const dim3 b(32, 8);
-    k_cg_direction<<<interior_grid(A, b), b, 0, s>>>(A, beta, z, p);
+    k_cg_direction<<<interior_grid(A, b), b, 0, s>>>(A, sc, inum, iden, z, p);
 }
 
 // ---------------------------------------------------------------- coarsest solve
