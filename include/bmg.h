@@ -138,6 +138,9 @@ bmg_status_t bmg_vcycle_host(bmg_solver_t h, const double *rhs_host, double *x_h
  * x = 0 (interior) and returns 0 iterations.  iters_out (host, may be NULL)
  * receives the cycle count; hist_host (host, maxiter+1 doubles, may be NULL)
  * the absolute residual norms.  Returns ENOTCONV if maxiter was reached.
+ * Single-GPU handles run the loop on the device (one graph launch: a
+ * conditional WHILE node around cycle + norm + stopping test) and synchronise
+ * cuda_stream once; distributed handles loop on the host.
  */
 bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol, int maxiter, int *iters_out,
                        double *hist_host, void *cuda_stream);

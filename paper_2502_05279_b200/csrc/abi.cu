@@ -106,6 +106,12 @@ struct bmg_solver {
     double *line_scr = nullptr;       // c11 line relaxation scratch (line modes only)
     double *pcg_ws = nullptr;         // c13 PCG vectors r, z, p, q (level-0 arrays) + scalars, lazily
     cudaEvent_t pcg_ev = nullptr;     // marks the residual norm's arrival in h_norm
+    // device-side solve loop: per (rhs, x) a graph [WHILE: cycle, residual norm, k_solve_step]
+    std::map<std::pair<const void *, const void *>, cudaGraphExec_t> sgraphs;
+    SolveState *solve_st = nullptr;   // device state
+    SolveState *solve_st_h = nullptr; // pinned staging
+    double *solve_hist = nullptr;     // device history, solve_cap doubles
+    int solve_cap = 0;
     int tail_l0 = 1 << 30;            // first level of the tail kernel (none: > L)
     TailPlan *tail = nullptr;         // its device-side plan
     bool timing = false;              // bmg_timing: timed graph variant, event pair per launch
@@ -202,6 +208,12 @@ bmg_status_t bmg_destroy(bmg_solver_t h)
             cudaEventDestroy(e);
     if (h->pcg_ev)
         cudaEventDestroy(h->pcg_ev);
+    for (auto &kv : h->sgraphs)
+        cudaGraphExecDestroy(kv.second);
+    if (h->solve_hist)
+        cudaFree(h->solve_hist);
+    if (h->solve_st_h)
+        cudaFreeHost(h->solve_st_h);
     for (void *p : h->allocs)
         cudaFree(p);
     for (auto &kv : h->bgraphs)
@@ -641,6 +653,55 @@ static bmg_status_t get_graph(bmg_solver *h, const double *f, double *x, bool ti
     return BMG_OK;
 }
 
+// The device-side solve loop for (f, x): ONE graph whose conditional WHILE node
+// runs [V-cycle, residual norm, k_solve_step] until the stopping test fails --
+// no host round trip per cycle (conditional graph nodes).
+static bmg_status_t get_solve_graph(bmg_solver *h, const double *f, double *x, cudaGraphExec_t *out)
+{
+    auto key = std::make_pair((const void *)f, (const void *)x);
+    auto it = h->sgraphs.find(key);
+    if (it != h->sgraphs.end()) {
+        *out = it->second;
+        return BMG_OK;
+    }
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle hd;
+    CK(cudaGraphConditionalHandleCreate(&hd, g, 1, cudaGraphCondAssignDefault));  // enter the loop
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hd;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(h->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    h->cycle_err = false;
+    enqueue_cycle(h, f, x, h->cap);
+    launch_resid_norm(h->lv[0].op(), f, x, nullptr, h->partials, h->d_norm, h->cap);
+    launch_solve_step(hd, h->d_norm, h->solve_st, h->solve_hist, h->cap);
+    cudaError_t e = cudaStreamEndCapture(h->cap, &body);
+    if (e != cudaSuccess || h->cycle_err) {
+        cudaGraphDestroy(g);
+        return fail(BMG_ECUDA, std::string("solve graph capture: ") +
+                                   (h->cycle_err ? "a fused leg was rejected" : cudaGetErrorString(e)));
+    }
+    cudaGraphExec_t ex;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess)
+        return fail(BMG_ECUDA, std::string("solve graph instantiate: ") + cudaGetErrorString(e));
+    if (h->sgraphs.size() > 16) {
+        for (auto &kv : h->sgraphs)
+            cudaGraphExecDestroy(kv.second);
+        h->sgraphs.clear();
+    }
+    h->sgraphs[key] = ex;
+    *out = ex;
+    return BMG_OK;
+}
+
 extern "C" {
 
 bmg_status_t bmg_vcycle(bmg_solver_t h, const double *rhs, double *x, int ncycles, void *cuda_stream)
@@ -774,12 +835,47 @@ bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol,
     if (hist_host)
         hist_host[0] = rn;
     int k = 0;
-    while (rn > tol * fn && k < maxiter) {
-        TRY(bmg_vcycle(h, rhs, x, 1, cuda_stream));
-        k++;
-        TRY(bmg_residual_norm(h, rhs, x, nullptr, &rn, cuda_stream));
+    if (h->dist || h->timing) {  // host loop: one synchronised norm per cycle
+        while (rn > tol * fn && k < maxiter) {
+            TRY(bmg_vcycle(h, rhs, x, 1, cuda_stream));
+            k++;
+            TRY(bmg_residual_norm(h, rhs, x, nullptr, &rn, cuda_stream));
+            if (hist_host)
+                hist_host[k] = rn;
+        }
+    } else if (rn > tol * fn && maxiter > 0) {  // device loop: one graph launch, one wait
+        if (h->solve_cap < maxiter + 1) {
+            CK(cudaStreamSynchronize(s));
+            for (auto &kv : h->sgraphs)  // their step nodes point at the old history
+                cudaGraphExecDestroy(kv.second);
+            h->sgraphs.clear();
+            if (h->solve_hist)
+                cudaFree(h->solve_hist);
+            h->solve_hist = nullptr;
+            h->solve_cap = 0;
+            const int cap = maxiter + 1 > 1024 ? maxiter + 1 : 1024;  // rarely reallocated (graphs go with it)
+            void *q;
+            CK(cudaMalloc(&q, sizeof(double) * (size_t)cap + sizeof(SolveState) + 64));
+            h->solve_hist = (double *)q;
+            h->solve_cap = cap;
+            h->solve_st = (SolveState *)(h->solve_hist + h->solve_cap + 1);
+            if (!h->solve_st_h)
+                CK(cudaMallocHost(&h->solve_st_h, sizeof(SolveState)));
+        }
+        cudaGraphExec_t ex;
+        TRY(get_solve_graph(h, rhs, x, &ex));
+        *h->solve_st_h = SolveState{fn, tol, 0, maxiter};
+        CK(cudaMemcpyAsync(h->solve_st, h->solve_st_h, sizeof(SolveState), cudaMemcpyHostToDevice, s));
+        CK(cudaGraphLaunch(ex, s));
+        CK(cudaMemcpyAsync(h->solve_st_h, h->solve_st, sizeof(SolveState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        k = h->solve_st_h->k;
+        std::vector<double> hv(k + 1);
+        CK(cudaMemcpy(hv.data(), h->solve_hist, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost));
+        rn = hv[k];
         if (hist_host)
-            hist_host[k] = rn;
+            for (int i = 1; i <= k; i++)
+                hist_host[i] = hv[i];
     }
     if (iters_out)
         *iters_out = k;

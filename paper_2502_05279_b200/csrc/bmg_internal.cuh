@@ -195,6 +195,16 @@ struct TailPlan {
 };
 void launch_tail(const TailPlan *tp_dev, int ncoarse, const double *f0, double *u0, cudaStream_t s);
 
+// Device-side solve loop (bmg_solve): state read and advanced by k_solve_step,
+// the last node of the body of a conditional WHILE graph node.
+struct SolveState {
+    double fn, tol;   // ||rhs||, relative tolerance
+    int k, maxiter;   // cycles done, cap
+};
+// k = ++st->k; hist[k] = *norm; continue while *norm > tol*fn and k < maxiter
+void launch_solve_step(cudaGraphConditionalHandle hd, const double *norm, SolveState *st, double *hist,
+                       cudaStream_t s);
+
 constexpr int NORM_BLOCKS = 592;  // 4 x 148 SMs; fixed so the reduction tree is fixed
 
 }  // namespace bmg

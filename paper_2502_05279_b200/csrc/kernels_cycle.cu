@@ -319,6 +319,26 @@ void launch_norm(const Op &A, const double *g, double *partials, double *result,
     k_norm_final<<<1, 1024, 0, s>>>(partials, NORM_BLOCKS, result);
 }
 
+// ---------------------------------------------------------------- device-side solve loop
+// The stopping test of the solve loop on the device: the
+// residual norm of the cycle just run goes to hist[k], and the enclosing WHILE
+// node repeats while ||r_k|| > tol ||rhs|| and k < maxiter -- the comparison the
+// host loop makes, on the same double values.
+__global__ void k_solve_step(cudaGraphConditionalHandle hd, const double *__restrict__ norm, SolveState *st,
+                             double *__restrict__ hist)
+{
+    const int k = ++st->k;
+    const double rn = *norm;
+    hist[k] = rn;
+    cudaGraphSetConditional(hd, (rn > st->tol * st->fn && k < st->maxiter) ? 1u : 0u);
+}
+
+void launch_solve_step(cudaGraphConditionalHandle hd, const double *norm, SolveState *st, double *hist,
+                       cudaStream_t s)
+{
+    k_solve_step<<<1, 1, 0, s>>>(hd, norm, st, hist);
+}
+
 // ---------------------------------------------------------------- PCG vectors (c13)
 // q = A p on the owned interior (ring of q untouched).
 __global__ void k_matvec(Op A, const double *__restrict__ p, double *__restrict__ q)
