@@ -25,6 +25,7 @@ from paper_2502_05279_b200 import bmg, dist as D, problems as P  # noqa: E402
 
 N = int(os.environ.get("N", "8191"))
 EXCH_US = float(os.environ.get("EXCH_US", "25"))  # assumed latency of one grouped NCCL exchange
+AGGLOM = os.environ.get("AGGLOM")  # params.agglom_rows (default: the library's)
 
 
 def time_cycles(fn, ncyc=20):
@@ -43,13 +44,17 @@ def time_cycles(fn, ncyc=20):
 st = P.workload("poisson", N, N)
 f_np = P.rhs_const(N, N)
 out = {"n": N, "exch_us_assumed": EXCH_US}
+prm = bmg.bmg_params_default()
+if AGGLOM:
+    prm.agglom_rows = int(AGGLOM)
+out["agglom_rows"] = prm.agglom_rows
 s = bmg.Solver(st)
 f, x = s.grid(f_np), s.grid()
 out["single_ms"] = time_cycles(lambda: s.vcycle(f, x, 1))
 s.close()
 for nr in (2, 4, 8):
-    yb, K = bmg.bmg_partition(N, N, nr)
-    d = D.DistSolver(st, nr, 0, None, loopback=True)
+    yb, K = bmg.bmg_partition(N, N, nr, prm)
+    d = D.DistSolver(st, nr, 0, None, params=prm, loopback=True)
     f, x = d.local(f_np), d.local()
     t_lb = time_cycles(lambda: d.vcycle(f, x, 1))
     d.close()
