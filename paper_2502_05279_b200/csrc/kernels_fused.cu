@@ -32,6 +32,7 @@
 // loading all operands of its points before the arithmetic.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -1445,6 +1446,14 @@ bmg_status_t fused_plan_level(FusedPlan &fp, int l, int nx, int ny, long long pi
     lp.gu.rev = rev;
     lp.down = lp.gd.ok;
     lp.up = lp.gu.ok;
+    if (getenv("BMG_SETUP_TRACE"))  // tuning aid: the plan of this level's legs
+        for (const FusedGeom *g : {&lp.gd, &lp.gu})
+            fprintf(stderr,
+                    "fused plan l=%d %dx%d kind %d %s: ok %d TX %d WD %d D %d threads %d smem %d B, %d strips x %d "
+                    "chunks of %d rows (%d CTAs, %d/SM)\n",
+                    l, nx, ny, kind, g == &lp.gd ? "down" : "up", (int)g->ok, g->TX, g->WD, g->D, g->threads,
+                    (int)g->smem, g->nstrips, g->nchunks, g->chunk, g->nstrips * g->nchunks,
+                    (int)std::min<long long>(g_smem_sm / (g->smem + 1024), 2048 / g->threads));
     return BMG_OK;
 }
 
