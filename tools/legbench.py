@@ -1,6 +1,6 @@
 """Micro-benchmark of the level-0 legs (bmg_smooth_restrict / bmg_correct_smooth)."""
 import os, sys, json, time
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2502_05279_b200 import bmg, problems as P
 

@@ -1,6 +1,6 @@
 """One V(2,1) cycle (NRHS=K: one block cycle) between cudaProfilerStart/Stop (for ncu --profile-from-start off)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2502_05279_b200 import bmg, problems as P
 

@@ -1,7 +1,7 @@
 """Write profiles/traffic.json (per-launch DRAM bytes for bench.py's roofline.traffic)
 and a metrics summary from ncu --set full captures.
 
-usage: python tools_traffic.py NX NY REPORT.ncu-rep [REPORT ...]
+usage: python tools/traffic.py NX NY REPORT.ncu-rep [REPORT ...]
 """
 import csv, io, json, os, re, subprocess, sys
 
@@ -29,9 +29,9 @@ def short(name):
 
 def main():
     nx, ny = int(sys.argv[1]), int(sys.argv[2])
-    root = os.path.dirname(os.path.abspath(__file__))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     path = os.path.join(root, "profiles", "traffic.json")
-    data = {"source": "ncu --set full --clock-control none, one launch per report (tools_traffic.py)",
+    data = {"source": "ncu --set full --clock-control none, one launch per report (tools/traffic.py)",
             "launches": []}
     if os.path.exists(path):
         data = json.load(open(path))

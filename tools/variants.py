@@ -1,10 +1,10 @@
 """Build libbmg.so variants with -D tuning macros (kernels_fused.cu Inst) into variants/.
 
-usage: python tools_variants.py NAME "-DBMG_E5DN=2 -DBMG_D5=3" [NAME FLAGS ...]
+usage: python tools/variants.py NAME "-DBMG_E5DN=2 -DBMG_D5=3" [NAME FLAGS ...]
 """
 import os, subprocess, sys
 from concurrent.futures import ThreadPoolExecutor
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import __graft_entry__ as ge
 
 out = os.path.join(ge.ROOT, "variants")
