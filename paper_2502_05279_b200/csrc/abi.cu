@@ -1045,7 +1045,10 @@ static int enqueue_cycle_block(bmg_solver *h, int K, const double *f0, double *u
     n += 1;
     for (int l = L - 2; l >= 0; l--) {
         const Op A = h->lv[l].op();
-        launch_interp_add_block(K, A, h->civ(l), U(l + 1), U(l), s, h->prm.affine ? h->blk_r[l] : nullptr);
+        // the post-smoother's first colour overwrites its points from their neighbours
+        // alone: those need no correction (exact; DESIGN §5.2 / §5.7)
+        const int skip = (h->prm.nu2 > 0 && !h->prm.affine) ? (h->prm.cycle_sym == 1 ? 2 : 1) : 0;
+        launch_interp_add_block(K, A, h->civ(l), U(l + 1), U(l), s, h->prm.affine ? h->blk_r[l] : nullptr, skip);
         n += 1;
         launch_relax_block(K, A, F(l), U(l), h->prm.nu2, s, &n, h->prm.cycle_sym == 1);
     }

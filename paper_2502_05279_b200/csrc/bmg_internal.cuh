@@ -170,8 +170,10 @@ void launch_restrict_block(int K, const Op &A, const CIv &ci, const double *r, d
 // residual + vanishing restriction fused (after nu1 >= 1 point-GS sweeps; r never stored)
 void launch_resid_restrict_block(int K, const Op &A, const CIv &ci, const double *f, const double *u, double *fc,
                                  double *uc, cudaStream_t s);
+// skip = 1 / 2: leave the points the post-smoother's first colour (forward / reversed
+// order) overwrites uncorrected
 void launch_interp_add_block(int K, const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s,
-                             const double *r = nullptr);
+                             const double *r = nullptr, int skip = 0);
 void launch_coarse_solve_block(int K, const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s);
 void launch_resid_norm_block(int K, const Op &A, const double *f, const double *u, double *partials, double *result,
                              cudaStream_t s);

@@ -383,7 +383,7 @@ __global__ void kb_resid_restrict(Op A, CIv ci, const double *__restrict__ f, co
 // ------------------------------------------------------------------ interpolation + correction (c7, c14)
 template <int K>
 __global__ void kb_interp_add(Op A, CIv ci, const double *__restrict__ e, const double *__restrict__ r,
-                              double *__restrict__ u)
+                              double *__restrict__ u, int skip)
 {
     constexpr int W = Split<K>::W, TP = Split<K>::TP;
     // the parity of i alternates with blockIdx.x, so that a warp (one j) takes one
@@ -393,6 +393,17 @@ __global__ void kb_interp_add(Op A, CIv ci, const double *__restrict__ e, const 
     const int j = blockIdx.y * blockDim.y + threadIdx.y + 1;
     if (i > A.nx || j > A.ny)
         return;
+    // skip = 1 (2: reversed colour order): the points the post-smoother's first
+    // colour pass overwrites from their neighbours alone are not corrected (their
+    // corrected value is never read) -- 5-point: (i + j) even (odd), 9-point: the
+    // C points (the Z points); as the fused up leg does
+    if (skip) {
+        const bool rev = skip == 2;
+        const bool first = A.kind == 5 ? (((i + j) & 1) == (rev ? 1 : 0))
+                                       : (rev ? ((i & 1) && (j & 1)) : (!(i & 1) && !(j & 1)));
+        if (first)
+            return;
+    }
     const long long C = ci.pitch;
     const int I = (i + 1) >> 1, J = (j + 1) >> 1;
     const double *eb = e + sub * W;
@@ -564,10 +575,11 @@ struct Launch {
         const dim3 b(32, 8), g(((A.nx / 2 + 2) * TP + 31) / 32, (A.ny / 2 + 2 + 7) / 8);
         kb_resid_restrict<K><<<g, b, 0, s>>>(A, ci, f, u, fc, uc);
     }
-    static void interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s, const double *r)
+    static void interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s, const double *r,
+                           int skip)
     {
         const dim3 b(32, 8), g(2 * (((A.nx + 1) / 2 * TP + 31) / 32), (A.ny + 7) / 8);
-        kb_interp_add<K><<<g, b, 0, s>>>(A, ci, ec, r, u);
+        kb_interp_add<K><<<g, b, 0, s>>>(A, ci, ec, r, u, skip);
     }
     static void coarse(const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s)
     {
@@ -624,9 +636,9 @@ void launch_resid_restrict_block(int K, const Op &A, const CIv &ci, const double
 }
 
 void launch_interp_add_block(int K, const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s,
-                             const double *r)
+                             const double *r, int skip)
 {
-    BMG_BLOCK_DISPATCH(K, interp_add(A, ci, ec, u, s, r));
+    BMG_BLOCK_DISPATCH(K, interp_add(A, ci, ec, u, s, r, skip));
 }
 
 void launch_coarse_solve_block(int K, const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s)
