@@ -5,7 +5,7 @@
  * V-cycle and its setup, written step by step from the paper
  * (/root/reference/PAPER.md, "P:<line>") and, where the paper delegates to
  * Dendy/Reisner (§2), from the readings fixed in SURVEY.md §8(c)
- * ("c0".."c10"), every one of which is listed in DESIGN.md §3.
+ * ("c0".."c15"), every one of which is listed in DESIGN.md §3.
  *
  * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
  * --impl reference legs may load this library.  It shares no code, header,

@@ -1,5 +1,8 @@
+# Leg micro-benchmarks of libbmg variants built by tools/variants.py (run under gpurun):
+# VARIANTS="base h100" [WLS="poisson:8191 aniso:4095"] bash tools/sweep.sh
 cd $GRAFT_REPO_ROOT
 for v in ${VARIANTS:-h0 h1 h2}; do
-  BMG_LIB=variants/libbmg_$v.so timeout 120 python tools/legbench.py
-  BMG_LIB=variants/libbmg_$v.so WL=aniso N=4095 timeout 120 python tools/legbench.py
+  for w in ${WLS:-poisson:8191 aniso:4095}; do
+    BMG_LIB=variants/libbmg_$v.so WL=${w%%:*} N=${w##*:} timeout 120 python tools/legbench.py
+  done
 done
