@@ -63,6 +63,15 @@ def test_host_only_calls_without_gpu(libbmg):
     assert libbmg.bmg_setup(ctypes.byref(st), None, None, ctypes.byref(h)) == bmg.BMG_EINVAL
     assert b"kind" in libbmg.bmg_last_error_detail()
     assert libbmg.bmg_destroy(None) == bmg.BMG_OK
+    # the newer entry points reject a null handle / bad sizes before any device work
+    d = ctypes.c_double()
+    it = ctypes.c_int()
+    assert libbmg.bmg_pcg(None, None, None, 1e-8, 10, ctypes.byref(it), None, None) == bmg.BMG_EINVAL
+    for K in (1, 0, bmg.BMG_MAX_NRHS + 1):
+        assert libbmg.bmg_vcycle_block(None, K, None, None, 1, None) == bmg.BMG_EINVAL
+        assert libbmg.bmg_residual_norm_block(None, K, None, None, ctypes.byref(d), None) == bmg.BMG_EINVAL
+        assert libbmg.bmg_solve_block(None, K, None, None, 1e-8, 10, ctypes.byref(it), None, None) == bmg.BMG_EINVAL
+    assert b"nrhs" in libbmg.bmg_last_error_detail()
 
 
 def test_product_package_does_not_import_oracle():
