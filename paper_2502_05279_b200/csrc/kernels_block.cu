@@ -380,6 +380,88 @@ __global__ void kb_resid_restrict(Op A, CIv ci, const double *__restrict__ f, co
     stk<W>(qc + sub * W + c * K, v);
 }
 
+// 5-point levels: the same residual + vanishing restriction, tiled so that every
+// residual is evaluated once.  A CTA covers RT_CX x RT_CY coarse points; phase 1
+// evaluates r at the fine points their restrictions keep -- the centres
+// (2I, 2J) and the corners (odd, odd), a ring of corners included -- into
+// shared memory; phase 2 forms each coarse value from there in
+// restrict_pt_vanish's order.  (The untiled kernel evaluates each corner for
+// all four coarse points that use it.)
+constexpr int RT_CX = 16, RT_CY = 8;
+template <int K>
+__global__ void __launch_bounds__(256) kb_resid_restrict5_tiled(Op A, CIv ci, const double *__restrict__ f,
+                                                                const double *__restrict__ u, double *__restrict__ qc,
+                                                                double *__restrict__ uc)
+{
+    constexpr int W = Split<K>::W, TP = Split<K>::TP;
+    constexpr int FX = 2 * RT_CX + 1, FY = 2 * RT_CY + 1;  // fine region 2*I0-1 .. 2*(I0+CX-1)+1
+    __shared__ __align__(16) double sr[FY * FX * K];
+    const int I0 = 1 + blockIdx.x * RT_CX, J0 = 1 + blockIdx.y * RT_CY;
+    const int ncx = A.nx / 2, ncy = A.ny / 2;
+    const int x0 = 2 * I0 - 1, y0 = 2 * J0 - 1;
+    // phase 1: residual at the kept points of the region ((x + y) even: centres and corners)
+    constexpr int HALF = (FX + 1) / 2;  // kept points per fine row (rows alternate odd/even)
+    for (int it = threadIdx.x; it < FY * HALF * TP; it += blockDim.x) {
+        const int sub = it % TP, q = it / TP, ry = q / HALF, k = q % HALF;
+        const int y = y0 + ry;
+        const int x = x0 + ((ry & 1) ? 1 : 0) + 2 * k;  // row y0 (odd) starts at x0 (odd)
+        if (x - x0 >= FX)
+            continue;
+        double r[W];
+        if (x > A.nx || y > A.ny)  // the Dirichlet ring (and beyond): r = 0, as k_residual stores
+#pragma unroll
+            for (int k2 = 0; k2 < W; k2++)
+                r[k2] = 0.0;
+        else
+            resid_w<W, K>(A, f + sub * W, u + sub * W, x, y, r);
+        stk<W>(sr + ((ry * FX) + (x - x0)) * K + sub * W, r);
+    }
+    __syncthreads();
+    // phase 2: one coarse point per item (ring points of the coarse grid: 0)
+    for (int it = threadIdx.x; it < RT_CX * RT_CY * TP; it += blockDim.x) {
+        const int sub = it % TP, q = it / TP, I = I0 + q % RT_CX, J = J0 + q / RT_CX;
+        if (I > ncx + 1 || J > ncy + 1)
+            continue;
+        const long long C = ci.pitch, c = J * C + I;
+        if (uc)
+            setk<W>(uc + sub * W + c * K, 0.0);
+        if (I > ncx || J > ncy) {
+            setk<W>(qc + sub * W + c * K, 0.0);
+            continue;
+        }
+        const int lx = 2 * I - x0, ly = 2 * J - y0;  // local fine coordinates of the centre
+        auto at = [&](int dx, int dy) { return sr + (((ly + dy) * FX) + (lx + dx)) * K + sub * W; };
+        double v[W], r[W];
+        ldk<W>(at(-1, -1), r);
+        racc<W>(v, ci.w[CI_LNE][c], r, true);
+        ldk<W>(at(1, -1), r);
+        racc<W>(v, ci.w[CI_LNW][c + 1], r, false);
+        ldk<W>(at(0, 0), r);
+#pragma unroll
+        for (int k2 = 0; k2 < W; k2++)
+            v[k2] = __dadd_rn(v[k2], r[k2]);
+        ldk<W>(at(-1, 1), r);
+        racc<W>(v, ci.w[CI_LSE][c + C], r, false);
+        ldk<W>(at(1, 1), r);
+        racc<W>(v, ci.w[CI_LSW][c + C + 1], r, false);
+        stk<W>(qc + sub * W + c * K, v);
+    }
+}
+
+// the coarse ring row/column 0 (the tiled kernel's tiles start at I, J = 1)
+template <int K>
+__global__ void kb_coarse_ring0(int ncx, int ncy, long long C, double *__restrict__ qc, double *__restrict__ uc)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n0 = ncx + 2, n1 = ncy + 2;
+    if (t >= n0 + n1)
+        return;
+    const long long c = t < n0 ? (long long)t : (long long)(t - n0) * C;  // row 0, then column 0
+    setk<K>(qc + c * K, 0.0);
+    if (uc)
+        setk<K>(uc + c * K, 0.0);
+}
+
 // ------------------------------------------------------------------ interpolation + correction (c7, c14)
 template <int K>
 __global__ void kb_interp_add(Op A, CIv ci, const double *__restrict__ e, const double *__restrict__ r,
@@ -572,6 +654,13 @@ struct Launch {
     static void resid_restrict(const Op &A, const CIv &ci, const double *f, const double *u, double *fc, double *uc,
                                cudaStream_t s)
     {
+        if (A.kind == 5) {  // tiled: every residual evaluated once
+            const int ncx = A.nx / 2, ncy = A.ny / 2;
+            const dim3 g((ncx + 1 + RT_CX - 1) / RT_CX, (ncy + 1 + RT_CY - 1) / RT_CY);
+            kb_resid_restrict5_tiled<K><<<g, 256, 0, s>>>(A, ci, f, u, fc, uc);
+            kb_coarse_ring0<K><<<(ncx + ncy + 4 + 255) / 256, 256, 0, s>>>(ncx, ncy, ci.pitch, fc, uc);
+            return;
+        }
         const dim3 b(32, 8), g(((A.nx / 2 + 2) * TP + 31) / 32, (A.ny / 2 + 2 + 7) / 8);
         kb_resid_restrict<K><<<g, b, 0, s>>>(A, ci, f, u, fc, uc);
     }
