@@ -277,11 +277,11 @@ __global__ void kb_restrict(Op A, CIv ci, const double *__restrict__ q, double *
 }
 
 // Residual and vanishing restriction in one pass (after nu1 >= 1 point-GS sweeps,
-// DESIGN §5.2): each coarse point evaluates r = f - A u at exactly the fine points
-// its restriction keeps -- 5-point: the centre and the 4 Z corners; 9-point: the
-// centre and the 4 X/Y edge points -- so r is never stored.  Per column the
-// residual is the per-step one (f - fma(a_O, u, offdiag)) and the sum is
-// restrict_pt_vanish's, in source order.
+// DESIGN §5.2): r = f - A u is evaluated only at the fine points the restriction
+// keeps -- 5-point: the centres and the Z corners; 9-point: the centres and the
+// X/Y edge points -- and never stored in HBM.  Per column the residual is the
+// per-step one (f - fma(a_O, u, offdiag)) and the sum is restrict_pt_vanish's,
+// in source order.
 template <int W, int K>
 __device__ __forceinline__ void resid_w(const Op &A, const double *__restrict__ f, const double *__restrict__ u,
                                         int i, int j, double (&r)[W])
@@ -331,67 +331,17 @@ __device__ __forceinline__ void racc(double (&v)[W], double w, const double (&r)
         v[c] = first ? __dmul_rn(w, r[c]) : __fma_rn(w, r[c], v[c]);
 }
 
-template <int K>
-__global__ void kb_resid_restrict(Op A, CIv ci, const double *__restrict__ f, const double *__restrict__ u,
-                                  double *__restrict__ qc, double *__restrict__ uc)
-{
-    constexpr int W = Split<K>::W, TP = Split<K>::TP;
-    const int gx = blockIdx.x * blockDim.x + threadIdx.x, sub = gx % TP, I = gx / TP;
-    const int J = blockIdx.y * blockDim.y + threadIdx.y;
-    if (I > A.nx / 2 + 1 || J > A.ny / 2 + 1)
-        return;
-    const long long C = ci.pitch, c = J * C + I;
-    if (uc)
-        setk<W>(uc + sub * W + c * K, 0.0);
-    if (I == 0 || J == 0 || I > A.nx / 2 || J > A.ny / 2) {
-        setk<W>(qc + sub * W + c * K, 0.0);
-        return;
-    }
-    const double *fb = f + sub * W, *ub = u + sub * W;
-    const int i = 2 * I, j = 2 * J;
-    double v[W], r[W];
-    if (A.kind == 5) {  // centre + Z terms
-        resid_w<W, K>(A, fb, ub, i - 1, j - 1, r);
-        racc<W>(v, ci.w[CI_LNE][c], r, true);
-        resid_w<W, K>(A, fb, ub, i + 1, j - 1, r);
-        racc<W>(v, ci.w[CI_LNW][c + 1], r, false);
-        resid_w<W, K>(A, fb, ub, i, j, r);
-#pragma unroll
-        for (int k = 0; k < W; k++)
-            v[k] = __dadd_rn(v[k], r[k]);
-        resid_w<W, K>(A, fb, ub, i - 1, j + 1, r);
-        racc<W>(v, ci.w[CI_LSE][c + C], r, false);
-        resid_w<W, K>(A, fb, ub, i + 1, j + 1, r);
-        racc<W>(v, ci.w[CI_LSW][c + C + 1], r, false);
-    } else {  // centre + X/Y terms
-        resid_w<W, K>(A, fb, ub, i, j - 1, r);
-        racc<W>(v, ci.w[CI_LA][c], r, true);
-        resid_w<W, K>(A, fb, ub, i - 1, j, r);
-        racc<W>(v, ci.w[CI_LR][c], r, false);
-        resid_w<W, K>(A, fb, ub, i, j, r);
-#pragma unroll
-        for (int k = 0; k < W; k++)
-            v[k] = __dadd_rn(v[k], r[k]);
-        resid_w<W, K>(A, fb, ub, i + 1, j, r);
-        racc<W>(v, ci.w[CI_LL][c + 1], r, false);
-        resid_w<W, K>(A, fb, ub, i, j + 1, r);
-        racc<W>(v, ci.w[CI_LB][c + C], r, false);
-    }
-    stk<W>(qc + sub * W + c * K, v);
-}
-
-// 5-point levels: the same residual + vanishing restriction, tiled so that every
-// residual is evaluated once.  A CTA covers RT_CX x RT_CY coarse points; phase 1
+// Tiled so that every residual is evaluated once.  A CTA covers RT_CX x RT_CY coarse points; phase 1
 // evaluates r at the fine points their restrictions keep -- the centres
 // (2I, 2J) and the corners (odd, odd), a ring of corners included -- into
 // shared memory; phase 2 forms each coarse value from there in
 // restrict_pt_vanish's order.  (The untiled kernel evaluates each corner for
 // all four coarse points that use it.)
 constexpr int RT_CX = 16, RT_CY = 8;
-template <int K>
-__global__ void __launch_bounds__(256) kb_resid_restrict5_tiled(Op A, CIv ci, const double *__restrict__ f,
-                                                                const double *__restrict__ u, double *__restrict__ qc,
-                                                                double *__restrict__ uc)
+template <int K, int KIND>
+__global__ void __launch_bounds__(256) kb_resid_restrict_tiled(Op A, CIv ci, const double *__restrict__ f,
+                                                               const double *__restrict__ u, double *__restrict__ qc,
+                                                               double *__restrict__ uc)
 {
     constexpr int W = Split<K>::W, TP = Split<K>::TP;
     constexpr int FX = 2 * RT_CX + 1, FY = 2 * RT_CY + 1;  // fine region 2*I0-1 .. 2*(I0+CX-1)+1
@@ -399,13 +349,15 @@ __global__ void __launch_bounds__(256) kb_resid_restrict5_tiled(Op A, CIv ci, co
     const int I0 = 1 + blockIdx.x * RT_CX, J0 = 1 + blockIdx.y * RT_CY;
     const int ncx = A.nx / 2, ncy = A.ny / 2;
     const int x0 = 2 * I0 - 1, y0 = 2 * J0 - 1;
-    // phase 1: residual at the kept points of the region ((x + y) even: centres and corners)
-    constexpr int HALF = (FX + 1) / 2;  // kept points per fine row (rows alternate odd/even)
-    for (int it = threadIdx.x; it < FY * HALF * TP; it += blockDim.x) {
-        const int sub = it % TP, q = it / TP, ry = q / HALF, k = q % HALF;
+    // phase 1: residual at the kept points of the region -- 5-point: (x + y) even
+    // (centres and corners); 9-point: all but (odd, odd) (centres and edges)
+    constexpr int HALF = (FX + 1) / 2;  // 5-point: kept points per fine row (rows alternate odd/even)
+    constexpr int PER_ROW = KIND == 5 ? HALF : FX;
+    for (int it = threadIdx.x; it < FY * PER_ROW * TP; it += blockDim.x) {
+        const int sub = it % TP, q = it / TP, ry = q / PER_ROW, k = q % PER_ROW;
         const int y = y0 + ry;
-        const int x = x0 + ((ry & 1) ? 1 : 0) + 2 * k;  // row y0 (odd) starts at x0 (odd)
-        if (x - x0 >= FX)
+        const int x = KIND == 5 ? x0 + ((ry & 1) ? 1 : 0) + 2 * k : x0 + k;  // x0, y0 odd
+        if (x - x0 >= FX || (KIND == 9 && (x & 1) && (y & 1)))
             continue;
         double r[W];
         if (x > A.nx || y > A.ny)  // the Dirichlet ring (and beyond): r = 0, as k_residual stores
@@ -432,18 +384,33 @@ __global__ void __launch_bounds__(256) kb_resid_restrict5_tiled(Op A, CIv ci, co
         const int lx = 2 * I - x0, ly = 2 * J - y0;  // local fine coordinates of the centre
         auto at = [&](int dx, int dy) { return sr + (((ly + dy) * FX) + (lx + dx)) * K + sub * W; };
         double v[W], r[W];
-        ldk<W>(at(-1, -1), r);
-        racc<W>(v, ci.w[CI_LNE][c], r, true);
-        ldk<W>(at(1, -1), r);
-        racc<W>(v, ci.w[CI_LNW][c + 1], r, false);
-        ldk<W>(at(0, 0), r);
+        if (KIND == 5) {  // centre + Z terms
+            ldk<W>(at(-1, -1), r);
+            racc<W>(v, ci.w[CI_LNE][c], r, true);
+            ldk<W>(at(1, -1), r);
+            racc<W>(v, ci.w[CI_LNW][c + 1], r, false);
+            ldk<W>(at(0, 0), r);
 #pragma unroll
-        for (int k2 = 0; k2 < W; k2++)
-            v[k2] = __dadd_rn(v[k2], r[k2]);
-        ldk<W>(at(-1, 1), r);
-        racc<W>(v, ci.w[CI_LSE][c + C], r, false);
-        ldk<W>(at(1, 1), r);
-        racc<W>(v, ci.w[CI_LSW][c + C + 1], r, false);
+            for (int k2 = 0; k2 < W; k2++)
+                v[k2] = __dadd_rn(v[k2], r[k2]);
+            ldk<W>(at(-1, 1), r);
+            racc<W>(v, ci.w[CI_LSE][c + C], r, false);
+            ldk<W>(at(1, 1), r);
+            racc<W>(v, ci.w[CI_LSW][c + C + 1], r, false);
+        } else {  // centre + X/Y terms
+            ldk<W>(at(0, -1), r);
+            racc<W>(v, ci.w[CI_LA][c], r, true);
+            ldk<W>(at(-1, 0), r);
+            racc<W>(v, ci.w[CI_LR][c], r, false);
+            ldk<W>(at(0, 0), r);
+#pragma unroll
+            for (int k2 = 0; k2 < W; k2++)
+                v[k2] = __dadd_rn(v[k2], r[k2]);
+            ldk<W>(at(1, 0), r);
+            racc<W>(v, ci.w[CI_LL][c + 1], r, false);
+            ldk<W>(at(0, 1), r);
+            racc<W>(v, ci.w[CI_LB][c + C], r, false);
+        }
         stk<W>(qc + sub * W + c * K, v);
     }
 }
@@ -654,15 +621,14 @@ struct Launch {
     static void resid_restrict(const Op &A, const CIv &ci, const double *f, const double *u, double *fc, double *uc,
                                cudaStream_t s)
     {
-        if (A.kind == 5) {  // tiled: every residual evaluated once
-            const int ncx = A.nx / 2, ncy = A.ny / 2;
-            const dim3 g((ncx + 1 + RT_CX - 1) / RT_CX, (ncy + 1 + RT_CY - 1) / RT_CY);
-            kb_resid_restrict5_tiled<K><<<g, 256, 0, s>>>(A, ci, f, u, fc, uc);
-            kb_coarse_ring0<K><<<(ncx + ncy + 4 + 255) / 256, 256, 0, s>>>(ncx, ncy, ci.pitch, fc, uc);
-            return;
-        }
-        const dim3 b(32, 8), g(((A.nx / 2 + 2) * TP + 31) / 32, (A.ny / 2 + 2 + 7) / 8);
-        kb_resid_restrict<K><<<g, b, 0, s>>>(A, ci, f, u, fc, uc);
+        // tiled: every residual evaluated once
+        const int ncx = A.nx / 2, ncy = A.ny / 2;
+        const dim3 g((ncx + 1 + RT_CX - 1) / RT_CX, (ncy + 1 + RT_CY - 1) / RT_CY);
+        if (A.kind == 5)
+            kb_resid_restrict_tiled<K, 5><<<g, 256, 0, s>>>(A, ci, f, u, fc, uc);
+        else
+            kb_resid_restrict_tiled<K, 9><<<g, 256, 0, s>>>(A, ci, f, u, fc, uc);
+        kb_coarse_ring0<K><<<(ncx + ncy + 4 + 255) / 256, 256, 0, s>>>(ncx, ncy, ci.pitch, fc, uc);
     }
     static void interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s, const double *r,
                            int skip)
