@@ -435,21 +435,30 @@ __global__ void kb_interp_add(Op A, CIv ci, const double *__restrict__ e, const 
                               double *__restrict__ u, int skip)
 {
     constexpr int W = Split<K>::W, TP = Split<K>::TP;
-    // the parity of i alternates with blockIdx.x, so that a warp (one j) takes one
-    // branch below while the two parities of a strip run side by side (u read once)
-    const int gx = (blockIdx.x >> 1) * blockDim.x + threadIdx.x, sub = gx % TP;
-    const int i = 2 * (gx / TP) + 1 + (blockIdx.x & 1);
     const int j = blockIdx.y * blockDim.y + threadIdx.y + 1;
+    int gx, i;
+    if (skip && A.kind == 5) {
+        // only the colour the post-smoother relaxes second is corrected: threads map
+        // onto its points alone ((i + j) odd, reversed order (i + j) even)
+        gx = blockIdx.x * blockDim.x + threadIdx.x;
+        const int want = skip == 2 ? 0 : 1;
+        i = ((((1 + j) & 1) == want) ? 1 : 2) + 2 * (gx / TP);
+    } else {
+        // the parity of i alternates with blockIdx.x, so that a warp (one j) takes one
+        // branch below while the two parities of a strip run side by side (u read once)
+        gx = (blockIdx.x >> 1) * blockDim.x + threadIdx.x;
+        i = 2 * (gx / TP) + 1 + (blockIdx.x & 1);
+    }
+    const int sub = gx % TP;
     if (i > A.nx || j > A.ny)
         return;
     // skip = 1 (2: reversed colour order): the points the post-smoother's first
     // colour pass overwrites from their neighbours alone are not corrected (their
-    // corrected value is never read) -- 5-point: (i + j) even (odd), 9-point: the
-    // C points (the Z points); as the fused up leg does
-    if (skip) {
-        const bool rev = skip == 2;
-        const bool first = A.kind == 5 ? (((i + j) & 1) == (rev ? 1 : 0))
-                                       : (rev ? ((i & 1) && (j & 1)) : (!(i & 1) && !(j & 1)));
+    // corrected value is never read) -- 5-point: (i + j) even (odd), handled by the
+    // thread mapping above; 9-point: the C points (the Z points); as the fused up
+    // leg does
+    if (skip && A.kind == 9) {  // 9-point: the C points (reversed order: the Z points)
+        const bool first = skip == 2 ? ((i & 1) && (j & 1)) : (!(i & 1) && !(j & 1));
         if (first)
             return;
     }
@@ -633,7 +642,8 @@ struct Launch {
     static void interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s, const double *r,
                            int skip)
     {
-        const dim3 b(32, 8), g(2 * (((A.nx + 1) / 2 * TP + 31) / 32), (A.ny + 7) / 8);
+        const int gxn = ((A.nx + 1) / 2 * TP + 31) / 32;  // CTAs per row for one parity of i
+        const dim3 b(32, 8), g(skip && A.kind == 5 ? gxn : 2 * gxn, (A.ny + 7) / 8);
         kb_interp_add<K><<<g, b, 0, s>>>(A, ci, ec, r, u, skip);
     }
     static void coarse(const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s)
