@@ -338,6 +338,14 @@ __device__ __forceinline__ void racc(double (&v)[W], double w, const double (&r)
 // restrict_pt_vanish's order.  (The untiled kernel evaluates each corner for
 // all four coarse points that use it.)
 constexpr int RT_CX = 16, RT_CY = 8;
+
+// CTA shape of the per-colour GS kernels (tuning knob)
+#ifndef BMG_KB_BX
+#define BMG_KB_BX 128
+#endif
+#ifndef BMG_KB_BY
+#define BMG_KB_BY 2
+#endif
 template <int K, int KIND>
 __global__ void __launch_bounds__(256) kb_resid_restrict_tiled(Op A, CIv ci, const double *__restrict__ f,
                                                                const double *__restrict__ u, double *__restrict__ qc,
@@ -599,16 +607,16 @@ struct Launch {
     static constexpr int TP = Split<K>::TP;
     static void relax(const Op &A, const double *f, double *u, int nsweeps, cudaStream_t s, int *nlaunch, bool rev)
     {
-        const dim3 b(32, 8);
+        const dim3 b(BMG_KB_BX, BMG_KB_BY);
         for (int sw = 0; sw < nsweeps; sw++) {
             if (A.kind == 5) {
-                const dim3 g(((A.nx / 2 + 1) * TP + 31) / 32, (A.ny + 7) / 8);
+                const dim3 g(((A.nx / 2 + 1) * TP + b.x - 1) / b.x, (A.ny + b.y - 1) / b.y);
                 for (int c = 0; c < 2; c++)
                     kb_relax5<K><<<g, b, 0, s>>>(A, f, u, rev ? 1 - c : c);
                 if (nlaunch)
                     *nlaunch += 2;
             } else {
-                const dim3 g(((A.nx / 2 + 1) * TP + 31) / 32, (A.ny / 2 + 1 + 7) / 8);
+                const dim3 g(((A.nx / 2 + 1) * TP + b.x - 1) / b.x, (A.ny / 2 + 1 + b.y - 1) / b.y);
                 for (int c = 0; c < 4; c++)
                     kb_relax9<K><<<g, b, 0, s>>>(A, f, u, rev ? 3 - c : c);
                 if (nlaunch)
