@@ -399,10 +399,29 @@ def main():
         t0 = time.perf_counter()
         itb, hb, rcb = solver.solve_block(fb, xb, args.solve_tol or SOLVE_TOL.get(args.config, 1e-10), SOLVE_MAXIT)
         dtb = time.perf_counter() - t0
+        if args.pcg > 0:  # block PCG with the symmetric block V(NU,NU) cycle
+            prm3 = bmg.bmg_params_default()
+            prm3.nu1 = prm3.nu2 = args.pcg
+            prm3.cycle_sym = 1
+            s3 = bmg.Solver(P.workload(wl, nx, ny), prm3)
+            fb3, xb3 = s3.block_grid(K), s3.block_grid(K)
+            fb3.copy_(fb)
+            s3.pcg_block(fb3, xb3, 1e-3, 2)  # warm-up: workspaces + block graph
+            xb3.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            itp, hp, rcp = s3.pcg_block(fb3, xb3, args.solve_tol or SOLVE_TOL.get(args.config, 1e-10), SOLVE_MAXIT)
+            pcg_block = {"preconditioner": f"block V({args.pcg},{args.pcg}) symmetric", "steps": itp,
+                         "converged": rcp == 0, "ms": (time.perf_counter() - t0) * 1e3}
+            s3.close()
+            del fb3, xb3
+        else:
+            pcg_block = None
         block = {"nrhs": K, "ms_per_block_cycle": bms, "ms_per_rhs_cycle": bms / K,
                  "rhs_cycles_per_s": K * 1e3 / bms, "vs_single_rhs_cycle": ms_per_step / (bms / K),
                  "solve": {"steps": itb, "converged": rcb == 0, "ms": dtb * 1e3,
                            "final_rel_residual": float(hb[-1].max() / fnorm) if len(hb) else None},
+                 "pcg": pcg_block,
                  "note": ("K columns interleaved per point; per-step block kernels (one read of the stencil and "
                           "weights per block), CUDA-graph replay, device-timed; vs_single_rhs_cycle = the "
                           "single-RHS cycle time of this line / the block cycle time per right-hand side")}

@@ -200,6 +200,21 @@ bmg_status_t bmg_residual_norm_block(bmg_solver_t h, int nrhs, const double *rhs
 bmg_status_t bmg_solve_block(bmg_solver_t h, int nrhs, const double *rhs, double *x, double tol, int maxiter,
                              int *iters_out, double *hist_host, void *cuda_stream);
 
+/*
+ * Block PCG (c13 on each column of a c15 block): column c runs the recurrences
+ * of bmg_pcg on (rhs_c, x_c) -- its own alpha_c and beta_c, the preconditioner
+ * one block V(nu,nu) cycle from zero (needs nu1 == nu2 and cycle_sym = 1,
+ * EINVAL otherwise) -- and is frozen once ||r_c|| <= tol*||rhs_c|| (so x_c is
+ * what bmg_pcg would return for it, up to rounding).  A column with
+ * ||rhs_c|| = 0 is set to 0.  hist_host: (maxiter+1) * nrhs doubles, row k =
+ * the K recursive residual norms after k steps (a frozen column repeats its
+ * last); iters_out: steps taken (the slowest column's count).  Layout, limits
+ * and workspace as bmg_vcycle_block (plus four block arrays for r, z, p, q).
+ * Synchronises cuda_stream once per step.  Returns ENOTCONV at maxiter.
+ */
+bmg_status_t bmg_pcg_block(bmg_solver_t h, int nrhs, const double *rhs, double *x, double tol, int maxiter,
+                           int *iters_out, double *hist_host, void *cuda_stream);
+
 /* ||rhs - A x||_2 over the fine interior ("l2 norm"), deterministic
  * fixed-tree reduction; optional r_out (device, setup pitch, ring untouched)
  * receives the residual.  *norm_host is a host double.  Synchronises. */

@@ -307,3 +307,10 @@ class Hierarchy:
         it = ctypes.c_int()
         rc = lib().orc_solve_block(self._h, K, _p(F), _p(U), tol, maxiter, ctypes.byref(it), _p(hist))
         return U, it.value, hist[: it.value + 1], rc
+
+    def pcg_block(self, F, U, tol, maxiter):
+        """c13 on each column of a c15 block (bmg_pcg_block's reading): the columns
+        are independent PCG runs (orc_pcg), each stopping at its own test.
+        Returns (U, per-column iterations, per-column histories, per-column status)."""
+        outs = [self.pcg(F[c], U[c], tol, maxiter) for c in range(len(F))]
+        return (np.stack([o[0] for o in outs]), [o[1] for o in outs], [o[2] for o in outs], [o[3] for o in outs])

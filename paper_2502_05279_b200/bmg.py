@@ -26,7 +26,7 @@ EXPORTS = (
     "bmg_restrict", "bmg_interp_add", "bmg_smooth_restrict", "bmg_correct_smooth", "bmg_cycle_kernel_count", "bmg_timing",
     "bmg_timing_read", "bmg_destroy", "bmg_strerror",
     "bmg_last_error_detail", "bmg_partition", "bmg_setup_dist", "bmg_local_rows", "bmg_vcycle_block",
-    "bmg_residual_norm_block", "bmg_solve_block",
+    "bmg_residual_norm_block", "bmg_solve_block", "bmg_pcg_block",
 )
 
 BMG_MAX_NRHS = 8
@@ -83,6 +83,7 @@ def lib():
             "bmg_vcycle_block": (i, [vp, i, vp, vp, i, vp]),
             "bmg_residual_norm_block": (i, [vp, i, vp, vp, dp, vp]),
             "bmg_solve_block": (i, [vp, i, vp, vp, d, i, ip, dp, vp]),
+            "bmg_pcg_block": (i, [vp, i, vp, vp, d, i, ip, dp, vp]),
             "bmg_residual_norm": (i, [vp, vp, vp, vp, dp, vp]),
             "bmg_num_levels": (i, [vp, ip]),
             "bmg_level_shape": (i, [vp, i, ip, ip, ip]),
@@ -199,6 +200,16 @@ def bmg_solve_block(h, nrhs: int, rhs, x, tol: float, maxiter: int, stream=None)
     rc = lib().bmg_solve_block(h, nrhs, _ptr(rhs), _ptr(x), tol, maxiter, ctypes.byref(it),
                                hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream(stream))
     _check(rc, "bmg_solve_block", ok=(BMG_OK, BMG_ENOTCONV))
+    return it.value, hist[: it.value + 1], rc
+
+
+def bmg_pcg_block(h, nrhs: int, rhs, x, tol: float, maxiter: int, stream=None):
+    """Block PCG.  Returns (steps, hist (steps+1, nrhs) recursive residual norms, status)."""
+    it = ctypes.c_int()
+    hist = np.zeros((maxiter + 1, nrhs))
+    rc = lib().bmg_pcg_block(h, nrhs, _ptr(rhs), _ptr(x), tol, maxiter, ctypes.byref(it),
+                             hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream(stream))
+    _check(rc, "bmg_pcg_block", ok=(BMG_OK, BMG_ENOTCONV))
     return it.value, hist[: it.value + 1], rc
 
 
@@ -399,6 +410,9 @@ class Solver:
 
     def solve_block(self, rhs, x, tol, maxiter):
         return bmg_solve_block(self.h, rhs.shape[-1], rhs, x, tol, maxiter)
+
+    def pcg_block(self, rhs, x, tol, maxiter):
+        return bmg_pcg_block(self.h, rhs.shape[-1], rhs, x, tol, maxiter)
 
     def solve(self, rhs, x, tol, maxiter):
         return bmg_solve(self.h, rhs, x, tol, maxiter)

@@ -125,6 +125,8 @@ struct bmg_solver {
     std::vector<double *> blk_f, blk_u, blk_r;
     double *blk_partials = nullptr, *blk_norm = nullptr;
     std::map<std::pair<const void *, const void *>, cudaGraphExec_t> bgraphs;  // block cycle graphs (blk_K)
+    double *pcgb_ws = nullptr;  // block PCG: r, z, p, q (K-interleaved level-0 arrays) + scalar slots
+    int pcgb_K = 0;
 
     CIv civ(int l) const
     {
@@ -220,6 +222,8 @@ bmg_status_t bmg_destroy(bmg_solver_t h)
         cudaGraphExecDestroy(kv.second);
     if (h->blk_arena)
         cudaFree(h->blk_arena);
+    if (h->pcgb_ws)
+        cudaFree(h->pcgb_ws);
     if (h->h_norm)
         cudaFreeHost(h->h_norm);
     if (h->cap)
@@ -1165,6 +1169,103 @@ bmg_status_t bmg_solve_block(bmg_solver_t h, int nrhs, const double *rhs, double
     if (iters_out)
         *iters_out = k;
     return done() ? BMG_OK : fail(BMG_ENOTCONV, "maxiter reached");
+}
+
+/*
+ * Block PCG (c13 on every column of a c15 block): column c runs exactly the
+ * recurrences of bmg_pcg on (rhs_c, x_c) -- alpha_c, beta_c from its own dot
+ * products (device slots), the preconditioner the block V(nu,nu) cycle from
+ * zero -- and stops updating once ||r_c|| <= tol ||rhs_c|| (its x_c and r_c are
+ * then frozen: the column's result is its single-column PCG's).  The host
+ * waits once per step for the K norms.
+ */
+bmg_status_t bmg_pcg_block(bmg_solver_t h, int nrhs, const double *rhs, double *x, double tol, int maxiter,
+                           int *iters_out, double *hist_host, void *cuda_stream)
+{
+    TRY(block_args(h, nrhs, rhs, x, "bmg_pcg_block"));
+    if (maxiter < 0 || !(tol >= 0))
+        return fail(BMG_EINVAL, "bad arguments to bmg_pcg_block");
+    if (h->prm.nu1 != h->prm.nu2 || h->prm.cycle_sym != 1)
+        return fail(BMG_EINVAL, "bmg_pcg_block: the preconditioner must be symmetric (nu1 == nu2, cycle_sym = 1)");
+    const int K = nrhs;
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    TRY(block_workspace(h, K, s));
+    if (iters_out)
+        *iters_out = 0;
+    const Level &v = h->lv[0];
+    const Op A = v.op();
+    const size_t np = (size_t)(v.ny + 2) * (size_t)v.pitch * (size_t)K;
+    if (h->pcgb_K != K) {
+        CK(cudaStreamSynchronize(s));
+        if (h->pcgb_ws)
+            cudaFree(h->pcgb_ws);
+        h->pcgb_ws = nullptr;
+        h->pcgb_K = 0;
+        void *q;
+        CK(cudaMalloc(&q, sizeof(double) * (4 * np + 8 * BMG_MAX_NRHS)));
+        h->pcgb_ws = (double *)q;
+        CK(cudaMemsetAsync(q, 0, sizeof(double) * (4 * np + 8 * BMG_MAX_NRHS), s));
+        h->pcgb_K = K;
+    }
+    double *r = h->pcgb_ws, *z = r + np, *p = z + np, *q = p + np, *sc = q + np;
+    // scalar slots (K each): rho in slot 0 / 1 alternately, p.q in slot 2
+    const int PQ = 2 * K;
+    auto host_norms = [&](const double *src, double *out) -> bmg_status_t {
+        CK(cudaMemcpyAsync(h->h_norm, src, K * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        memcpy(out, h->h_norm, K * sizeof(double));
+        return BMG_OK;
+    };
+    double fn[BMG_MAX_NRHS], rn[BMG_MAX_NRHS];
+    launch_norm_block(K, A, rhs, h->blk_partials, h->blk_norm, s);
+    TRY(host_norms(h->blk_norm, fn));
+    for (int c = 0; c < K; c++)
+        if (fn[c] == 0.0)  // SPEC S:444 per column
+            launch_zero_col_block(K, A, x, c, s);
+    launch_residual_block(K, A, rhs, x, r, s);  // r = f - A x0 (ring 0)
+    launch_norm_block(K, A, r, h->blk_partials, h->blk_norm, s);
+    TRY(host_norms(h->blk_norm, rn));
+    if (hist_host)
+        memcpy(hist_host, rn, K * sizeof(double));
+    unsigned mask = 0;
+    for (int c = 0; c < K; c++)
+        if (rn[c] > tol * fn[c])
+            mask |= 1u << c;
+    int k = 0;
+    if (mask && maxiter > 0) {
+        auto precondition = [&]() -> bmg_status_t {  // z = one block V-cycle on r from z = 0
+            launch_zero_block(K, A, z, s);
+            return bmg_vcycle_block(h, K, r, z, 1, cuda_stream);
+        };
+        int cur = 0;
+        TRY(precondition());
+        CK(cudaMemcpyAsync(p, z, np * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        launch_dot_block(K, A, r, z, h->blk_partials, sc + cur * K, s);
+        while (k < maxiter) {
+            launch_matvec_block(K, A, p, q, s);
+            launch_dot_block(K, A, p, q, h->blk_partials, sc + PQ, s);
+            launch_cg_update_block(K, A, sc, cur * K, PQ, mask, p, q, x, r, s);  // alpha_c = rho_c / (p.q)_c
+            k++;
+            launch_norm_block(K, A, r, h->blk_partials, h->blk_norm, s);
+            TRY(host_norms(h->blk_norm, rn));
+            if (hist_host)
+                memcpy(hist_host + (size_t)k * K, rn, K * sizeof(double));
+            for (int c = 0; c < K; c++)
+                if (rn[c] <= tol * fn[c])
+                    mask &= ~(1u << c);
+            if (!mask)
+                break;
+            const int nxt = 1 - cur;
+            TRY(precondition());
+            launch_dot_block(K, A, r, z, h->blk_partials, sc + nxt * K, s);
+            launch_cg_direction_block(K, A, sc, nxt * K, cur * K, mask, z, p, s);  // beta_c = rho'_c / rho_c
+            cur = nxt;
+        }
+    }
+    CK(cudaGetLastError());
+    if (iters_out)
+        *iters_out = k;
+    return mask == 0 ? BMG_OK : fail(BMG_ENOTCONV, "maxiter reached");
 }
 
 bmg_status_t bmg_num_levels(bmg_solver_t h, int *L)

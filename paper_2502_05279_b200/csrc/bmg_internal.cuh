@@ -179,6 +179,15 @@ void launch_resid_norm_block(int K, const Op &A, const double *f, const double *
                              cudaStream_t s);
 void launch_norm_block(int K, const Op &A, const double *g, double *partials, double *result, cudaStream_t s);
 void launch_zero_block(int K, const Op &A, double *x, cudaStream_t s);
+// block PCG (c13 x c15): per-column dot products (K results), q = A p, and the
+// CG updates of the columns in `mask` with alpha/beta = sc[inum + c] / sc[iden + c]
+void launch_dot_block(int K, const Op &A, const double *a, const double *b, double *partials, double *result,
+                      cudaStream_t s);
+void launch_matvec_block(int K, const Op &A, const double *p, double *q, cudaStream_t s);
+void launch_cg_update_block(int K, const Op &A, const double *sc, int inum, int iden, unsigned mask, const double *p,
+                            const double *q, double *x, double *r, cudaStream_t s);
+void launch_cg_direction_block(int K, const Op &A, const double *sc, int inum, int iden, unsigned mask,
+                               const double *z, double *p, cudaStream_t s);
 void launch_zero_col_block(int K, const Op &A, double *x, int col, cudaStream_t s);
 
 // Small levels l0..L-1 of the cycle in one single-CTA launch (k_tail).  Lives in

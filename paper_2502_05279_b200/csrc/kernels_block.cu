@@ -594,6 +594,105 @@ __global__ void kb_norm_final(const double *__restrict__ partials, double *__res
         result[blockIdx.x] = sqrt(acc);
 }
 
+// ------------------------------------------------------------------ block PCG vectors (c13 x c15)
+// <a_c, b_c> per column: the tree of k_dot_partial / k_sum_final per column
+template <int K>
+__global__ void kb_dot_partial(Op A, const double *__restrict__ a, const double *__restrict__ b,
+                               double *__restrict__ partials)
+{
+    double acc[K];
+#pragma unroll
+    for (int c = 0; c < K; c++)
+        acc[c] = 0.0;
+    const long long P = A.pitch;
+    for (int j = A.ylo + blockIdx.x; j < A.yhi; j += gridDim.x)
+        for (int i = 1 + threadIdx.x; i <= A.nx; i += blockDim.x) {
+            const long long p = j * P + i;
+            double va[K], vb[K];
+            ldk<K>(a + p * K, va);
+            ldk<K>(b + p * K, vb);
+#pragma unroll
+            for (int c = 0; c < K; c++)
+                acc[c] = __fma_rn(va[c], vb[c], acc[c]);
+        }
+#pragma unroll
+    for (int c = 0; c < K; c++) {
+        const double t = block_sum(acc[c]);
+        if (threadIdx.x == 0)
+            partials[c * NORM_BLOCKS + blockIdx.x] = t;
+    }
+}
+
+__global__ void kb_sum_final(const double *__restrict__ partials, double *__restrict__ result)
+{
+    double acc = 0.0;
+    const double *pc = partials + blockIdx.x * NORM_BLOCKS;
+    for (int k = threadIdx.x; k < NORM_BLOCKS; k += blockDim.x)
+        acc += pc[k];
+    acc = block_sum(acc);
+    if (threadIdx.x == 0)
+        result[blockIdx.x] = acc;
+}
+
+// q = A p (interior), k_matvec per column
+template <int K>
+__global__ void kb_matvec(Op A, const double *__restrict__ p, double *__restrict__ q)
+{
+    constexpr int W = Split<K>::W, TP = Split<K>::TP;
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x, sub = gx % TP, i = gx / TP + 1;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y + A.ylo;
+    if (i > A.nx || j >= A.yhi)
+        return;
+    const long long P = A.pitch, k = j * P + i;
+    const Row9 a = load_row9(A, k);
+    double sm[W], pp[W];
+    offdiag_w<W, K>(a, p + sub * W, k, P, sm);
+    ldk<W>(p + sub * W + k * K, pp);
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        sm[c] = __fma_rn(a.o, pp[c], sm[c]);
+    stk<W>(q + sub * W + k * K, sm);
+}
+
+// active columns (bit c of mask): x_c += alpha_c p_c, r_c -= alpha_c q_c with
+// alpha_c = sc[inum + c] / sc[iden + c] (k_cg_update per column); others untouched
+template <int K>
+__global__ void kb_cg_update(Op A, const double *__restrict__ sc, int inum, int iden, unsigned mask,
+                             const double *__restrict__ p, const double *__restrict__ q, double *__restrict__ x,
+                             double *__restrict__ r)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y + A.ylo;
+    if (i > A.nx || j >= A.yhi)
+        return;
+    const long long k = (j * A.pitch + i) * K;
+#pragma unroll
+    for (int c = 0; c < K; c++)
+        if ((mask >> c) & 1u) {
+            const double alpha = sc[inum + c] / sc[iden + c];
+            x[k + c] = __fma_rn(alpha, p[k + c], x[k + c]);
+            r[k + c] = __fma_rn(-alpha, q[k + c], r[k + c]);
+        }
+}
+
+// active columns: p_c = z_c + beta_c p_c, beta_c = sc[inum + c] / sc[iden + c]
+template <int K>
+__global__ void kb_cg_direction(Op A, const double *__restrict__ sc, int inum, int iden, unsigned mask,
+                                const double *__restrict__ z, double *__restrict__ p)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y + A.ylo;
+    if (i > A.nx || j >= A.yhi)
+        return;
+    const long long k = (j * A.pitch + i) * K;
+#pragma unroll
+    for (int c = 0; c < K; c++)
+        if ((mask >> c) & 1u) {
+            const double beta = sc[inum + c] / sc[iden + c];
+            p[k + c] = __fma_rn(beta, p[k + c], z[k + c]);
+        }
+}
+
 __global__ void kb_zero(long long n, double *x)
 {
     const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -659,6 +758,28 @@ struct Launch {
         const int n = A.nx * A.ny;
         const int threads = n < 32 ? 32 : (n < 1024 ? ((n + 31) / 32) * 32 : 1024);
         kb_coarse_solve<K><<<K, threads, sizeof(double) * n, s>>>(A, Lf, f, u);
+    }
+    static void dot(const Op &A, const double *a, const double *b, double *partials, double *result, cudaStream_t s)
+    {
+        kb_dot_partial<K><<<NORM_BLOCKS, 256, 0, s>>>(A, a, b, partials);
+        kb_sum_final<<<K, 1024, 0, s>>>(partials, result);
+    }
+    static void matvec(const Op &A, const double *p, double *q, cudaStream_t s)
+    {
+        const dim3 b(32, 8), g((A.nx * TP + 31) / 32, (A.yhi - A.ylo + 7) / 8);
+        kb_matvec<K><<<g, b, 0, s>>>(A, p, q);
+    }
+    static void cg_update(const Op &A, const double *sc, int inum, int iden, unsigned mask, const double *p,
+                          const double *q, double *x, double *r, cudaStream_t s)
+    {
+        const dim3 b(32, 8), g((A.nx + 31) / 32, (A.yhi - A.ylo + 7) / 8);
+        kb_cg_update<K><<<g, b, 0, s>>>(A, sc, inum, iden, mask, p, q, x, r);
+    }
+    static void cg_direction(const Op &A, const double *sc, int inum, int iden, unsigned mask, const double *z,
+                             double *p, cudaStream_t s)
+    {
+        const dim3 b(32, 8), g((A.nx + 31) / 32, (A.yhi - A.ylo + 7) / 8);
+        kb_cg_direction<K><<<g, b, 0, s>>>(A, sc, inum, iden, mask, z, p);
     }
     static void norm(const Op &A, const double *f, const double *u, double *partials, double *result, cudaStream_t s)
     {
@@ -741,6 +862,29 @@ void launch_zero_col_block(int K, const Op &A, double *x, int col, cudaStream_t 
 {
     const long long n = (A.ny + 2) * A.pitch;
     kb_zero_col<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, K, col, x);
+}
+
+void launch_dot_block(int K, const Op &A, const double *a, const double *b, double *partials, double *result,
+                      cudaStream_t s)
+{
+    BMG_BLOCK_DISPATCH(K, dot(A, a, b, partials, result, s));
+}
+
+void launch_matvec_block(int K, const Op &A, const double *p, double *q, cudaStream_t s)
+{
+    BMG_BLOCK_DISPATCH(K, matvec(A, p, q, s));
+}
+
+void launch_cg_update_block(int K, const Op &A, const double *sc, int inum, int iden, unsigned mask, const double *p,
+                            const double *q, double *x, double *r, cudaStream_t s)
+{
+    BMG_BLOCK_DISPATCH(K, cg_update(A, sc, inum, iden, mask, p, q, x, r, s));
+}
+
+void launch_cg_direction_block(int K, const Op &A, const double *sc, int inum, int iden, unsigned mask,
+                               const double *z, double *p, cudaStream_t s)
+{
+    BMG_BLOCK_DISPATCH(K, cg_direction(A, sc, inum, iden, mask, z, p, s));
 }
 
 void launch_zero_block(int K, const Op &A, double *x, cudaStream_t s)

@@ -207,3 +207,33 @@ def test_block_fullsize_vs_single():
         tol = 2e-12 * torch.maximum(o.abs(), o.abs().max())
         assert bool(((g - o).abs() <= tol).all()), float((g - o).abs().max())
     s.close()
+
+
+@pytest.mark.parametrize("wl,n,K,tol", [("checker", 127, 3, 1e-10), ("lognormal", 63, 4, 1e-10),
+                                        ("random9", 65, 2, 1e-10), ("checker", 511, 8, 1e-9)])
+def test_block_pcg_parity(orc, wl, n, K, tol):
+    """bmg_pcg_block: every column against its own oracle PCG (c13) -- its
+    iteration count (the first step whose norm meets the test), its history up
+    to there (DESIGN §7 norms) and its iterate (1e-10, as tests/test_gpu_pcg.py);
+    the block takes the slowest column's count; frozen columns repeat their norm."""
+    st = P.workload(wl, n, n)
+    prm = bmg.bmg_params_default()
+    prm.nu1, prm.nu2, prm.cycle_sym = 1, 1, 1
+    s = bmg.Solver(st, prm)
+    h = orc.Hierarchy(st, nu1=1, nu2=1, cycle_sym=1)
+    F = [P.rhs_const(n, n)] + [P.field_uniform(n, n, seed=700 + c) for c in range(K - 1)]
+    X = [np.zeros((n + 2, n + 2))] + [P.field_uniform(n, n, seed=800 + c) for c in range(K - 1)]
+    xb = s.block_grid(K, X)
+    it, hist, rc = s.pcg_block(s.block_grid(K, F), xb, tol, 200)
+    Uo, its, hists, rcs = h.pcg_block(np.stack(F), np.stack(X), tol, 200)
+    assert rc == 0 and all(r == 0 for r in rcs) and it == max(its)
+    got = bmg.from_device_block(xb, n)
+    for c in range(K):
+        fn = np.linalg.norm(F[c][1:-1, 1:-1])
+        kc = int(np.argmax(hist[:, c] <= tol * fn))
+        assert kc == its[c], (c, kc, its[c])
+        ho = hists[c]
+        assert np.all(np.abs(hist[: kc + 1, c] - ho) <= 1e-10 * ho + 1e-12 * ho[0])
+        assert np.all(hist[kc:, c] == hist[kc, c])  # frozen after convergence
+        assert_iterate_close(got[c], Uo[c], rtol=1e-10)
+    s.close()

@@ -81,3 +81,19 @@ def test_block_not_converged(orc):
     F = np.stack([P.rhs_const(n, n), P.field_uniform(n, n, seed=1)])
     U, it, hist, rc = h.solve_block(F, np.zeros_like(F), 1e-14, 3)
     assert rc == orc.ENOTCONV and it == 3 and hist.shape == (4, 2)
+
+
+def test_block_pcg_columns(orc):
+    """c13 x c15: block PCG = independent PCG per column.  Pinned by exact
+    homogeneity (CG from x0 = 0 on 2f / -f runs the same alpha, beta on scaled
+    vectors: x(2f) = 2 x(f), x(-f) = -x(f), same iteration counts) and the zero
+    column (x = 0, 0 iterations)."""
+    n = 63
+    st = P.workload("checker", n, n)
+    h = orc.Hierarchy(st, nu1=1, nu2=1, cycle_sym=1)
+    f = P.rhs_const(n, n)
+    F = np.stack([f, 2 * f, -f, np.zeros_like(f)])
+    U, its, hists, rcs = h.pcg_block(F, np.zeros_like(F), 1e-10, 100)
+    assert rcs == [orc.OK] * 4 and its[0] == its[1] == its[2] > 0 and its[3] == 0
+    assert np.array_equal(U[1], 2 * U[0]) and np.array_equal(U[2], -U[0]) and np.all(U[3] == 0)
+    assert np.array_equal(hists[1], 2 * hists[0]) and np.array_equal(hists[2], hists[0])

@@ -15,7 +15,7 @@ run --config checker4096 --steps 50 --e2e-steps 2 --pcg 1
 run --config poisson8193 --steps 200
 run --config poisson8193 --steps 200 --no-cpu-baseline --e2e-steps 0 --unfused
 run --config poisson8193 --steps 40 --no-cpu-baseline --e2e-steps 0 --nrhs 8
-run --config checker4096 --steps 40 --no-cpu-baseline --e2e-steps 0 --nrhs 4
+run --config checker4096 --steps 40 --no-cpu-baseline --e2e-steps 0 --nrhs 4 --pcg 1
 N=4095 WL=aniso NCYC=1 RELAX=2 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $out/yline_launches.csv python tools/profile_cycle.py > $out/ncu.log 2>&1
 N=8191 WL=poisson NCYC=2 RELAX=0 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $out/cycle_launches.csv python tools/profile_cycle.py >> $out/ncu.log 2>&1
 N=8191 WL=poisson NCYC=1 NRHS=8 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $out/block8_launches.csv python tools/profile_cycle.py >> $out/ncu.log 2>&1
