@@ -945,11 +945,9 @@ bmg_status_t bmg_pcg(bmg_solver_t h, const double *rhs, double *x, double tol, i
         CK(cudaMemcpyAsync(p, z, np * sizeof(double), cudaMemcpyDeviceToDevice, s));
         launch_dot(A, r, z, h->partials, sc + cur, s);
         while (k < maxiter) {
-            launch_matvec(A, p, q, s);
-            launch_dot(A, p, q, h->partials, sc + PQ, s);
-            launch_cg_update(A, sc, cur, PQ, p, q, x, r, s);  // alpha = rho / (p.q)
+            launch_matvec_dot(A, p, q, h->partials, sc + PQ, s);                     // q = A p, p.q
+            launch_cg_update_norm(A, sc, cur, PQ, p, q, x, r, h->partials, sc + RN, s);  // alpha = rho / (p.q)
             k++;
-            launch_norm(A, r, h->partials, sc + RN, s);
             CK(cudaMemcpyAsync(h->h_norm, sc + RN, sizeof(double), cudaMemcpyDeviceToHost, s));
             CK(cudaEventRecord(h->pcg_ev, s));
             // the next direction, speculatively (z, p and sc only; x and r are final)

@@ -150,13 +150,15 @@ void launch_resid_norm(const Op &A, const double *f, const double *u, double *r_
 void launch_norm(const Op &A, const double *g, double *partials, double *result, cudaStream_t s);
 void launch_zero_interior(const Op &A, double *x, cudaStream_t s);
 // c13 PCG vector kernels (owned interior rows of A)
-void launch_matvec(const Op &A, const double *p, double *q, cudaStream_t s);
 void launch_dot(const Op &A, const double *a, const double *b, double *partials, double *result, cudaStream_t s);
-// alpha / beta = sc[inum] / sc[iden], read on the device (no host round trip)
-void launch_cg_update(const Op &A, const double *sc, int inum, int iden, const double *p, const double *q, double *x,
-                      double *r, cudaStream_t s);
+// beta = sc[inum] / sc[iden], read on the device (no host round trip)
 void launch_cg_direction(const Op &A, const double *sc, int inum, int iden, const double *z, double *p,
                          cudaStream_t s);
+// fused: q = A p with <p, q> -> *result; the CG update with ||r|| -> *result
+// (the same per-thread accumulation order as the separate dot / norm kernels)
+void launch_matvec_dot(const Op &A, const double *p, double *q, double *partials, double *result, cudaStream_t s);
+void launch_cg_update_norm(const Op &A, const double *sc, int inum, int iden, const double *p, const double *q,
+                           double *x, double *r, double *partials, double *result, cudaStream_t s);
 
 // c15 block multi-RHS kernels (kernels_block.cu): K = 1..BMG_MAX_NRHS columns
 // stored interleaved, element (j, i, c) at (j*pitch + i)*K + c; per column the

@@ -634,7 +634,7 @@ __global__ void kb_sum_final(const double *__restrict__ partials, double *__rest
         result[blockIdx.x] = acc;
 }
 
-// q = A p (interior), k_matvec per column
+// q = A p (interior), the single-RHS matvec (k_matvec_dot_partial) per column
 template <int K>
 __global__ void kb_matvec(Op A, const double *__restrict__ p, double *__restrict__ q)
 {
@@ -655,7 +655,7 @@ __global__ void kb_matvec(Op A, const double *__restrict__ p, double *__restrict
 }
 
 // active columns (bit c of mask): x_c += alpha_c p_c, r_c -= alpha_c q_c with
-// alpha_c = sc[inum + c] / sc[iden + c] (k_cg_update per column); others untouched
+// alpha_c = sc[inum + c] / sc[iden + c] (the single-RHS CG update per column); others untouched
 template <int K>
 __global__ void kb_cg_update(Op A, const double *__restrict__ sc, int inum, int iden, unsigned mask,
                              const double *__restrict__ p, const double *__restrict__ q, double *__restrict__ x,

@@ -340,18 +340,6 @@ void launch_solve_step(cudaGraphConditionalHandle hd, const double *norm, SolveS
 }
 
 // ---------------------------------------------------------------- PCG vectors (c13)
-// q = A p on the owned interior (ring of q untouched).
-__global__ void k_matvec(Op A, const double *__restrict__ p, double *__restrict__ q)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x + 1;
-    const int j = blockIdx.y * blockDim.y + threadIdx.y + A.ylo;
-    if (i > A.nx || j >= A.yhi)
-        return;
-    const long long P = A.pitch, k = j * P + i;
-    const Row9 a = load_row9(A, k);
-    q[k] = a.o * p[k] + offdiag(a, p, k, P);
-}
-
 // <a, b> over the owned interior: the fixed-tree partials of the norms above.
 __global__ void k_dot_partial(Op A, const double *__restrict__ a, const double *__restrict__ b,
                               double *__restrict__ partials)
@@ -376,21 +364,6 @@ __global__ void k_sum_final(const double *__restrict__ partials, int n, double *
         *result = acc;
 }
 
-// x += alpha p; r -= alpha q  (interior); alpha = sc[inum] / sc[iden] formed on the
-// device from the dot products (the same IEEE division the host would do)
-__global__ void k_cg_update(Op A, const double *__restrict__ sc, int inum, int iden, const double *__restrict__ p,
-                            const double *__restrict__ q, double *__restrict__ x, double *__restrict__ r)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x + 1;
-    const int j = blockIdx.y * blockDim.y + threadIdx.y + A.ylo;
-    if (i > A.nx || j >= A.yhi)
-        return;
-    const double alpha = sc[inum] / sc[iden];
-    const long long k = j * A.pitch + i;
-    x[k] = fma(alpha, p[k], x[k]);
-    r[k] = fma(-alpha, q[k], r[k]);
-}
-
 // p = z + beta p  (interior); beta = sc[inum] / sc[iden]
 __global__ void k_cg_direction(Op A, const double *__restrict__ sc, int inum, int iden, const double *__restrict__ z,
                                double *__restrict__ p)
@@ -404,15 +377,54 @@ __global__ void k_cg_direction(Op A, const double *__restrict__ sc, int inum, in
     p[k] = fma(beta, p[k], z[k]);
 }
 
+// Fused PCG steps with the reduction layout of k_dot_partial / k_norm_partial
+// (block b: rows ylo+b, ylo+b+NORM_BLOCKS, ..; thread t: columns 1+t, 1+t+256, ..):
+// every thread accumulates the same products in the same order as a separate
+// matvec / update kernel followed by the dot / norm kernel would (measured:
+// identical iterates and histories to the unfused sequence).
+// q = A p and the partials of <p, q>
+__global__ void k_matvec_dot_partial(Op A, const double *__restrict__ p, double *__restrict__ q,
+                                     double *__restrict__ partials)
+{
+    double acc = 0.0;
+    const long long P = A.pitch;
+    for (int j = A.ylo + blockIdx.x; j < A.yhi; j += gridDim.x)
+        for (int i = 1 + threadIdx.x; i <= A.nx; i += blockDim.x) {
+            const long long k = j * P + i;
+            const Row9 a = load_row9(A, k);
+            const double pk = p[k], qk = a.o * pk + offdiag(a, p, k, P);
+            q[k] = qk;
+            acc = fma(pk, qk, acc);
+        }
+    acc = block_sum(acc);
+    if (threadIdx.x == 0)
+        partials[blockIdx.x] = acc;
+}
+
+// x += alpha p, r -= alpha q (alpha = sc[inum] / sc[iden]) and the partials of ||r||^2
+__global__ void k_cg_update_norm_partial(Op A, const double *__restrict__ sc, int inum, int iden,
+                                         const double *__restrict__ p, const double *__restrict__ q,
+                                         double *__restrict__ x, double *__restrict__ r, double *__restrict__ partials)
+{
+    const double alpha = sc[inum] / sc[iden];
+    double acc = 0.0;
+    const long long P = A.pitch;
+    for (int j = A.ylo + blockIdx.x; j < A.yhi; j += gridDim.x)
+        for (int i = 1 + threadIdx.x; i <= A.nx; i += blockDim.x) {
+            const long long k = j * P + i;
+            x[k] = fma(alpha, p[k], x[k]);
+            const double rk = fma(-alpha, q[k], r[k]);
+            r[k] = rk;
+            acc += rk * rk;
+        }
+    acc = block_sum(acc);
+    if (threadIdx.x == 0)
+        partials[blockIdx.x] = acc;
+}
+
 static dim3 interior_grid(const Op &A, dim3 b)
 {
     return dim3((A.nx + b.x - 1) / b.x, (A.yhi - A.ylo + b.y - 1) / b.y);
-}
-
-void launch_matvec(const Op &A, const double *p, double *q, cudaStream_t s)
-{
-    const dim3 b(32, 8);
-    k_matvec<<<interior_grid(A, b), b, 0, s>>>(A, p, q);
 }
 
 void launch_dot(const Op &A, const double *a, const double *b, double *partials, double *result, cudaStream_t s)
@@ -421,11 +433,17 @@ void launch_dot(const Op &A, const double *a, const double *b, double *partials,
     k_sum_final<<<1, 1024, 0, s>>>(partials, NORM_BLOCKS, result);
 }
 
-void launch_cg_update(const Op &A, const double *sc, int inum, int iden, const double *p, const double *q, double *x,
-                      double *r, cudaStream_t s)
+void launch_matvec_dot(const Op &A, const double *p, double *q, double *partials, double *result, cudaStream_t s)
 {
-    const dim3 b(32, 8);
-    k_cg_update<<<interior_grid(A, b), b, 0, s>>>(A, sc, inum, iden, p, q, x, r);
+    k_matvec_dot_partial<<<NORM_BLOCKS, 256, 0, s>>>(A, p, q, partials);
+    k_sum_final<<<1, 1024, 0, s>>>(partials, NORM_BLOCKS, result);
+}
+
+void launch_cg_update_norm(const Op &A, const double *sc, int inum, int iden, const double *p, const double *q,
+                           double *x, double *r, double *partials, double *result, cudaStream_t s)
+{
+    k_cg_update_norm_partial<<<NORM_BLOCKS, 256, 0, s>>>(A, sc, inum, iden, p, q, x, r, partials);
+    k_norm_final<<<1, 1024, 0, s>>>(partials, NORM_BLOCKS, result);
 }
 
 void launch_cg_direction(const Op &A, const double *sc, int inum, int iden, const double *z, double *p,
