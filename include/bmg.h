@@ -196,6 +196,7 @@ bmg_status_t bmg_residual_norm_block(bmg_solver_t h, int nrhs, const double *rhs
  * ||rhs_c|| = 0 is set to x_c = 0 and counts as converged.
  * hist_host: (maxiter+1) * nrhs doubles (row-major, may be NULL); iters_out:
  * block steps taken (may be NULL).  Returns ENOTCONV if maxiter was reached.
+ * The loop runs on the device (one graph launch, as bmg_solve).
  */
 bmg_status_t bmg_solve_block(bmg_solver_t h, int nrhs, const double *rhs, double *x, double tol, int maxiter,
                              int *iters_out, double *hist_host, void *cuda_stream);

@@ -127,6 +127,11 @@ struct bmg_solver {
     std::map<std::pair<const void *, const void *>, cudaGraphExec_t> bgraphs;  // block cycle graphs (blk_K)
     double *pcgb_ws = nullptr;  // block PCG: r, z, p, q (K-interleaved level-0 arrays) + scalar slots
     int pcgb_K = 0;
+    // device-side block solve loop (blk_K columns): graphs per (rhs, x), state, history
+    std::map<std::pair<const void *, const void *>, cudaGraphExec_t> sbgraphs;
+    SolveStateBlock *sb_st = nullptr, *sb_st_h = nullptr;
+    double *sb_hist = nullptr;
+    size_t sb_cap = 0;
 
     CIv civ(int l) const
     {
@@ -224,6 +229,12 @@ bmg_status_t bmg_destroy(bmg_solver_t h)
         cudaFree(h->blk_arena);
     if (h->pcgb_ws)
         cudaFree(h->pcgb_ws);
+    for (auto &kv : h->sbgraphs)
+        cudaGraphExecDestroy(kv.second);
+    if (h->sb_hist)
+        cudaFree(h->sb_hist);
+    if (h->sb_st_h)
+        cudaFreeHost(h->sb_st_h);
     if (h->h_norm)
         cudaFreeHost(h->h_norm);
     if (h->cap)
@@ -985,6 +996,9 @@ static bmg_status_t block_workspace(bmg_solver *h, int K, cudaStream_t s)
     for (auto &kv : h->bgraphs)
         cudaGraphExecDestroy(kv.second);
     h->bgraphs.clear();
+    for (auto &kv : h->sbgraphs)
+        cudaGraphExecDestroy(kv.second);
+    h->sbgraphs.clear();
     if (h->blk_arena)
         cudaFree(h->blk_arena);
     h->blk_arena = nullptr;
@@ -1157,12 +1171,74 @@ bmg_status_t bmg_solve_block(bmg_solver_t h, int nrhs, const double *rhs, double
         return true;
     };
     int k = 0;
-    while (!done() && k < maxiter) {
-        TRY(bmg_vcycle_block(h, K, rhs, x, 1, cuda_stream));
-        k++;
-        TRY(block_norms(h, K, rhs, x, rn, s));
+    if (!done() && maxiter > 0) {  // device loop: one graph launch (as bmg_solve), one wait
+        const size_t need = (size_t)(maxiter + 1) * K;
+        if (h->sb_cap < need) {
+            CK(cudaStreamSynchronize(s));
+            for (auto &kv : h->sbgraphs)
+                cudaGraphExecDestroy(kv.second);
+            h->sbgraphs.clear();
+            if (h->sb_hist)
+                cudaFree(h->sb_hist);
+            h->sb_hist = nullptr;
+            h->sb_cap = 0;
+            const size_t cap = need > 8192 ? need : 8192;
+            void *q;
+            CK(cudaMalloc(&q, sizeof(double) * cap + sizeof(SolveStateBlock) + 64));
+            h->sb_hist = (double *)q;
+            h->sb_cap = cap;
+            h->sb_st = (SolveStateBlock *)(h->sb_hist + cap + 1);
+            if (!h->sb_st_h)
+                CK(cudaMallocHost(&h->sb_st_h, sizeof(SolveStateBlock)));
+        }
+        auto key = std::make_pair((const void *)rhs, (const void *)x);
+        auto it = h->sbgraphs.find(key);
+        if (it == h->sbgraphs.end()) {
+            cudaGraph_t g;
+            CK(cudaGraphCreate(&g, 0));
+            cudaGraphConditionalHandle hd;
+            CK(cudaGraphConditionalHandleCreate(&hd, g, 1, cudaGraphCondAssignDefault));
+            cudaGraphNodeParams cp = {};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = hd;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            cudaGraphNode_t node;
+            CK(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+            cudaGraph_t body = cp.conditional.phGraph_out[0];
+            CK(cudaStreamBeginCaptureToGraph(h->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+            enqueue_cycle_block(h, K, rhs, x, h->cap);
+            launch_resid_norm_block(K, h->lv[0].op(), rhs, x, h->blk_partials, h->blk_norm, h->cap);
+            launch_solve_step_block(hd, h->blk_norm, h->sb_st, h->sb_hist, h->cap);
+            cudaError_t e = cudaStreamEndCapture(h->cap, &body);
+            if (e == cudaSuccess) {
+                cudaGraphExec_t ex;
+                e = cudaGraphInstantiate(&ex, g, 0);
+                if (e == cudaSuccess)
+                    it = h->sbgraphs.emplace(key, ex).first;
+            }
+            cudaGraphDestroy(g);
+            if (e != cudaSuccess)
+                return fail(BMG_ECUDA, std::string("block solve graph: ") + cudaGetErrorString(e));
+        }
+        SolveStateBlock &st = *h->sb_st_h;
+        for (int c = 0; c < K; c++)
+            st.fn[c] = fn[c];
+        st.tol = tol;
+        st.k = 0;
+        st.maxiter = maxiter;
+        st.K = K;
+        CK(cudaMemcpyAsync(h->sb_st, h->sb_st_h, sizeof(SolveStateBlock), cudaMemcpyHostToDevice, s));
+        CK(cudaGraphLaunch(it->second, s));
+        CK(cudaMemcpyAsync(h->sb_st_h, h->sb_st, sizeof(SolveStateBlock), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        k = h->sb_st_h->k;
+        std::vector<double> hv((size_t)(k + 1) * K);
+        CK(cudaMemcpy(hv.data(), h->sb_hist, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost));
+        for (int c = 0; c < K; c++)
+            rn[c] = hv[(size_t)k * K + c];
         if (hist_host)
-            memcpy(hist_host + (size_t)k * K, rn, K * sizeof(double));
+            memcpy(hist_host + K, hv.data() + K, sizeof(double) * (size_t)k * K);
     }
     if (iters_out)
         *iters_out = k;

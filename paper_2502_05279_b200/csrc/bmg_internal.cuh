@@ -218,6 +218,14 @@ struct SolveState {
 void launch_solve_step(cudaGraphConditionalHandle hd, const double *norm, SolveState *st, double *hist,
                        cudaStream_t s);
 
+// the block solve's state (K columns): continue while any ||r_c|| > tol ||rhs_c||
+struct SolveStateBlock {
+    double fn[8], tol;
+    int k, maxiter, K;
+};
+void launch_solve_step_block(cudaGraphConditionalHandle hd, const double *norms, SolveStateBlock *st, double *hist,
+                             cudaStream_t s);
+
 constexpr int NORM_BLOCKS = 592;  // 4 x 148 SMs; fixed so the reduction tree is fixed
 
 }  // namespace bmg

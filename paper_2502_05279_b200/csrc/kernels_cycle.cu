@@ -339,6 +339,28 @@ void launch_solve_step(cudaGraphConditionalHandle hd, const double *norm, SolveS
     k_solve_step<<<1, 1, 0, s>>>(hd, norm, st, hist);
 }
 
+// the block solve's step (c15): the K norms go to hist row k; the loop repeats
+// while any column fails its test and k < maxiter
+__global__ void k_solve_step_block(cudaGraphConditionalHandle hd, const double *__restrict__ norms,
+                                   SolveStateBlock *st, double *__restrict__ hist)
+{
+    const int k = ++st->k, K = st->K;
+    bool more = false;
+    for (int c = 0; c < K; c++) {
+        const double rn = norms[c];
+        hist[(size_t)k * K + c] = rn;
+        if (rn > st->tol * st->fn[c])
+            more = true;
+    }
+    cudaGraphSetConditional(hd, (more && k < st->maxiter) ? 1u : 0u);
+}
+
+void launch_solve_step_block(cudaGraphConditionalHandle hd, const double *norms, SolveStateBlock *st, double *hist,
+                             cudaStream_t s)
+{
+    k_solve_step_block<<<1, 1, 0, s>>>(hd, norms, st, hist);
+}
+
 // ---------------------------------------------------------------- PCG vectors (c13)
 // <a, b> over the owned interior: the fixed-tree partials of the norms above.
 __global__ void k_dot_partial(Op A, const double *__restrict__ a, const double *__restrict__ b,
