@@ -550,33 +550,36 @@ template <int K, bool RESID>
 __global__ void kb_norm_partial(Op A, const double *__restrict__ f, const double *__restrict__ u,
                                 double *__restrict__ partials)
 {
-    double acc[K];
+    // thread t: column slice sub = t % TP of the points 1 + t/TP, 1 + t/TP + 256/TP, ...
+    // of the rows ylo + b, ylo + b + NORM_BLOCKS, ...; fixed trees per column
+    constexpr int W = Split<K>::W, TP = Split<K>::TP;
+    const int sub = threadIdx.x % TP, i0 = threadIdx.x / TP, di = blockDim.x / TP;
+    double acc[W];
 #pragma unroll
-    for (int c = 0; c < K; c++)
+    for (int c = 0; c < W; c++)
         acc[c] = 0.0;
     const long long P = A.pitch;
-    for (int j = A.ylo + blockIdx.x; j < A.yhi; j += gridDim.x) {
-        for (int i = 1 + threadIdx.x; i <= A.nx; i += blockDim.x) {
-            const long long p = j * P + i;
-            double v[K];
-            ldk<K>(f + p * K, v);
-            if (RESID) {
-                const Row9 a = load_row9(A, p);
-                double s[K], up[K];
-                offdiag_w<K, K>(a, u, p, P, s);
-                ldk<K>(u + p * K, up);
+    const bool idle = (int)threadIdx.x >= di * TP;  // TP need not divide blockDim.x
+    for (int j = A.ylo + blockIdx.x; j < A.yhi && !idle; j += gridDim.x) {
+        for (int i = 1 + i0; i <= A.nx; i += di) {
+            double v[W];
+            if (RESID)
+                resid_w<W, K>(A, f + sub * W, u + sub * W, i, j, v);  // 5-point: no zero corner terms
+            else
+                ldk<W>(f + sub * W + (j * P + i) * K, v);
 #pragma unroll
-                for (int c = 0; c < K; c++)
-                    v[c] = v[c] - __fma_rn(a.o, up[c], s[c]);
-            }
-#pragma unroll
-            for (int c = 0; c < K; c++)
+            for (int c = 0; c < W; c++)
                 acc[c] = __fma_rn(v[c], v[c], acc[c]);
         }
     }
 #pragma unroll
     for (int c = 0; c < K; c++) {
-        const double t = block_sum(acc[c]);
+        double mine = 0.0;
+#pragma unroll
+        for (int w = 0; w < W; w++)
+            if (sub * W + w == c)
+                mine = acc[w];
+        const double t = block_sum(mine);
         if (threadIdx.x == 0)
             partials[c * NORM_BLOCKS + blockIdx.x] = t;
     }
