@@ -603,24 +603,33 @@ template <int K>
 __global__ void kb_dot_partial(Op A, const double *__restrict__ a, const double *__restrict__ b,
                                double *__restrict__ partials)
 {
-    double acc[K];
+    // the thread layout of kb_norm_partial (column slices, fixed trees per column)
+    constexpr int W = Split<K>::W, TP = Split<K>::TP;
+    const int sub = threadIdx.x % TP, i0 = threadIdx.x / TP, di = blockDim.x / TP;
+    double acc[W];
 #pragma unroll
-    for (int c = 0; c < K; c++)
+    for (int c = 0; c < W; c++)
         acc[c] = 0.0;
     const long long P = A.pitch;
-    for (int j = A.ylo + blockIdx.x; j < A.yhi; j += gridDim.x)
-        for (int i = 1 + threadIdx.x; i <= A.nx; i += blockDim.x) {
-            const long long p = j * P + i;
-            double va[K], vb[K];
-            ldk<K>(a + p * K, va);
-            ldk<K>(b + p * K, vb);
+    const bool idle = (int)threadIdx.x >= di * TP;
+    for (int j = A.ylo + blockIdx.x; j < A.yhi && !idle; j += gridDim.x)
+        for (int i = 1 + i0; i <= A.nx; i += di) {
+            const long long p = (j * P + i) * K + sub * W;
+            double va[W], vb[W];
+            ldk<W>(a + p, va);
+            ldk<W>(b + p, vb);
 #pragma unroll
-            for (int c = 0; c < K; c++)
+            for (int c = 0; c < W; c++)
                 acc[c] = __fma_rn(va[c], vb[c], acc[c]);
         }
 #pragma unroll
     for (int c = 0; c < K; c++) {
-        const double t = block_sum(acc[c]);
+        double mine = 0.0;
+#pragma unroll
+        for (int w = 0; w < W; w++)
+            if (sub * W + w == c)
+                mine = acc[w];
+        const double t = block_sum(mine);
         if (threadIdx.x == 0)
             partials[c * NORM_BLOCKS + blockIdx.x] = t;
     }
