@@ -595,7 +595,11 @@ __device__ __forceinline__ void tail_relax(const Op &A, const double *f, double 
     }
 }
 
-__global__ void __launch_bounds__(1024, 1) k_tail(const TailPlan *__restrict__ tp, const double *f0, double *u0)
+#ifndef BMG_TAIL_THREADS
+#define BMG_TAIL_THREADS 512  // 1024 spilled (64 registers); 512: none, config-1 cycle 68 -> 60 us
+#endif
+__global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail(const TailPlan *__restrict__ tp, const double *f0,
+                                                              double *u0)
 {
     extern __shared__ double b[];
     const int l0 = tp->l0, L = tp->L, nt = blockDim.x;
@@ -652,7 +656,7 @@ __global__ void __launch_bounds__(1024, 1) k_tail(const TailPlan *__restrict__ t
 
 void launch_tail(const TailPlan *tp_dev, int ncoarse, const double *f0, double *u0, cudaStream_t s)
 {
-    k_tail<<<1, 1024, sizeof(double) * (ncoarse > 0 ? ncoarse : 1), s>>>(tp_dev, f0, u0);
+    k_tail<<<1, BMG_TAIL_THREADS, sizeof(double) * (ncoarse > 0 ? ncoarse : 1), s>>>(tp_dev, f0, u0);
 }
 
 }  // namespace bmg
