@@ -337,7 +337,13 @@ __device__ __forceinline__ void racc(double (&v)[W], double w, const double (&r)
 // shared memory; phase 2 forms each coarse value from there in
 // restrict_pt_vanish's order.  (The untiled kernel evaluates each corner for
 // all four coarse points that use it.)
-constexpr int RT_CX = 16, RT_CY = 8;
+#ifndef BMG_RT_CX
+#define BMG_RT_CX 16
+#endif
+#ifndef BMG_RT_CY
+#define BMG_RT_CY 8
+#endif
+constexpr int RT_CX = BMG_RT_CX, RT_CY = BMG_RT_CY;
 
 // CTA shape of the per-colour GS kernels (tuning knob)
 #ifndef BMG_KB_BX
