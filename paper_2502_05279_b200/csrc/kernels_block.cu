@@ -352,6 +352,12 @@ constexpr int RT_CX = BMG_RT_CX, RT_CY = BMG_RT_CY;
 #ifndef BMG_KB_BY
 #define BMG_KB_BY 2
 #endif
+#ifndef BMG_KB9_BX
+#define BMG_KB9_BX BMG_KB_BX
+#endif
+#ifndef BMG_KB9_BY
+#define BMG_KB9_BY BMG_KB_BY
+#endif
 template <int K, int KIND>
 __global__ void __launch_bounds__(256) kb_resid_restrict_tiled(Op A, CIv ci, const double *__restrict__ f,
                                                                const double *__restrict__ u, double *__restrict__ qc,
@@ -733,9 +739,10 @@ struct Launch {
                 if (nlaunch)
                     *nlaunch += 2;
             } else {
-                const dim3 g(((A.nx / 2 + 1) * TP + b.x - 1) / b.x, (A.ny / 2 + 1 + b.y - 1) / b.y);
+                const dim3 b9(BMG_KB9_BX, BMG_KB9_BY);
+                const dim3 g(((A.nx / 2 + 1) * TP + b9.x - 1) / b9.x, (A.ny / 2 + 1 + b9.y - 1) / b9.y);
                 for (int c = 0; c < 4; c++)
-                    kb_relax9<K><<<g, b, 0, s>>>(A, f, u, rev ? 3 - c : c);
+                    kb_relax9<K><<<g, b9, 0, s>>>(A, f, u, rev ? 3 - c : c);
                 if (nlaunch)
                     *nlaunch += 4;
             }
