@@ -30,6 +30,7 @@ CONFIG_KIND = {"aniso": 9}
 # floor of the residual at 4095^2 and 8191^2 with f = h^2 (measured floor ~6e-10 relative at 8191^2)
 SOLVE_TOL = {"aniso4097": 1e-8, "checker4096": 1e-8, "poisson8193": 1e-8}
 SOLVE_MAXIT = 100
+TAIL_UNKNOWNS = 1024  # levels with at most this many unknowns run in the tail kernel
 
 CONFIGS = {
     # name: (workload, nx, ny, description)
@@ -149,52 +150,52 @@ def host_info():
 
 
 # ------------------------------------------------------------------ oracle (CPU) legs
-ORACLE_SAMPLE_N = 2047
 RELAX = {"point": 0, "xline": 1, "yline": 2, "altline": 3}
 
 
-def oracle_cycles_per_s(wl, nx, ny, ncycles, warm=1, relax="point"):
-    """Time the oracle V(2,1) on a bounded sample (n=2047, 1/16 of the 8191^2
-    unknowns); returns (cycles/s scaled to the full workload, sample string)."""
+def oracle_cycles(wl, nx, ny, ncycles, warm=0, relax="point"):
+    """Time the oracle's V(2,1) cycle on the FULL workload (same operator, f = h^2, x0 = 0;
+    setup untimed): `warm` untimed cycles, then `ncycles` timed ones, single thread.
+    Returns (cycles/s, seconds per cycle, setup seconds, sample string)."""
     import numpy as np
 
     import oracle
     from paper_2502_05279_b200 import problems as P
 
-    n = min(ORACLE_SAMPLE_N, nx, ny)
-    st = P.workload(wl, n, n)
-    f = P.rhs_const(n, n)
+    st = P.workload(wl, nx, ny)
+    f = P.rhs_const(nx, ny)
+    t = time.perf_counter()
     h = oracle.Hierarchy(st, relax=relax)
+    setup_s = time.perf_counter() - t
+    del st
     u = np.zeros_like(f)
-    for _ in range(warm):
-        u = h.vcycle(f, u, 1)
+    if warm:
+        u = h.vcycle(f, u, warm)
     t = time.perf_counter()
     u = h.vcycle(f, u, ncycles)
     dt = time.perf_counter() - t
-    scale = (n * n) / (float(nx) * float(ny))
-    per_cycle = dt / ncycles
-    return ncycles / dt * scale, per_cycle, (f"oracle V(2,1) [{relax} relaxation] on {wl} {n}x{n} (same recipe, "
-                                             f"{n*n/(nx*ny):.4f} of the "
-                                             f"{nx}x{ny} unknowns), {ncycles} timed cycles after {warm} warm-up, "
-                                             f"setup untimed; cycles/s scaled by the unknown ratio to {nx}x{ny}")
+    return ncycles / dt, dt / ncycles, setup_s, (f"oracle V(2,1) [{relax} relaxation] on the full {wl} {nx}x{ny} "
+                                                 f"workload (f=h^2, x0=0), {ncycles} timed cycles after {warm} "
+                                                 f"untimed, setup ({setup_s:.1f} s) untimed; single thread")
 
 
 def run_reference(args, cfg):
-    """--impl reference: the oracle (this tier's reference arm), rank 0 only."""
+    """--impl reference: the oracle (this tier's reference arm) on the same workload,
+    K timed cycles after W untimed ones, rank 0 only (other ranks exit without work)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     wl, nx, ny, desc = CONFIGS[cfg]
     model, cores = host_info()
-    val, per_cycle, sample = oracle_cycles_per_s(wl, nx, ny, args.steps, warm=args.warmup, relax=args.relax)
+    val, per_cycle, setup_s, sample = oracle_cycles(wl, nx, ny, args.steps, warm=args.warmup, relax=args.relax)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "cycles/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / val,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_cycle * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "nx": nx, "ny": ny, "cycle": "V(2,1)"},
+        "config": {"workload": desc, "nx": nx, "ny": ny, "cycle": "V(2,1)", "relax": args.relax},
         "munknowns_per_s": val * nx * ny / 1e6,
         "cpu_baseline": {"value": val, "unit": "cycles/s", "cores": 1, "kind": "oracle", "sample": sample,
-                         "host_cpu": model, "host_cores": cores},
+                         "host_cpu": model, "host_cores": cores, "setup_s": setup_s},
         "e2e": {"value": val, "unit": "cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -204,7 +205,7 @@ def run_reference(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="poisson8193", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -286,11 +287,15 @@ def main():
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.mark("t0")
     if not distributed:
-        # the timed cycles launch their kernels directly with a CUDA event pair around
-        # every level-0 down leg (the roofline kernel) on this stream
+        # the timed cycles replay the cycle graph's variant with a CUDA event pair around
+        # every level-0 down leg (the roofline kernel) on this stream; that variant is
+        # captured and warmed here, outside the timed region, and its records cleared
         bmg.bmg_timing(solver.h, True)
+        solver.vcycle(f, x, 1)
+        bmg.bmg_timing_read(solver.h)
+        torch.cuda.synchronize()
+    clocks.mark("t0")
     ev0.record(stream)
     solver.vcycle(f, x, args.steps)
     ev1.record(stream)
@@ -326,6 +331,14 @@ def main():
         g1.record(stream)
         torch.cuda.synchronize()
         rl["graph_replay_ms_per_step"] = g0.elapsed_time(g1) / ng
+        levels = per_level(bmg, solver, f, x, stream)
+        cyc = cycle_traffic(nx, ny, args)
+        if cyc is not None:
+            rl["cycle_dram_bytes"] = cyc
+            rl["cycle_dram_GBps"] = cyc / (ms_per_step / 1e3) / 1e9
+            rl["cycle_dram_frac"] = rl["cycle_dram_GBps"] / peak
+    else:
+        levels = None
 
     # convergence sanity of the timed run (residual at the rounding floor after many cycles)
     rnorm = solver.residual_norm(f, x)
@@ -469,10 +482,12 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        val, per_cycle, sample = oracle_cycles_per_s(wl, nx, ny, 8, warm=1, relax=args.relax)
+        # bounded: 2 full-size cycles (~7 s each at 8191^2 on the B200 host) after an untimed setup
+        nc = 2 if nx * ny > 4e6 else (8 if nx * ny > 2e5 else 50)
+        val, per_cycle, setup_s, sample = oracle_cycles(wl, nx, ny, nc, warm=0, relax=args.relax)
         model, cores = host_info()
         cpu = {"value": val, "unit": "cycles/s", "cores": 1, "kind": "oracle", "sample": sample,
-               "host_cpu": model, "host_cores": cores}
+               "host_cpu": model, "host_cores": cores, "setup_s": setup_s}
 
     B, A = model_bytes(nx, ny, kind, L, 0)
     cs = clocks.summary()
@@ -507,6 +522,8 @@ def main():
         "solve": solve,
         "cpu_baseline": cpu,
     }
+    if levels is not None:
+        line["levels"] = levels
     if block is not None:
         line["block"] = block
     if rank == 0:
@@ -514,6 +531,37 @@ def main():
     solver.close()
     if dist:
         dist.destroy_process_group()
+
+
+def per_level(bmg, solver, f, x, stream, ncycles=10):
+    """Per-leg device times of one cycle (bmg_profile_legs: an event between every two
+    legs; the paper's per-level kernel timings, fig:kernel_timings P:492-500), measured
+    after the timed region on the same arrays."""
+    torch = sys.modules["torch"]
+    down, tail, up = bmg.bmg_profile_legs(solver.h, f, x, ncycles, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    out = {"legs": [], "tail_ms": tail, "tail_levels_from": len(down), "cycles_averaged": ncycles}
+    for l in range(len(down)):
+        lnx, lny, kind = bmg.bmg_level_shape(solver.h, l)
+        out["legs"].append({"level": l, "nx": lnx, "ny": lny, "kind": kind, "down_ms": down[l], "up_ms": up[l]})
+    out["sum_ms"] = sum(down) + sum(up) + tail
+    return out
+
+
+def cycle_traffic(nx, ny, args):
+    """Sum of ncu dram read+write bytes over every kernel of one cycle at this size
+    (profiles/traffic.json 'cycles' rows, from the committed launch list), or None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            rows = json.load(fh).get("cycles", [])
+    except (OSError, ValueError):
+        return None
+    for r in rows:
+        if r.get("nx") == nx and r.get("ny") == ny and r.get("relax", "point") == args.relax and \
+                r.get("fused", True) == (not args.unfused):
+            return r["dram_bytes_per_cycle"]
+    return None
 
 
 def traffic_per_launch(kernel: str, nx: int, ny: int):
@@ -549,7 +597,10 @@ def roofline(leg, nx, ny, kind, peak, peak_src, ms_per_step, args):
     # 2N-double CI planes of fig:restrict_kernel, write f_c and zero u_c (N/4 each).
     # The kernel itself reads only the half of the CI planes whose residual does not
     # vanish, so this is an effective bandwidth; `traffic` is the real one.
-    per_unk = 8.0 * (s_planes + 2 + 1 + 2 + 0.25 + 0.25)
+    # u_c: a fused coarse down leg never reads its zero start (C4), so the fused level-0
+    # leg writes no u_c when level 1 is fused too (levels above the tail threshold)
+    uc_written = args.unfused or args.relax != "point" or (nx // 2) * (ny // 2) <= TAIL_UNKNOWNS
+    per_unk = 8.0 * (s_planes + 2 + 1 + 2 + 0.25 + (0.25 if uc_written else 0.0))
     if args.relax != "point":
         # per-step kernels: every line sweep direction reads the s planes, f and
         # u and writes u once ((s+3) doubles); then residual (s+3) and restriction (3.25)

@@ -286,6 +286,19 @@ bmg_status_t bmg_cycle_kernel_count(bmg_solver_t h, int *count);
 bmg_status_t bmg_timing(bmg_solver_t h, int enable);
 bmg_status_t bmg_timing_read(bmg_solver_t h, double *ms_total, int *launches);
 
+/* Per-leg breakdown of one cycle (SURVEY §5 per-level report, mirroring the
+ * paper's per-level kernel timings, fig:kernel_timings P:492-500).  Captures a
+ * variant of the cycle's graph with an event-record node between every two
+ * legs, replays it ncycles times on cuda_stream (synchronising after each) and
+ * returns the mean duration (ms) of every segment in ms_out[0 .. *nseg-1]:
+ *   ms_out[l]            l = 0..lt-1   down leg of level l (fused kernel or per-step kernels)
+ *   ms_out[lt]                         the tail: levels >= lt, the coarse solve and their up legs
+ *   ms_out[lt+1+k]       k = 0..lt-1   up leg of level lt-1-k
+ * with lt = (*nseg - 1) / 2.  x is advanced by ncycles cycles (as bmg_vcycle).
+ * Blocking.  EINVAL if cap < 2L+1, ncycles < 1 or the handle is distributed. */
+bmg_status_t bmg_profile_legs(bmg_solver_t h, const double *rhs, double *x, int ncycles, double *ms_out, int cap,
+                              int *nseg, void *cuda_stream);
+
 /* ---------------------------------------------------------------------------
  * Multi-GPU: row-slab domain decomposition.
  *

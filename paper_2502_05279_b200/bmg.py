@@ -24,7 +24,7 @@ EXPORTS = (
     "bmg_params_default", "bmg_setup", "bmg_vcycle", "bmg_vcycle_host", "bmg_solve", "bmg_pcg", "bmg_residual_norm",
     "bmg_num_levels", "bmg_level_shape", "bmg_level_pitch", "bmg_export_level", "bmg_relax", "bmg_residual",
     "bmg_restrict", "bmg_interp_add", "bmg_smooth_restrict", "bmg_correct_smooth", "bmg_cycle_kernel_count", "bmg_timing",
-    "bmg_timing_read", "bmg_destroy", "bmg_strerror",
+    "bmg_timing_read", "bmg_profile_legs", "bmg_destroy", "bmg_strerror",
     "bmg_last_error_detail", "bmg_partition", "bmg_setup_dist", "bmg_local_rows", "bmg_vcycle_block",
     "bmg_residual_norm_block", "bmg_solve_block", "bmg_pcg_block",
 )
@@ -96,6 +96,7 @@ def lib():
             "bmg_smooth_restrict": (i, [vp, i, vp, vp, vp, vp, vp, vp]),
             "bmg_correct_smooth": (i, [vp, i, vp, vp, vp, vp, vp]),
             "bmg_cycle_kernel_count": (i, [vp, ip]),
+            "bmg_profile_legs": (i, [vp, vp, vp, i, dp, i, ip, vp]),
             "bmg_destroy": (i, [vp]),
             "bmg_strerror": (ctypes.c_char_p, [i]),
             "bmg_last_error_detail": (ctypes.c_char_p, []),
@@ -293,6 +294,18 @@ def bmg_timing_read(h):
     n = ctypes.c_int()
     _check(lib().bmg_timing_read(h, ctypes.byref(ms), ctypes.byref(n)), "bmg_timing_read")
     return ms.value, n.value
+
+
+def bmg_profile_legs(h, rhs, x, ncycles: int = 5, stream=None):
+    """Mean device time (ms) of every leg of one cycle: (down[0..lt-1], tail, up[lt-1..0])."""
+    L = bmg_num_levels(h)
+    out = (ctypes.c_double * (2 * L + 1))()
+    n = ctypes.c_int()
+    _check(lib().bmg_profile_legs(h, _ptr(rhs), _ptr(x), ncycles, out, 2 * L + 1, ctypes.byref(n), _stream(stream)),
+           "bmg_profile_legs")
+    v = list(out[: n.value])
+    lt = (n.value - 1) // 2
+    return v[:lt], v[lt], v[lt + 1:][::-1]
 
 
 def bmg_partition(nx: int, ny: int, nranks: int, params: bmg_params_t | None = None):

@@ -431,8 +431,9 @@ static bool next_events(bmg_solver *h, cudaEvent_t *e)
 
 // rec (bmg_timing): an event pair recorded around the level-0 down leg (external
 // event-record nodes when captured)
+// seg (bmg_profile_legs): 2*lt+2 events recorded at every leg boundary
 static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream_t s,
-                         const cudaEvent_t *rec = nullptr)
+                         const cudaEvent_t *rec = nullptr, const cudaEvent_t *seg = nullptr)
 {
     int n = 0;
     const int L = h->L;
@@ -450,12 +451,18 @@ static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream
         // so the level above need not write that zero start either
         const bool uz = l > 0 && fz[l];
         double *uc = (l + 1 < lt && fz[l + 1]) ? nullptr : h->lv[l + 1].u;
+        if (seg && l == 0)
+            cudaEventRecordWithFlags(seg[0], s, cudaEventRecordExternal);
         if (rec && l == 0)
             cudaEventRecordWithFlags(rec[0], s, cudaEventRecordExternal);
         enqueue_down(h, l, fz[l], F(l), uz ? nullptr : U(l), fz[l] ? T : U(l), h->lv[l + 1].f, uc, s, &n);
         if (rec && l == 0)
             cudaEventRecordWithFlags(rec[1], s, cudaEventRecordExternal);
+        if (seg)
+            cudaEventRecordWithFlags(seg[l + 1], s, cudaEventRecordExternal);
     }
+    if (seg && lt == 0)
+        cudaEventRecordWithFlags(seg[0], s, cudaEventRecordExternal);
     // no level-0 down leg of its own (the tail or the coarse solve starts at level 0):
     // bmg_timing records around that launch instead
     const bool rec_here = rec && lt == 0;
@@ -471,8 +478,13 @@ static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream
     }
     if (rec_here)
         cudaEventRecordWithFlags(rec[1], s, cudaEventRecordExternal);
-    for (int l = lt - 1; l >= 0; l--)
+    if (seg)
+        cudaEventRecordWithFlags(seg[lt + 1], s, cudaEventRecordExternal);
+    for (int l = lt - 1; l >= 0; l--) {
         enqueue_up(h, l, fz[l], F(l), fz[l] ? h->fplan.tmp[l] : U(l), h->lv[l + 1].u, U(l), s, &n);
+        if (seg)
+            cudaEventRecordWithFlags(seg[lt + 2 + (lt - 1 - l)], s, cudaEventRecordExternal);
+    }
     return n;
 }
 
@@ -638,6 +650,58 @@ bmg_status_t bmg_timing_read(bmg_solver_t h, double *ms_total, int *launches)
     *ms_total = tot;
     *launches = (int)(h->tev_used / 2);
     h->tev_used = 0;
+    return BMG_OK;
+}
+
+bmg_status_t bmg_profile_legs(bmg_solver_t h, const double *rhs, double *x, int ncycles, double *ms_out, int cap,
+                              int *nseg, void *cuda_stream)
+{
+    if (!h || h->dist || !rhs || !x || !ms_out || !nseg || ncycles < 1 || cap < 2 * h->L + 1)
+        return fail(BMG_EINVAL, "bmg_profile_legs: bad arguments");
+    const int lt = h->tail_l0 < h->L ? h->tail_l0 : h->L - 1;
+    const int ne = 2 * lt + 2;
+    std::vector<cudaEvent_t> ev(ne);
+    for (auto &e : ev)
+        CK(cudaEventCreate(&e));
+    auto cleanup = [&]() {
+        for (auto &e : ev)
+            cudaEventDestroy(e);
+    };
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+    h->cycle_err = false;
+    enqueue_cycle(h, rhs, x, h->cap, nullptr, ev.data());
+    cudaError_t e = cudaStreamEndCapture(h->cap, &g);
+    if (e != cudaSuccess || h->cycle_err) {
+        cleanup();
+        return fail(BMG_ECUDA, "bmg_profile_legs: capture failed");
+    }
+    cudaGraphExec_t ex;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+        cleanup();
+        return fail(BMG_ECUDA, std::string("bmg_profile_legs: ") + cudaGetErrorString(e));
+    }
+    std::vector<double> acc(ne - 1, 0.0);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    for (int c = 0; c < ncycles && e == cudaSuccess; c++) {
+        e = cudaGraphLaunch(ex, s);
+        if (e == cudaSuccess)
+            e = cudaStreamSynchronize(s);
+        for (int k = 0; k + 1 < ne && e == cudaSuccess; k++) {
+            float ms = 0.f;
+            e = cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+            acc[k] += ms;
+        }
+    }
+    cudaGraphExecDestroy(ex);
+    cleanup();
+    if (e != cudaSuccess)
+        return fail(BMG_ECUDA, std::string("bmg_profile_legs: ") + cudaGetErrorString(e));
+    for (int k = 0; k + 1 < ne; k++)
+        ms_out[k] = acc[k] / ncycles;
+    *nseg = ne - 1;
     return BMG_OK;
 }
 

@@ -584,7 +584,12 @@ bmg_status_t dist_setup(const bmg_stencil_t *st, const bmg_comm_t *cm, const bmg
         sk.pitch = d->pitchK;
         for (int k = 0; k < 5; k++)
             sk.plane[k] = d->plK + k * npk;
-        bmg_status_t rc = bmg_setup(&sk, &d->prm, s, &d->inner);
+        // the inner solver continues the SAME ladder from level K: partition() already
+        // counted max_levels from level 0, so the inner hierarchy gets what is left
+        bmg_params_t pin = d->prm;
+        if (pin.max_levels > 0)
+            pin.max_levels -= K;
+        bmg_status_t rc = bmg_setup(&sk, &pin, s, &d->inner);
         if (rc != BMG_OK) {
             err = std::string("inner solver setup: ") + bmg_last_error_detail();
             return fail(rc);

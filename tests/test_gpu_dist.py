@@ -59,6 +59,29 @@ def test_loopback_bitwise_vcycle(wl, n, nranks, agg):
     single.close()
 
 
+@pytest.mark.parametrize("max_levels", [5, 6, 7])
+def test_loopback_max_levels(max_levels):
+    """A truncated hierarchy (max_levels) has the same levels distributed or not: the
+    replicated inner solver gets max_levels - K (K distributed levels), so the level
+    count and the iterate match the single-GPU solver bitwise."""
+    n = 511
+    st = P.workload("checker", n, n)
+    prm = bmg.bmg_params_default()
+    prm.agglom_rows, prm.max_levels = 16, max_levels
+    single = bmg.Solver(st, prm)
+    h = loopback(st, 2, prm, single.pitch)
+    assert bmg.bmg_num_levels(h) == single.L == max_levels
+    f = single.grid(P.field_uniform(n, n, seed=53))
+    x0 = P.field_uniform(n, n, seed=54)
+    xs, xd = single.grid(x0), single.grid(x0)
+    single.vcycle(f, xs, 2)
+    bmg.bmg_vcycle(h, f, xd, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(xs, xd), float((xs - xd).abs().max())
+    bmg.bmg_destroy(h)
+    single.close()
+
+
 @pytest.mark.parametrize("wl,n,nranks,agg", [("poisson", 511, 3, 16), ("checker", 511, 2, 64)])
 def test_loopback_solve(wl, n, nranks, agg):
     st = P.workload(wl, n, n)

@@ -51,9 +51,11 @@ def assert_operator_close(gpu_planes, orc_st9, kind, exact=False):
 
 
 def assert_iterate_close(g, o, rtol=1e-12):
-    tol = rtol * np.maximum(np.abs(o), np.abs(o).max())
+    """NORMWISE per-component check: every component's error <= rtol * max|o| (the
+    iterate's scale; DESIGN §7 -- a pure per-element relative test is ill-posed where
+    the iterate crosses zero).  It is NOT an element-relative bound."""
     err = np.abs(g - o)
-    assert np.all(err <= tol), (err.max(), (err / np.maximum(np.abs(o), 1e-300)).max())
+    assert err.max() <= rtol * np.abs(o).max(), (err.max(), np.abs(o).max())
 
 
 CASES = [("poisson", 31, 31), ("lognormal", 63, 63), ("checker", 127, 127), ("aniso", 63, 63), ("random9", 33, 33),
@@ -312,18 +314,25 @@ def test_up_leg_sym_parity(orc, wl, nx, ny, nu2, fused):
 def test_random_shapes_vcycle_parity(orc):
     """Seeded sweep over shapes the fixed cases miss (odd/even, thin rectangles, sizes
     straddling the fused / tail / per-step thresholds and the strip width): one fused
-    V(2,1) cycle against the oracle at the DESIGN §7 tolerance.  The anisotropic operator
-    is left to the fixed cases: on tall rectangles its cond(A) ~ 1e5, and the
-    residual's inherent cancellation (ε·|A||u|, different on the two sides) is
-    amplified by the coarse correction to a few 1e-12 of max|x| (measured 2.8e-12 at
-    190x417) -- rounding, not a defect."""
+    V(2,1) cycle against the oracle, every operator including the anisotropic one, at
+    the DESIGN §7 rule.  Each case is also run through the oracle's extended-precision
+    build: where the fp64 oracle is within 1e-13 of that iterate, the GPU must match the
+    oracle to 1e-12 (normwise); where fp64 itself is less accurate (anisotropic, and
+    lognormal on some shapes: up to ~8e-12 of max|x|, tests/test_oracle_extended.py),
+    the GPU must be at most twice as far from the extended iterate as the oracle is."""
+    from oracle import extended
+
     rng = np.random.default_rng(2025)
-    for _ in range(16):
-        nx, ny = (int(v) for v in rng.integers(4, 420, size=2))
-        wl = ["lognormal", "random9", "checker_off3", "poisson"][int(rng.integers(0, 4))]
+    shapes = [(190, 417)] + [tuple(int(v) for v in rng.integers(4, 420, size=2)) for _ in range(19)]
+    n_ext = 0
+    for k, (nx, ny) in enumerate(shapes):
+        wl = "aniso" if k == 0 else ["lognormal", "random9", "checker_off3", "poisson", "aniso"][int(rng.integers(0, 5))]
         st = P.workload(wl, nx, ny)
+        try:
+            h = orc.Hierarchy(st)
+        except ValueError:  # EINVAL (reading c3 (iii)); the library agrees (test_den_nonpositive_rejected_like_oracle)
+            continue
         s = bmg.Solver(st)
-        h = orc.Hierarchy(st)
         f = P.field_uniform(nx, ny, seed=int(rng.integers(1 << 30)))
         x0 = P.field_uniform(nx, ny, seed=int(rng.integers(1 << 30)))
         x = s.grid(x0)
@@ -331,9 +340,16 @@ def test_random_shapes_vcycle_parity(orc):
         torch.cuda.synchronize()
         ref = h.vcycle(f, x0, 1)
         got = bmg.from_device(x, nx)
-        tol = 1e-12 * np.maximum(np.abs(ref), np.abs(ref).max())
-        assert np.all(np.abs(got - ref) <= tol), (wl, nx, ny, np.abs(got - ref).max())
         s.close()
+        e = extended.HierarchyExt(st).vcycle(f, x0, 1).astype(np.float64)
+        scale = np.abs(e).max()
+        dg, do = np.abs(got - e).max() / scale, np.abs(ref - e).max() / scale
+        if do <= 1e-13:
+            assert_iterate_close(got, ref)
+        else:
+            n_ext += 1
+            assert dg <= 2 * do, (wl, nx, ny, dg, do)
+    assert n_ext >= 2  # the sweep does exercise the ill-conditioned cases
 
 
 @pytest.mark.parametrize("nu1,nu2,coarsest,max_levels", [(1, 1, 3, 0), (2, 2, 3, 0), (0, 1, 3, 0), (1, 0, 3, 0),
