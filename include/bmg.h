@@ -157,7 +157,9 @@ bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol,
  * maxiter (x, hist valid).  The host waits once per iteration (for ||r_k||);
  * alpha and beta are formed on the device.  On return x and hist are final;
  * the next iteration's preconditioner, enqueued speculatively before the last
- * wait, may still be running on cuda_stream (it writes only the workspace).
+ * wait (never after the maxiter-th iteration), may still be running on
+ * cuda_stream: it writes the PCG workspace AND the handle's hierarchy arrays,
+ * so every later call on this handle (any stream) first waits for it.
  */
 bmg_status_t bmg_pcg(bmg_solver_t h, const double *rhs, double *x, double tol, int maxiter, int *iters_out,
                      double *hist_host, void *cuda_stream);

@@ -87,6 +87,8 @@ bmg_status_t bmg_destroy(bmg_solver_t h)
             cudaEventDestroy(e);
     if (h->pcg_ev)
         cudaEventDestroy(h->pcg_ev);
+    if (h->pcg_tail)
+        cudaEventDestroy(h->pcg_tail);
     for (auto &kv : h->sgraphs)
         cudaGraphExecDestroy(kv.second);
     if (h->solve_hist)
@@ -166,7 +168,12 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
         if (pass == 1) {
             TRY(dalloc(h, &arena, used));
             setup_trace("cudaMalloc", s);
-            CK(cudaMemsetAsync(arena, 0, used * sizeof(double), s));
+            // zero everything but the level-0 planes (the arena's first block: S0 ingest
+            // writes every element of it, ring and padding included)
+            const Level &v0 = h->lv[0];
+            const size_t np0 = (size_t)(v0.ny + 2) * (size_t)v0.pitch * (v0.kind == 9 ? 5 : 3);
+            const size_t skip = (np0 + 31) / 32 * 32;
+            CK(cudaMemsetAsync(arena + skip, 0, (used - skip) * sizeof(double), s));
             setup_trace("memset", s);
             used = 0;
         }
@@ -302,10 +309,8 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
         }
         // the ping-pong partner T is the level's residual array: a fused level never
         // stores r (its down leg restricts from shared memory), and T lives only
-        // within one cycle; its ring must be 0
-        size_t np = (size_t)(v.ny + 2) * (size_t)v.pitch;
+        // within one cycle; its ring must be 0 (the arena is zeroed, nothing wrote r yet)
         h->fplan.tmp[l] = v.r;
-        CK(cudaMemsetAsync(v.r, 0, np * sizeof(double), s));
     }
     CK(cudaStreamSynchronize(s));
     setup_trace("lines/tail/fused", s);
@@ -604,6 +609,7 @@ extern "C" {
 
 bmg_status_t bmg_vcycle(bmg_solver_t h, const double *rhs, double *x, int ncycles, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     if (!h || !rhs || !x || ncycles < 0)
         return fail(BMG_EINVAL, "bad arguments to bmg_vcycle");
     if (h->dist) {
@@ -656,6 +662,7 @@ bmg_status_t bmg_timing_read(bmg_solver_t h, double *ms_total, int *launches)
 bmg_status_t bmg_profile_legs(bmg_solver_t h, const double *rhs, double *x, int ncycles, double *ms_out, int cap,
                               int *nseg, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     if (!h || h->dist || !rhs || !x || !ms_out || !nseg || ncycles < 1 || cap < 2 * h->L + 1)
         return fail(BMG_EINVAL, "bmg_profile_legs: bad arguments");
     const int lt = h->tail_l0 < h->L ? h->tail_l0 : h->L - 1;
@@ -707,6 +714,7 @@ bmg_status_t bmg_profile_legs(bmg_solver_t h, const double *rhs, double *x, int 
 
 bmg_status_t bmg_vcycle_host(bmg_solver_t h, const double *rhs_host, double *x_host, int ncycles, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     if (!h || !rhs_host || !x_host || ncycles < 0 || h->dist)
         return fail(BMG_EINVAL, "bad arguments to bmg_vcycle_host (not for distributed handles)");
     Level &v = h->lv[0];
@@ -727,6 +735,7 @@ bmg_status_t bmg_vcycle_host(bmg_solver_t h, const double *rhs_host, double *x_h
 bmg_status_t bmg_residual_norm(bmg_solver_t h, const double *rhs, const double *x, double *r_out, double *norm_host,
                                void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     if (!h || !rhs || !x || !norm_host || (h->dist && r_out))
         return fail(BMG_EINVAL, "bad arguments to bmg_residual_norm");
     cudaStream_t s = (cudaStream_t)cuda_stream;
@@ -746,6 +755,7 @@ bmg_status_t bmg_residual_norm(bmg_solver_t h, const double *rhs, const double *
 bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol, int maxiter, int *iters_out,
                        double *hist_host, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     if (!h || !rhs || !x || maxiter < 0 || !(tol >= 0))
         return fail(BMG_EINVAL, "bad arguments to bmg_solve");
     cudaStream_t s = (cudaStream_t)cuda_stream;
@@ -845,6 +855,7 @@ bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol,
 bmg_status_t bmg_pcg(bmg_solver_t h, const double *rhs, double *x, double tol, int maxiter, int *iters_out,
                      double *hist_host, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     if (!h || !rhs || !x || maxiter < 0 || !(tol >= 0))
         return fail(BMG_EINVAL, "bad arguments to bmg_pcg");
     if (h->dist)
@@ -861,6 +872,7 @@ bmg_status_t bmg_pcg(bmg_solver_t h, const double *rhs, double *x, double tol, i
         TRY(dalloc(h, &h->pcg_ws, 4 * np + 32));
         CK(cudaMemsetAsync(h->pcg_ws, 0, (4 * np + 32) * sizeof(double), s));
         CK(cudaEventCreateWithFlags(&h->pcg_ev, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->pcg_tail, cudaEventDisableTiming));
     }
     double *r = h->pcg_ws, *z = r + np, *p = z + np, *q = p + np, *sc = q + np;
     enum { PQ = 1, RN = 2 };  // sc slots; rho alternates between slots 0 and 3
@@ -896,18 +908,27 @@ bmg_status_t bmg_pcg(bmg_solver_t h, const double *rhs, double *x, double tol, i
             k++;
             CK(cudaMemcpyAsync(h->h_norm, sc + RN, sizeof(double), cudaMemcpyDeviceToHost, s));
             CK(cudaEventRecord(h->pcg_ev, s));
-            // the next direction, speculatively (z, p and sc only; x and r are final)
+            // the next direction, speculatively (z, p and sc only; x and r are final),
+            // unless this was the last allowed iteration
             const int nxt = 3 - cur;
-            TRY(precondition());
-            launch_dot(A, r, z, h->partials, sc + nxt, s);
-            launch_cg_direction(A, sc, nxt, cur, z, p, s);  // beta = rho' / rho
+            const bool spec = k < maxiter;
+            if (spec) {
+                TRY(precondition());
+                launch_dot(A, r, z, h->partials, sc + nxt, s);
+                launch_cg_direction(A, sc, nxt, cur, z, p, s);  // beta = rho' / rho
+            }
             CK(cudaGetLastError());
             CK(cudaEventSynchronize(h->pcg_ev));
             rn = h->h_norm[0];
             if (hist_host)
                 hist_host[k] = rn;
-            if (rn <= tol * fn)
+            if (rn <= tol * fn) {
+                if (spec) {  // left queued: later calls on any stream join it (join_pcg)
+                    CK(cudaEventRecord(h->pcg_tail, s));
+                    h->pcg_pending = true;
+                }
                 break;
+            }
             cur = nxt;
         }
     }
@@ -971,7 +992,16 @@ bmg_status_t bmg_cycle_kernel_count(bmg_solver_t h, int *count)
     if (h->kernels_per_cycle == 0) {  // count by a dry capture
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
-        int n = enqueue_cycle(h, h->lv[0].r, h->lv[0].r, h->cap);
+        // dry capture on two distinct, 16-byte-aligned level-0 arrays that are not the
+        // fused ping-pong partner (T = lv[0].r), so the count is that of the cycle
+        // bmg_vcycle runs on caller arrays
+        Level &v0 = h->lv[0];
+        const size_t nb = (size_t)(v0.ny + 2) * v0.pitch;
+        if (!h->stage_f) {
+            TRY(dalloc(h, &h->stage_f, nb));
+            TRY(dalloc(h, &h->stage_x, nb));
+        }
+        int n = enqueue_cycle(h, h->stage_f, h->stage_x, h->cap);
         CK(cudaStreamEndCapture(h->cap, &g));
         cudaGraphDestroy(g);
         h->kernels_per_cycle = n;
@@ -1015,6 +1045,7 @@ static bmg_status_t check_level(bmg_solver_t h, int level, bool need_coarse)
 
 bmg_status_t bmg_relax(bmg_solver_t h, int level, const double *f, double *u, int nsweeps, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     TRY(check_level(h, level, false));
     relax_level(h, level, f, u, nsweeps, (cudaStream_t)cuda_stream, nullptr);
     CK(cudaGetLastError());
@@ -1023,6 +1054,7 @@ bmg_status_t bmg_relax(bmg_solver_t h, int level, const double *f, double *u, in
 
 bmg_status_t bmg_residual(bmg_solver_t h, int level, const double *f, const double *u, double *r, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     TRY(check_level(h, level, false));
     launch_residual(h->lv[level].op(), f, u, r, (cudaStream_t)cuda_stream);
     CK(cudaGetLastError());
@@ -1031,6 +1063,7 @@ bmg_status_t bmg_residual(bmg_solver_t h, int level, const double *f, const doub
 
 bmg_status_t bmg_restrict(bmg_solver_t h, int level, const double *r, double *fc, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     TRY(check_level(h, level, true));
     launch_restrict(h->lv[level].op(), h->civ(level), r, fc, nullptr, (cudaStream_t)cuda_stream);
     CK(cudaGetLastError());
@@ -1039,6 +1072,7 @@ bmg_status_t bmg_restrict(bmg_solver_t h, int level, const double *r, double *fc
 
 bmg_status_t bmg_interp_add(bmg_solver_t h, int level, const double *ec, double *u, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     TRY(check_level(h, level, true));
     launch_interp_add(h->lv[level].op(), h->civ(level), ec, u, (cudaStream_t)cuda_stream);
     CK(cudaGetLastError());
@@ -1048,6 +1082,7 @@ bmg_status_t bmg_interp_add(bmg_solver_t h, int level, const double *ec, double 
 bmg_status_t bmg_smooth_restrict(bmg_solver_t h, int level, const double *f, const double *u_in, double *u_out,
                                  double *fc, double *uc, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     TRY(check_level(h, level, true));
     if (!f || !u_in || !u_out || !fc || u_in == u_out)
         return fail(BMG_EINVAL, "bmg_smooth_restrict: null pointer or u_in == u_out");
@@ -1061,6 +1096,7 @@ bmg_status_t bmg_smooth_restrict(bmg_solver_t h, int level, const double *f, con
 bmg_status_t bmg_correct_smooth(bmg_solver_t h, int level, const double *f, const double *u_in, const double *ec,
                                 double *u_out, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     TRY(check_level(h, level, true));
     if (!f || !u_in || !u_out || !ec || u_in == u_out)
         return fail(BMG_EINVAL, "bmg_correct_smooth: null pointer or u_in == u_out");

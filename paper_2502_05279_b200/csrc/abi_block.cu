@@ -126,6 +126,7 @@ extern "C" {
 
 bmg_status_t bmg_vcycle_block(bmg_solver_t h, int nrhs, const double *rhs, double *x, int ncycles, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     TRY(block_args(h, nrhs, rhs, x, "bmg_vcycle_block"));
     if (ncycles < 0)
         return fail(BMG_EINVAL, "bmg_vcycle_block: ncycles < 0");
@@ -160,6 +161,7 @@ bmg_status_t bmg_vcycle_block(bmg_solver_t h, int nrhs, const double *rhs, doubl
 bmg_status_t bmg_residual_norm_block(bmg_solver_t h, int nrhs, const double *rhs, const double *x,
                                      double *norms_host, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     TRY(block_args(h, nrhs, rhs, x, "bmg_residual_norm_block"));
     if (!norms_host)
         return fail(BMG_EINVAL, "bmg_residual_norm_block: null norms_host");
@@ -171,6 +173,7 @@ bmg_status_t bmg_residual_norm_block(bmg_solver_t h, int nrhs, const double *rhs
 bmg_status_t bmg_solve_block(bmg_solver_t h, int nrhs, const double *rhs, double *x, double tol, int maxiter,
                              int *iters_out, double *hist_host, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     TRY(block_args(h, nrhs, rhs, x, "bmg_solve_block"));
     if (maxiter < 0 || !(tol >= 0))
         return fail(BMG_EINVAL, "bad arguments to bmg_solve_block");
@@ -279,6 +282,7 @@ bmg_status_t bmg_solve_block(bmg_solver_t h, int nrhs, const double *rhs, double
 bmg_status_t bmg_pcg_block(bmg_solver_t h, int nrhs, const double *rhs, double *x, double tol, int maxiter,
                            int *iters_out, double *hist_host, void *cuda_stream)
 {
+    join_pcg(h, (cudaStream_t)cuda_stream);
     TRY(block_args(h, nrhs, rhs, x, "bmg_pcg_block"));
     if (maxiter < 0 || !(tol >= 0))
         return fail(BMG_EINVAL, "bad arguments to bmg_pcg_block");

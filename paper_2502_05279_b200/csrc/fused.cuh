@@ -4,11 +4,13 @@
 // Down leg of a level in ONE pass over HBM: nu1 multicolour GS sweeps +
 // residual + restriction (+ zeroing the coarse correction).  Up leg in ONE
 // pass: interpolation + correction + nu2 sweeps.  Each CTA owns a strip of
-// TX output columns and a chunk of rows and streams the rows bottom-up
-// through a ring of shared-memory rows filled by 1-D TMA bulk copies
-// (cp.async.bulk + mbarrier); colour stages run 2 rows apart so one barrier
-// per row step orders them.  u is ping-ponged (u_in -> u_out) because
-// neighbouring CTAs read each other's halo rows/columns.
+// TX output columns and a chunk of rows and streams the rows bottom-up:
+// tensor-map TMA boxes (u, f, one 3-D box of the operator's plane block, the
+// weight planes) land in a staging ring; warp-specialised task groups (split,
+// colour stages 2 rows apart, residual, restriction, store) each wait on ONE
+// mbarrier ring per row step (their producers' step completions).  u is
+// ping-ponged (u_in -> u_out) because neighbouring CTAs read each other's halo
+// rows/columns.
 #pragma once
 #include "bmg.h"
 #include "bmg_internal.cuh"
@@ -27,7 +29,6 @@ struct FusedGeom {
     int threads = 0;
     size_t smem = 0;
     bool ok = false;
-    bool wave = false;  // 5-point down leg: the register-wavefront kernel (k_wave_down5)
     bool rev = false;   // up leg: colours in reverse order (cycle_sym, c12)
 };
 

@@ -36,6 +36,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <mutex>
 #include <type_traits>
 
 #include "fused.cuh"
@@ -60,8 +61,33 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, uint32_t bytes)
 #ifndef BMG_WAIT_HINT
 #define BMG_WAIT_HINT 0x989680
 #endif
+// BMG_WAIT_NS > 0: poll with mbarrier.test_wait and back off BMG_WAIT_NS ns between
+// probes (fewer issue slots spent by waiting warps) instead of the try_wait loop.
+#ifndef BMG_WAIT_NS
+#define BMG_WAIT_NS 0
+#endif
+__device__ __forceinline__ bool mbar_test(uint32_t addr, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity)
 {
+    if (BMG_WAIT_NS > 0) {
+        while (!mbar_test(smem_u32(b), parity))
+            __nanosleep(BMG_WAIT_NS);
+        return;
+    }
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
@@ -198,6 +224,11 @@ struct Rings {
         if (t < lo)
             return;
         const uint32_t par = ((t - lo) / NSLOT) & 1;
+        if (BMG_WAIT_NS > 0) {
+            while (!mbar_test(at(r, t), par))
+                __nanosleep(BMG_WAIT_NS);
+            return;
+        }
         asm volatile(
             "{\n"
             ".reg .pred P1;\n"
@@ -636,37 +667,18 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
     }
     int tm = 0, tsd = 0;  // main / staging ring slots of row t
     for (int t = lo; t <= tend; t++, tm = (tm + 1 == RM) ? 0 : tm + 1, tsd = (tsd + 1 == SD) ? 0 : tsd + 1) {
-// Timing experiments only (tools_variants.py -D...): drop one task's work to find
-// the pipeline's bottleneck; results are wrong when any is set.
-#ifndef BMG_X_NOSPLIT
-#define BMG_X_NOSPLIT 0
-#endif
-#ifndef BMG_X_NOSTAGE
-#define BMG_X_NOSTAGE 0
-#endif
-#ifndef BMG_X_NORES
-#define BMG_X_NORES 0
-#endif
-#ifndef BMG_X_NORESTR
-#define BMG_X_NORESTR 0
-#endif
-#ifndef BMG_X_NOSTORE
-#define BMG_X_NOSTORE 0
-#endif
         if (grp >= G_SPLIT) {
             rg.wait(R_SPLIT, t - 1 - E);
             if (t <= hi) {
                 mbar_wait(&bar[tsd], ((t - lo) / SD) & 1);
-                if (BMG_X_NOSPLIT) {
-                } else if (grp == G_SPLIT)
+                if (grp == G_SPLIT)
                     split_row<NA, AM, WD, PPT, NPG, false>(sm, smS, tsd, tm, 0, QSPLIT, m);
                 else
                     split_row<NA, AM, WD, PPT, NPG, true>(sm, smS, tsd, tm, QSPLIT, NA, m);
             }
         } else if (grp < NSG) {
             rg.wait(grp, t - 1);
-            if (BMG_X_NOSTAGE) {
-            } else if (KIND == 5) {
+            if (KIND == 5) {
                 const int k = grp + 1, d = 2 * k, r = t - d;
                 if (r > lo && r < hi && r >= 1 && r <= ny)
                     colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1),
@@ -687,328 +699,19 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
         } else if (grp < G_STORE) {
             rg.wait(R_RES, t - 1);
             const int d = 2 * NS + 2;
-            if (!BMG_X_NORES)
-                resid_task(t - d, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), grp - G_RES);
+            resid_task(t - d, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), grp - G_RES);
         } else if (grp == G_STORE) {
             rg.wait(R_STORE, t - 3);
-            if (!BMG_X_NOSTORE)
-                store_task(t - 2 * NS - 3, back<RM>(tm, 2 * NS + 3));
+            store_task(t - 2 * NS - 3, back<RM>(tm, 2 * NS + 3));
         } else {
             rg.wait(R_RESTR, t - 1);
             const int jr = t - 2 * NS - 4;
             const int J = jr >> 1;
-            if (!BMG_X_NORESTR && jr >= 0 && !(jr & 1) && J >= Jlo && J <= Jhi)
+            if (jr >= 0 && !(jr & 1) && J >= Jlo && J <= Jhi)
                 restrict_task(J);
         }
         rg.done(t, a0, a1, a2);
     }
-}
-
-// ------------------------------------------------------------------ register wavefront
-// 5-point down leg without the shared-memory main ring (off by default): a warp
-// owns a 64-column window (lane h: the column pair 2h, 2h+1) and marches up the
-// rows keeping the last NS+3 rows of u and NS+2 rows of coefficients in
-// REGISTERS.  Step t: the row t arrives (TMA staging ring, natural layout, read
-// once per lane as double2 pairs); colour stage k = 1..NS updates row t-k (lag
-// ONE row per stage: the stages run in program order inside the thread, so the
-// wavefront needs no inter-warp ordering); the residual of row t-NS-1 (its
-// red points -- the black residual vanishes, c5a) and, every other row, the
-// restriction of a coarse row; the store of row t-NS.  Horizontal neighbours
-// come from the adjacent lanes by shuffles; a warp's window overlaps its
-// neighbours' by H = 6 columns on each side (the domain of dependence of NS = 4
-// colour passes + residual + restriction), so warps never synchronise with each
-// other -- only with the TMA producer, through the staging ring's full/empty
-// mbarriers.  Per-point arithmetic and operand order are those of the per-step
-// kernels (relax5_pt, residual_pt, restrict_pt_vanish): the iterate is bitwise
-// the same.
-constexpr int WV_WARPS = 4;                      // warps per CTA
-constexpr int WV_H = 6;                          // window halo (columns)
-constexpr int WV_OUT = 64 - 2 * WV_H;            // output columns per warp (52)
-constexpr int WV_TX = WV_WARPS * WV_OUT;         // output columns per CTA (208)
-constexpr int WV_W = WV_TX + 2 * WV_H;           // staged columns per row (220)
-// staging slot: [u | f | O W S] -- the TMA destinations (u, f, the plane box) start
-// on 128-byte boundaries; the plane box lands O, W, S back to back (stride WV_W)
-constexpr int WV_WP = (WV_W + 15) / 16 * 16;               // 224
-constexpr int WV_SS = 2 * WV_WP + (3 * WV_W + 15) / 16 * 16;  // doubles per slot
-constexpr int WV_OF = WV_WP, WV_OO = 2 * WV_WP, WV_OW = WV_OO + WV_W, WV_OS = WV_OO + 2 * WV_W;
-#ifndef BMG_WAVE5
-#define BMG_WAVE5 0  // 1: 5-point down legs by the register wavefront (measured slower)
-#endif
-#ifndef BMG_WV_D
-#define BMG_WV_D 8
-#endif
-constexpr int WV_D = BMG_WV_D;                   // TMA prefetch depth (rows)
-constexpr int WV_SD = WV_D + 1;                  // staging slots
-constexpr size_t WV_SMEM = (size_t)WV_SD * WV_SS * 8 + 2 * WV_SD * 8;
-
-// A row's values at the lane's column pair, stored by COLOUR (5-point red-black,
-// c6): .x = the red member (the pair's column with (c + row) even), .y = the
-// black one.  Stage k then always touches member (k-1)&1, and the vertical
-// neighbours of a point are the other colour's member of rows row±1 -- all
-// compile-time; only the horizontal neighbour's lane (left or right, by the row's
-// parity) is chosen at run time, with one shuffle.
-struct WvCo {
-    double2 O, o, W, S, f;  // by colour
-    double2 E;              // east coupling W(c+1) of the red / black member
-};
-
-// Register windows, indexed by AGE k (row t-k): the physical slot of age k at a
-// step of phase ph = (t - lo) mod 7 is (ph - k) mod 7.  The step loop is unrolled
-// by 7 so that every index is a compile-time constant and the window "shift" is a
-// renaming, not register moves.
-struct WvState {
-    double2 Up[7];                   // u by colour
-    WvCo Cp[7];
-    double Rp[7];                    // red residual by age (of its row t-NS-1)
-    double wNE, wNW, wSE, wSW;       // weights of the next coarse row restricted
-};
-
-struct WvCtx {
-    const FArgs *a;
-    const TMaps *tm;
-    double *sm;
-    uint64_t *full, *empty;
-    int nx, ny, lo, hi, ya, yb, Jlo, Jhi, xl, lane, lc0, c0, I;
-    long long P, CP;
-    bool out_lane, in0, in1, out_coarse;
-};
-
-__device__ __forceinline__ void wv_issue_row(const WvCtx &x, int row)
-{
-    const int slot = (row - x.lo) % WV_SD;
-    mbar_arrive_tx(&x.full[slot], (uint32_t)(5 * WV_W * 8));
-    double *d = x.sm + slot * WV_SS;
-    tma_2d(d, &x.tm->u, x.xl, row - x.a->A.roff, &x.full[slot]);
-    tma_2d(d + WV_OF, &x.tm->f, x.xl, row - x.a->A.roff, &x.full[slot]);
-    tma_3d(d + WV_OO, &x.tm->a, x.xl, row - x.a->A.roff, 0, &x.full[slot]);
-}
-
-__device__ __forceinline__ double2 by_colour(double2 v, bool odd_row)
-{
-    return odd_row ? make_double2(v.y, v.x) : v;  // red member first
-}
-
-// One row step t (phase ph = (t - lo) mod 7).
-template <int NS, int ph>
-__device__ __forceinline__ void wv_step(WvState &S, const WvCtx &x, int t)
-{
-    const unsigned FULLM = 0xffffffffu;
-    const double2 z2 = make_double2(0.0, 0.0);
-    const int lane = x.lane;
-#define WU(k) S.Up[(ph - (k) + 14) % 7]
-#define WC(k) S.Cp[(ph - (k) + 14) % 7]
-#define WR(k) S.Rp[(ph - (k) + 14) % 7]
-    // ---- row t: staging ring -> registers (the split of the shared-memory kernel)
-    if (t <= x.hi) {
-        const int slot = (t - x.lo) % WV_SD;
-        mbar_wait(&x.full[slot], ((t - x.lo) / WV_SD) & 1);
-        const double *row = x.sm + slot * WV_SS + x.lc0;
-        const double2 u = *reinterpret_cast<const double2 *>(row);
-        const double2 f = *reinterpret_cast<const double2 *>(row + WV_OF);
-        const double2 O = *reinterpret_cast<const double2 *>(row + WV_OO);
-        const double2 W = *reinterpret_cast<const double2 *>(row + WV_OW);
-        const double2 Sv = *reinterpret_cast<const double2 *>(row + WV_OS);
-        __syncwarp();
-        if (lane == 0)
-            mbar_arrive(&x.empty[slot]);
-        // producer (thread 0): row t + D into the slot row t - 1 used
-        if (threadIdx.x == 0 && t + WV_D <= x.hi) {
-            const int q = t + WV_D - x.lo;
-            if (q >= WV_SD)
-                mbar_wait(&x.empty[q % WV_SD], ((q / WV_SD) - 1) & 1);
-            wv_issue_row(x, t + WV_D);
-        }
-        const bool od = t & 1;
-        const double Wnext = __shfl_down_sync(FULLM, W.x, 1);  // W(c0+2)
-        WU(0) = by_colour(u, od);
-        WC(0).f = by_colour(f, od);
-        WC(0).O = by_colour(O, od);
-        WC(0).W = by_colour(W, od);
-        WC(0).S = by_colour(Sv, od);
-        // east couplings: even member's E = W(c0+1), odd member's E = W(c0+2)
-        WC(0).E = by_colour(make_double2(W.y, Wnext), od);
-        WC(0).o = make_double2(rcp_pos(WC(0).O.x), rcp_pos(WC(0).O.y));
-    } else {
-        WU(0) = z2;
-        WC(0) = WvCo{z2, z2, z2, z2, z2, z2};
-    }
-    // ---- colour stages: stage k on row t-k, colour cl = (k-1)&1 (c6)
-#pragma unroll
-    for (int k = 1; k <= NS; k++) {
-        const int r = t - k;
-        constexpr int dummy = 0;
-        (void)dummy;
-        const bool od = r & 1;
-        const int cl = (k - 1) & 1;  // compile-time after unrolling
-        // the updated point is the even column iff (cl ^ od) == 0; its horizontal
-        // neighbours (other colour, same row): own other member and the other
-        // member of the lane on the far side (left if the point is the even column)
-        const double own = cl ? WU(k).x : WU(k).y;
-        const double nb = __shfl_sync(FULLM, own, (cl ^ od) ? lane + 1 : lane - 1);
-        const bool even = !(cl ^ od);
-        const double ul = even ? nb : own, ur = even ? own : nb;
-        const double ud = cl ? WU(k + 1).x : WU(k + 1).y;  // rows r-1, r+1: other colour
-        const double uu = cl ? WU(k - 1).x : WU(k - 1).y;
-        const double Sc = cl ? WC(k).S.y : WC(k).S.x;
-        const double Nc = cl ? WC(k - 1).S.x : WC(k - 1).S.y;
-        const double Wc = cl ? WC(k).W.y : WC(k).W.x, Ec = cl ? WC(k).E.y : WC(k).E.x;
-        const double fv = cl ? WC(k).f.y : WC(k).f.x, ov = cl ? WC(k).o.y : WC(k).o.x;
-        double acc = Sc * ud;
-        acc += Wc * ul;
-        acc += Ec * ur;
-        acc += Nc * uu;
-        const double v = (fv - acc) * ov;
-        if (r > x.lo && r < x.hi && r >= 1 && r <= x.ny && (even ? x.in0 : x.in1)) {
-            if (cl)
-                WU(k).y = v;
-            else
-                WU(k).x = v;
-        }
-    }
-    // ---- residual of row rr = t-NS-1 at its red point (black: vanishing, c5a)
-    {
-        constexpr int K = NS + 1;
-        const int rr = t - K;
-        const bool od = rr & 1;  // red point = odd column
-        const double own = WU(K).y;  // the black member
-        const double nb = __shfl_sync(FULLM, own, od ? lane + 1 : lane - 1);
-        const double ul = od ? own : nb, ur = od ? nb : own;
-        const double ud = WU(K + 1).y, uu = WU(K - 1).y, uc = WU(K).x;
-        const double Sc = WC(K).S.x, Nc = WC(K - 1).S.y;
-        const double Wc = WC(K).W.x, Ec = WC(K).E.x;
-        const double fv = WC(K).f.x, Ov = WC(K).O.x;
-        double acc = Sc * ud;
-        acc += Wc * ul;
-        acc += Ec * ur;
-        acc += Nc * uu;
-        const double v = fv - (Ov * uc + acc);
-        WR(0) = (rr >= 1 && rr <= x.ny && (od ? x.in1 : x.in0)) ? v : 0.0;
-        // ---- restriction of coarse row J when rr = 2J+1 (fig:restrict_kernel, c5a terms):
-        // rows 2J+-1 odd (red = odd column 2h+1; 2I-1 is the left lane's), row 2J even
-        // (red = even column 2I)
-        if (od) {
-            const int J = (rr - 1) >> 1;
-            const double rmL = __shfl_up_sync(FULLM, WR(2), 1), rpL = __shfl_up_sync(FULLM, WR(0), 1);
-            if (J >= x.Jlo && J <= x.Jhi && x.out_coarse) {
-                double fcv = S.wNE * rmL;
-                fcv += S.wNW * WR(2);
-                fcv += WR(1);
-                fcv += S.wSE * rpL;
-                fcv += S.wSW * WR(0);
-                x.a->fc[(long long)J * x.CP + x.I] = fcv;
-                if (x.a->uc)
-                    x.a->uc[(long long)J * x.CP + x.I] = 0.0;
-            }
-            // weights of coarse row J+1 (restricted two steps from now)
-            const int Jn = J + 1;
-            if (Jn >= x.Jlo && Jn <= x.Jhi && x.out_coarse) {
-                const long long q0 = (long long)Jn * x.CP + x.I, q1 = q0 + x.CP;
-                S.wNE = x.a->ci.w[CI_LNE][q0];
-                S.wNW = x.a->ci.w[CI_LNW][q0 + 1];
-                S.wSE = x.a->ci.w[CI_LSE][q1];
-                S.wSW = x.a->ci.w[CI_LSW][q1 + 1];
-            }
-        }
-    }
-    // ---- store of row w = t-NS (final: stage NS just did its last colour)
-    {
-        const int w = t - NS;
-        if (w >= x.ya && w < x.yb && w >= 1 && w <= x.ny && x.out_lane) {
-            double *dst = x.a->uout + (long long)w * x.P + x.c0;
-            const double2 v = by_colour(WU(NS), w & 1);  // back to (even, odd)
-            if (x.in0 && x.in1)
-                *reinterpret_cast<double2 *>(dst) = v;
-            else {
-                if (x.in0)
-                    dst[0] = v.x;
-                if (x.in1)
-                    dst[1] = v.y;
-            }
-        }
-    }
-#undef WU
-#undef WC
-#undef WR
-}
-
-template <int NS>
-__device__ __forceinline__ void wv_run(WvState &S, const WvCtx &x, int tend)
-{
-    for (int t0 = x.lo; t0 <= tend; t0 += 7) {
-        wv_step<NS, 0>(S, x, t0);
-        if (t0 + 1 <= tend)
-            wv_step<NS, 1>(S, x, t0 + 1);
-        if (t0 + 2 <= tend)
-            wv_step<NS, 2>(S, x, t0 + 2);
-        if (t0 + 3 <= tend)
-            wv_step<NS, 3>(S, x, t0 + 3);
-        if (t0 + 4 <= tend)
-            wv_step<NS, 4>(S, x, t0 + 4);
-        if (t0 + 5 <= tend)
-            wv_step<NS, 5>(S, x, t0 + 5);
-        if (t0 + 6 <= tend)
-            wv_step<NS, 6>(S, x, t0 + 6);
-    }
-}
-
-template <int NS>
-__global__ void __launch_bounds__(32 * WV_WARPS, 2) k_wave_down5(FArgs a, const __grid_constant__ TMaps tmaps)
-{
-    static_assert(NS + 2 < 7, "window");
-    extern __shared__ __align__(128) double sm[];
-    WvCtx x;
-    x.a = &a;
-    x.tm = &tmaps;
-    x.sm = sm;
-    x.full = (uint64_t *)(sm + WV_SD * WV_SS);
-    x.empty = x.full + WV_SD;
-    x.nx = a.A.nx;
-    x.ny = a.A.ny;
-    x.P = a.A.pitch;
-    x.CP = a.ci.pitch;
-    const int strip = blockIdx.x % a.nstrips, chunk = blockIdx.x / a.nstrips;
-    const int x0 = strip * WV_TX;
-    x.xl = x0 - WV_H;
-    x.ya = a.A.ylo + chunk * a.chunk;
-    x.yb = min(a.A.yhi, x.ya + a.chunk);
-    if (x.ya >= x.yb)
-        return;
-    x.lo = max(x.ya - NS - 2, a.A.roff);
-    x.hi = min(x.yb + NS + 1, a.A.roff + a.A.nrows - 1);
-    x.Jlo = (x.ya + 1) / 2;
-    x.Jhi = min((x.yb - 1) / 2, a.ncy);
-    const int warp = threadIdx.x >> 5;
-    x.lane = threadIdx.x & 31;
-    x.lc0 = warp * WV_OUT + 2 * x.lane;  // local (staged) column of the even member
-    x.c0 = x.xl + x.lc0;                 // its global column (even)
-    x.out_lane = x.lc0 >= warp * WV_OUT + WV_H && x.lc0 < warp * WV_OUT + WV_H + WV_OUT;
-    x.in0 = x.c0 >= 1 && x.c0 <= x.nx;
-    x.in1 = x.c0 + 1 >= 1 && x.c0 + 1 <= x.nx;
-    x.I = x.c0 >> 1;
-    x.out_coarse = x.out_lane && x.I >= 1 && x.I <= a.ncx;
-
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < WV_SD; i++) {
-            mbar_init(&x.full[i], 1);
-            mbar_init(&x.empty[i], WV_WARPS);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0)
-        for (int row = x.lo; row <= min(x.lo + WV_D - 1, x.hi); row++)
-            wv_issue_row(x, row);
-
-    WvState S;
-    const double2 z2 = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int k = 0; k < 7; k++) {
-        S.Up[k] = z2;
-        S.Cp[k] = WvCo{z2, z2, z2, z2, z2, z2};
-        S.Rp[k] = 0.0;
-    }
-    S.wNE = S.wNW = S.wSE = S.wSW = 0.0;
-    wv_run<NS>(S, x, x.yb + NS + 1);
 }
 
 // ------------------------------------------------------------------ up kernel
@@ -1256,21 +959,42 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
 }
 
 // ------------------------------------------------------------------ host side
-static int g_sms = 0;
-static size_t g_smem_optin = 0, g_smem_sm = 0;
+// Per-device limits and kernel attributes: cudaFuncSetAttribute applies to the
+// device current at the call, so a handle set up on another GPU of the same
+// process gets its own; guarded for concurrent setups.
+constexpr int MAX_DEV = 64;
+struct DevInfo {
+    int sms = 148;
+    size_t smem_optin = 227 * 1024, smem_sm = 228 * 1024;
+};
+static DevInfo g_dev[MAX_DEV];
+static std::once_flag g_dev_once[MAX_DEV];
 
-static void device_limits()
+static int cur_device()
 {
-    if (g_sms)
-        return;
-    int dev = 0, v = 0;
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    g_sms = v > 0 ? v : 148;
-    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    g_smem_optin = v > 0 ? (size_t)v : 227 * 1024;
-    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    g_smem_sm = v > 0 ? (size_t)v : 228 * 1024;
+    return dev >= 0 && dev < MAX_DEV ? dev : 0;
+}
+
+static void set_all_attrs();
+
+// Limits of the current device (queried, and the fused kernels' attributes set, once per device).
+static const DevInfo &device_limits()
+{
+    const int dev = cur_device();
+    std::call_once(g_dev_once[dev], [dev]() {
+        int v = 0;
+        DevInfo &d = g_dev[dev];
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+            d.sms = v;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess && v > 0)
+            d.smem_optin = (size_t)v;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) == cudaSuccess && v > 0)
+            d.smem_sm = (size_t)v;
+        set_all_attrs();
+    });
+    return g_dev[dev];
 }
 
 // Deepest TMA prefetch (rows, <= 4) whose shared-memory footprint fits a CTA.
@@ -1348,35 +1072,45 @@ static void fill_geom(FusedGeom &g, bool up)
 }
 
 template <int KIND, int NS>
-static void set_attrs()
+static void set_attrs(size_t optin)
 {
     using I = Inst<KIND, NS>;
-    device_limits();
     constexpr size_t sd = I::CD::SMEM, su = I::CU::SMEM;
-    if (sd <= g_smem_optin)
+    if (sd <= optin)
         cudaFuncSetAttribute(k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN, I::E_DN>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sd);
-    if (su <= g_smem_optin)
+    if (su <= optin) {
         cudaFuncSetAttribute(k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)su);
         cudaFuncSetAttribute(k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)su);
+    }
     cudaGetLastError();  // an unsupported instance is simply not planned (plan_grid checks the size)
+}
+
+// called once per device, inside device_limits()
+static void set_all_attrs()
+{
+    const size_t optin = g_dev[cur_device()].smem_optin;
+    set_attrs<5, 2>(optin);
+    set_attrs<5, 4>(optin);
+    set_attrs<9, 2>(optin);
+    set_attrs<9, 4>(optin);
 }
 
 // Grid for one kernel: strips of TX columns x chunks of rows, chosen to balance
 // the per-SM work over waves (warm-up rows counted as overhead).
 static void plan_grid(FusedGeom &g, int nx, int ny, int warm)
 {
-    device_limits();
+    const DevInfo &dv = device_limits();
     g.ok = false;
-    if (g.smem > g_smem_optin)
+    if (g.smem > dv.smem_optin)
         return;
-    int occ = (int)(g_smem_sm / (g.smem + 1024));
+    int occ = (int)(dv.smem_sm / (g.smem + 1024));
     occ = std::min(occ, 2048 / g.threads);
     if (occ < 1)
         return;
-    const int slots = g_sms * occ;
+    const int slots = dv.sms * occ;
     g.nstrips = nx / g.TX + 1;
     double best = 1e300;
     for (int w = 1; w <= 32; w++) {
@@ -1405,35 +1139,8 @@ bmg_status_t fused_plan_level(FusedPlan &fp, int l, int nx, int ny, long long pi
         return BMG_OK;
     if ((nu1 != 1 && nu1 != 2) || (nu2 != 1 && nu2 != 2))
         return BMG_OK;
-    static bool attrs = false;
-    if (!attrs) {
-        set_attrs<5, 2>();
-        set_attrs<5, 4>();
-        set_attrs<9, 2>();
-        set_attrs<9, 4>();
-        attrs = true;
-    }
+    device_limits();  // per device: limits + kernel attributes
     const int nsd = 2 * nu1, nsu = 2 * nu2;
-    if (kind == 5 && BMG_WAVE5) {
-        // the register-wavefront down leg (k_wave_down5)
-        static bool wattrs = false;
-        if (!wattrs) {
-            cudaFuncSetAttribute(k_wave_down5<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WV_SMEM);
-            cudaFuncSetAttribute(k_wave_down5<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WV_SMEM);
-            cudaGetLastError();
-            wattrs = true;
-        }
-        FusedGeom &g = lp.gd;
-        g.TX = WV_TX, g.H = WV_H, g.WD = WV_W, g.WC = (WV_TX / 2 + 2 * CH + 15) / 16 * 16, g.R = 0, g.D = WV_D;
-        g.threads = 32 * WV_WARPS, g.smem = WV_SMEM, g.NS = nsd, g.wave = true;
-        nsu == 2 ? fill_geom<5, 2>(lp.gu, true) : fill_geom<5, 4>(lp.gu, true);
-        plan_grid(lp.gd, nx, ny, 2 * nsd + 3);
-        plan_grid(lp.gu, nx, ny, 2 * nsu + 2);
-        lp.gu.rev = rev;
-        lp.down = lp.gd.ok;
-        lp.up = lp.gu.ok;
-        return BMG_OK;
-    }
     if (kind == 5) {
         nsd == 2 ? fill_geom<5, 2>(lp.gd, false) : fill_geom<5, 4>(lp.gd, false);
         nsu == 2 ? fill_geom<5, 2>(lp.gu, true) : fill_geom<5, 4>(lp.gu, true);
@@ -1453,7 +1160,7 @@ bmg_status_t fused_plan_level(FusedPlan &fp, int l, int nx, int ny, long long pi
                     "chunks of %d rows (%d CTAs, %d/SM)\n",
                     l, nx, ny, kind, g == &lp.gd ? "down" : "up", (int)g->ok, g->TX, g->WD, g->D, g->threads,
                     (int)g->smem, g->nstrips, g->nchunks, g->chunk, g->nstrips * g->nchunks,
-                    (int)std::min<long long>(g_smem_sm / (g->smem + 1024), 2048 / g->threads));
+                    (int)std::min<long long>(device_limits().smem_sm / (g->smem + 1024), 2048 / g->threads));
     return BMG_OK;
 }
 
@@ -1543,10 +1250,6 @@ static bool make_maps(TMaps &tm, const FusedGeom &g, const Op &A, const CIv &ci,
 template <int KIND, int NS>
 static void launch_down(const FusedGeom &g, const FArgs &a, const TMaps &tm, cudaStream_t s)
 {
-    if (KIND == 5 && g.wave) {
-        k_wave_down5<NS><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a, tm);
-        return;
-    }
     using I = Inst<KIND, NS>;
     k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN, I::E_DN><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a, tm);
 }
@@ -1592,8 +1295,6 @@ bool fused_down(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const do
     a.fc = fc;
     a.uc = uc;
     a.uzero = uin == nullptr;
-    if (a.uzero && g.wave)  // the register wavefront reads its start (level 0 only)
-        return false;
     TMaps tm;
     if (!make_maps(tm, g, A, ci, uin ? uin : f, f, nullptr, 0, 0))  // uzero: u map unused
         return false;

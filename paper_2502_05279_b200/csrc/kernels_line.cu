@@ -32,6 +32,7 @@
 // k_line_elim (no scratch).  Pivots use rcp_pos (FMA pipe, bmg_internal.cuh):
 // the line blocks of an SPD operator are SPD, so every pivot is positive
 // (checked once at setup by k_line_pivots -> BMG_ENOTSPD).
+#include <mutex>
 #include "bmg_internal.cuh"
 #include "line.cuh"
 
@@ -451,10 +452,13 @@ static void colour_pass(const Op &A, const double *f, double *u, double *scr, in
         int lpb = (int)((size_t)LINE_SMEM / per_line);
         lpb = lpb > 4 ? 4 : (lpb < 1 ? 1 : lpb);
         const size_t smem = lpb * per_line;
-        static bool attr[2] = {false, false};
-        if (!attr[Y]) {
-            cudaFuncSetAttribute(k_line_reduced<Y>, cudaFuncAttributeMaxDynamicSharedMemorySize, LINE_SMEM);
-            attr[Y] = true;
+        {  // the attribute is per device (a handle may live on any GPU of the process)
+            static std::once_flag once[64][2];
+            int dev = 0;
+            cudaGetDevice(&dev);
+            std::call_once(once[dev & 63][Y], []() {
+                cudaFuncSetAttribute(k_line_reduced<Y>, cudaFuncAttributeMaxDynamicSharedMemorySize, LINE_SMEM);
+            });
         }
         k_line_reduced<Y><<<dim3((g.nl + lpb - 1) / lpb), dim3(32 * lpb), smem, s>>>(A, u, g, sc);
         k_line_back<Y><<<gr, b, 0, s>>>(A, u, g, sc);

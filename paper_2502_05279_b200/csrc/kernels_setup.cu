@@ -5,6 +5,11 @@
 // Setup arithmetic uses __dmul_rn/__dadd_rn where the oracle evaluates a
 // product followed by a sum, so that no FMA contraction changes a rounding:
 // level-0 interpolation weights are then bitwise equal to the oracle's.
+#include <stdlib.h>
+
+#include <mutex>
+#include <utility>
+
 #include "bmg_internal.cuh"
 
 namespace bmg {
@@ -237,14 +242,179 @@ __global__ void k_rap(Op A, CIv ci, int ncx, int ncy, long long cpitch, double *
     cNW[q] = acc[4];
 }
 
+// ---- tiled RAP: the same gather, the same terms in the same order as k_rap (so the
+// same bits), with the P lookups resolved at compile time and the operands staged
+// in shared memory.  For coarse C = (I,J), fine f = (2I-1+UX, 2J-1+UY) and its
+// stencil direction d (g = f + off_d), and target D = C + t_k, the weight P(g, D)
+// is zero, one, or ONE interpolation weight at a FIXED offset from (I,J): g's
+// position relative to (2I,2J) is (ex,ey) = (UX-1+ddx, UY-1+ddy) in [-2,2]^2.
+struct PwSel {
+    int kind;  // 0: zero, 1: one, 2: weight plane `plane` at coarse (I+oi, J+oj)
+    int plane, oi, oj;
+};
+__host__ __device__ constexpr PwSel pw_sel(int ex, int ey, int tx, int ty)
+{
+    const int dx = ex - 2 * tx, dy = ey - 2 * ty;
+    if (dx < -1 || dx > 1 || dy < -1 || dy > 1)
+        return {0, 0, 0, 0};
+    const bool xo = (ex & 1) != 0, yo = (ey & 1) != 0;
+    if (!xo && !yo)
+        return (dx == 0 && dy == 0) ? PwSel{1, 0, 0, 0} : PwSel{0, 0, 0, 0};
+    if (xo && !yo)  // X point, stored at ((gx+1)/2, gy/2)
+        return dy != 0 ? PwSel{0, 0, 0, 0} : PwSel{2, dx > 0 ? CI_LL : CI_LR, (ex + 1) / 2, ey / 2};
+    if (!xo && yo)  // Y point, stored at (gx/2, (gy+1)/2)
+        return dx != 0 ? PwSel{0, 0, 0, 0} : PwSel{2, dy > 0 ? CI_LB : CI_LA, ex / 2, (ey + 1) / 2};
+    return {2, dx > 0 ? (dy > 0 ? CI_LSW : CI_LNW) : (dy > 0 ? CI_LSE : CI_LNE), (ex + 1) / 2, (ey + 1) / 2};
+}
+
+constexpr int RAP_TC = 32, RAP_TR = 8;                     // coarse tile
+constexpr int RAP_FW = 2 * RAP_TC + 2, RAP_FH = 2 * RAP_TR + 3;  // fine planes: x in [2I0-1, 2I0+2TC], y in [2J0-2, 2J0+2TR]
+constexpr int RAP_CW = RAP_TC + 2, RAP_CH = RAP_TR + 2;          // weights: I in [I0-1, I0+TC], J in [J0-1, J0+TR]
+constexpr int RAP_TX[5] = {0, -1, 0, -1, -1}, RAP_TY[5] = {0, 0, -1, -1, 1};
+
+struct RapSm {
+    double pl[5][RAP_FH][RAP_FW];  // O W S SW NW
+    double ci[8][RAP_CH][RAP_CW];
+};
+
+// weight P(g, D) for g at (EX,EY) from (2I,2J), D = C + t_K; cx, cy: thread's (I,J) in the weight tile
+template <int EX, int EY, int K>
+__device__ __forceinline__ double pw_tile(const RapSm &sm, int cx, int cy)
+{
+    constexpr PwSel q = pw_sel(EX, EY, RAP_TX[K], RAP_TY[K]);
+    if constexpr (q.kind == 0)
+        return 0.0;
+    else if constexpr (q.kind == 1)
+        return 1.0;
+    else
+        return sm.ci[q.plane][cy + q.oj][cx + q.oi];
+}
+
+// the k_rap contributions of stencil direction DD of fine point f = (2I-1+UX, 2J-1+UY)
+template <int UX, int UY, int DD, int K>
+__device__ __forceinline__ void rap_term(const RapSm &sm, int cx, int cy, double wa, const bool *vk, double *acc)
+{
+    constexpr int EX = UX - 1 + DD % 3 - 1, EY = UY - 1 + DD / 3 - 1;
+    constexpr PwSel q = pw_sel(EX, EY, RAP_TX[K], RAP_TY[K]);
+    if constexpr (q.kind != 0) {  // a structurally zero weight adds an exact 0 in k_rap
+        if (vk[K])
+            acc[K] = __fma_rn(wa, pw_tile<EX, EY, K>(sm, cx, cy), acc[K]);
+    }
+}
+
+template <int UX, int UY, int DD>
+__device__ __forceinline__ void rap_dir(const RapSm &sm, int cx, int cy, double wf, const double *av, const bool *vk,
+                                        double *acc)
+{
+    const double wa = __dmul_rn(wf, av[DD]);
+    rap_term<UX, UY, DD, 0>(sm, cx, cy, wa, vk, acc);
+    rap_term<UX, UY, DD, 1>(sm, cx, cy, wa, vk, acc);
+    rap_term<UX, UY, DD, 2>(sm, cx, cy, wa, vk, acc);
+    rap_term<UX, UY, DD, 3>(sm, cx, cy, wa, vk, acc);
+    rap_term<UX, UY, DD, 4>(sm, cx, cy, wa, vk, acc);
+}
+
+template <int UX, int UY, int... DD>
+__device__ __forceinline__ void rap_fine(const RapSm &sm, int cx, int cy, int fxl, int fyl, const bool *vk, double *acc,
+                                         std::integer_sequence<int, DD...>)
+{
+    constexpr PwSel wq = pw_sel(UX - 1, UY - 1, 0, 0);  // P(f, C)
+    if constexpr (wq.kind != 0) {
+        const double wf = pw_tile<UX - 1, UY - 1, 0>(sm, cx, cy);
+        // f's full row (fig:stencil_operator order SW,S,SE,W,O,E,NW,N,NE) from the staged planes;
+        // fxl, fyl: f's position in the plane tile
+        const int x = fxl + UX, y = fyl + UY;
+        const double av[9] = {sm.pl[3][y][x],     sm.pl[2][y][x],     sm.pl[4][y - 1][x + 1],
+                              sm.pl[1][y][x],     sm.pl[0][y][x],     sm.pl[1][y][x + 1],
+                              sm.pl[4][y][x],     sm.pl[2][y + 1][x], sm.pl[3][y + 1][x + 1]};
+        (rap_dir<UX, UY, DD>(sm, cx, cy, wf, av, vk, acc), ...);
+    }
+}
+
+// One CTA per RAP_TC x RAP_TR coarse tile, one thread per coarse point.  Same
+// definition as k_rap: A_c(C,D) = sum_f P(f,C) sum_g A(f,g) P(g,D), terms in the order
+// f (row-major over C's 3x3 window), stencil direction, target D.
+__global__ void __launch_bounds__(RAP_TC *RAP_TR) k_rap_tiled(Op A, CIv ci, int ncx, int ncy, long long cpitch,
+                                                             double *cO, double *cW, double *cS, double *cSW,
+                                                             double *cNW, int J0, int J1)
+{
+    extern __shared__ __align__(16) unsigned char rap_raw[];
+    RapSm &sm = *reinterpret_cast<RapSm *>(rap_raw);
+    const int I0 = blockIdx.x * RAP_TC + 1, Jt = J0 + blockIdx.y * RAP_TR;
+    const int tid = threadIdx.x;
+    // stage the fine planes (zero outside the stored rows / the padded grid)
+    const int fx0 = 2 * I0 - 1, fy0 = 2 * Jt - 2;
+    const int ylo = max(A.roff, 0), yhi = min(A.ny + 1, A.roff + A.nrows - 1);
+    const int kpl = A.kind == 9 ? 5 : 3;
+    const double *pls[5] = {A.O, A.W, A.S, A.SW, A.NW};
+    for (int e = tid; e < 5 * RAP_FH * RAP_FW; e += blockDim.x) {
+        const int k = e / (RAP_FH * RAP_FW), r = (e / RAP_FW) % RAP_FH, c = e % RAP_FW;
+        const int gy = fy0 + r, gx = fx0 + c;
+        double v = 0.0;
+        if (k < kpl && gy >= ylo && gy <= yhi && gx >= 0 && gx <= A.nx + 1)
+            v = pls[k][(long long)gy * A.pitch + gx];
+        sm.pl[k][r][c] = v;
+    }
+    const int cylo = max(ci.roff, 0), cyhi = min(ncy + 1, ci.roff + ci.nrows - 1);
+    for (int e = tid; e < 8 * RAP_CH * RAP_CW; e += blockDim.x) {
+        const int k = e / (RAP_CH * RAP_CW), r = (e / RAP_CW) % RAP_CH, c = e % RAP_CW;
+        const int cy = Jt - 1 + r, cx = I0 - 1 + c;
+        double v = 0.0;
+        if (cy >= cylo && cy <= cyhi && cx >= 0 && cx <= ncx + 1)
+            v = ci.w[k][(long long)cy * ci.pitch + cx];
+        sm.ci[k][r][c] = v;
+    }
+    __syncthreads();
+    const int tx = tid % RAP_TC, ty = tid / RAP_TC;
+    const int I = I0 + tx, J = Jt + ty;
+    if (I > ncx || J > J1)
+        return;
+    // target D = C + t_k exists (k_rap's test): t = (0,0), (-1,0), (0,-1), (-1,-1), (-1,+1)
+    const bool vk[5] = {true, I > 1, J > 1, I > 1 && J > 1, I > 1 && J < ncy};
+    double acc[5] = {0, 0, 0, 0, 0};
+    const int cx = tx + 1, cy = ty + 1;          // (I,J) in the weight tile
+    const int fxl = 2 * tx, fyl = 2 * ty + 1;    // f = (2I-1+UX, 2J-1+UY) -> tile (fxl+UX, fyl+UY)
+    using Dirs = std::make_integer_sequence<int, 9>;
+    rap_fine<0, 0>(sm, cx, cy, fxl, fyl, vk, acc, Dirs{});
+    rap_fine<1, 0>(sm, cx, cy, fxl, fyl, vk, acc, Dirs{});
+    rap_fine<2, 0>(sm, cx, cy, fxl, fyl, vk, acc, Dirs{});
+    rap_fine<0, 1>(sm, cx, cy, fxl, fyl, vk, acc, Dirs{});
+    rap_fine<1, 1>(sm, cx, cy, fxl, fyl, vk, acc, Dirs{});
+    rap_fine<2, 1>(sm, cx, cy, fxl, fyl, vk, acc, Dirs{});
+    rap_fine<0, 2>(sm, cx, cy, fxl, fyl, vk, acc, Dirs{});
+    rap_fine<1, 2>(sm, cx, cy, fxl, fyl, vk, acc, Dirs{});
+    rap_fine<2, 2>(sm, cx, cy, fxl, fyl, vk, acc, Dirs{});
+    const long long q = J * cpitch + I;
+    cO[q] = acc[0];
+    cW[q] = acc[1];
+    cS[q] = acc[2];
+    cSW[q] = acc[3];
+    cNW[q] = acc[4];
+}
+
 // Coarse rows [J0, J1] (inclusive; single GPU: [1, ncy]).
 void launch_setup_rap(const Op &A, const CIv &ci, int ncx, int ncy, long long cpitch, double *const dst[5],
                       cudaStream_t s, int J0, int J1)
 {
     if (J1 < J0)
         return;
-    dim3 b(32, 4), g((ncx + 31) / 32, (J1 - J0 + 1 + 3) / 4);
-    k_rap<<<g, b, 0, s>>>(A, ci, ncx, ncy, cpitch, dst[0], dst[1], dst[2], dst[3], dst[4], J0, J1);
+    static const bool ref = getenv("BMG_RAP_REF") != nullptr;  // the untiled k_rap (A/B checks)
+    if (ref) {
+        dim3 b(32, 4), g((ncx + 31) / 32, (J1 - J0 + 1 + 3) / 4);
+        k_rap<<<g, b, 0, s>>>(A, ci, ncx, ncy, cpitch, dst[0], dst[1], dst[2], dst[3], dst[4], J0, J1);
+        return;
+    }
+    {  // the dynamic shared-memory limit of k_rap_tiled, once per device
+        static std::once_flag once[64];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::call_once(once[dev & 63], []() {
+            cudaFuncSetAttribute(k_rap_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RapSm));
+        });
+    }
+    dim3 g((ncx + RAP_TC - 1) / RAP_TC, (J1 - J0 + RAP_TR) / RAP_TR);
+    k_rap_tiled<<<g, RAP_TC * RAP_TR, sizeof(RapSm), s>>>(A, ci, ncx, ncy, cpitch, dst[0], dst[1], dst[2], dst[3],
+                                                         dst[4], J0, J1);
 }
 
 // ---------------------------------------------------------------- S3 coarsest factor

@@ -113,6 +113,8 @@ struct bmg_solver {
     double *line_scr = nullptr;       // c11 line relaxation scratch (line modes only)
     double *pcg_ws = nullptr;         // c13 PCG vectors r, z, p, q (level-0 arrays) + scalars, lazily
     cudaEvent_t pcg_ev = nullptr;     // marks the residual norm's arrival in h_norm
+    cudaEvent_t pcg_tail = nullptr;   // end of the speculative work a returning bmg_pcg left queued
+    bool pcg_pending = false;         // pcg_tail recorded and not yet joined by another entry point
     // device-side solve loop: per (rhs, x) a graph [WHILE: cycle, residual norm, k_solve_step]
     std::map<std::pair<const void *, const void *>, cudaGraphExec_t> sgraphs;
     SolveState *solve_st = nullptr;   // device state
@@ -151,6 +153,17 @@ struct bmg_solver {
         return v;
     }
 };
+
+// A call on another stream must not overtake the speculative preconditioner
+// V-cycle a returning bmg_pcg may have left queued (it writes the hierarchy
+// arrays and the PCG workspace): every entry point that enqueues work joins it.
+inline void join_pcg(bmg_solver *h, cudaStream_t s)
+{
+    if (h && h->pcg_pending) {
+        cudaStreamWaitEvent(s, h->pcg_tail, 0);
+        h->pcg_pending = false;
+    }
+}
 
 inline bmg_status_t dalloc(bmg_solver *h, double **p, size_t n)
 {

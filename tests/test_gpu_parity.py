@@ -316,10 +316,10 @@ def test_random_shapes_vcycle_parity(orc):
     straddling the fused / tail / per-step thresholds and the strip width): one fused
     V(2,1) cycle against the oracle, every operator including the anisotropic one, at
     the DESIGN §7 rule.  Each case is also run through the oracle's extended-precision
-    build: where the fp64 oracle is within 1e-13 of that iterate, the GPU must match the
-    oracle to 1e-12 (normwise); where fp64 itself is less accurate (anisotropic, and
-    lognormal on some shapes: up to ~8e-12 of max|x|, tests/test_oracle_extended.py),
-    the GPU must be at most twice as far from the extended iterate as the oracle is."""
+    build: the GPU must match the oracle to 1e-12 (normwise), or, where it does not, be
+    at most twice as far from the extended iterate as the fp64 oracle is (fp64 itself is
+    that inaccurate there: anisotropic, and lognormal on some shapes, up to ~8e-12 of
+    max|x|, tests/test_oracle_extended.py)."""
     from oracle import extended
 
     rng = np.random.default_rng(2025)
@@ -344,12 +344,11 @@ def test_random_shapes_vcycle_parity(orc):
         e = extended.HierarchyExt(st).vcycle(f, x0, 1).astype(np.float64)
         scale = np.abs(e).max()
         dg, do = np.abs(got - e).max() / scale, np.abs(ref - e).max() / scale
-        if do <= 1e-13:
-            assert_iterate_close(got, ref)
-        else:
+        dgo = np.abs(got - ref).max() / np.abs(ref).max()
+        if dgo > 1e-12:  # the contract's 1e-12 missed: only admissible where fp64 itself is that inaccurate
             n_ext += 1
-            assert dg <= 2 * do, (wl, nx, ny, dg, do)
-    assert n_ext >= 2  # the sweep does exercise the ill-conditioned cases
+            assert dg <= 2 * do, (wl, nx, ny, dgo, dg, do)
+    assert n_ext >= 1  # the sweep does exercise the ill-conditioned cases (190x417 anisotropic)
 
 
 @pytest.mark.parametrize("nu1,nu2,coarsest,max_levels", [(1, 1, 3, 0), (2, 2, 3, 0), (0, 1, 3, 0), (1, 0, 3, 0),
@@ -391,3 +390,43 @@ def test_user_pitch_vcycle_parity(orc, extra):
     xg = x.cpu().numpy()
     assert np.all(xg[:, nx + 1:] == 0)  # padding and ring untouched
     s.close()
+
+
+_RAP_DUMP = r'''
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from paper_2502_05279_b200 import bmg, problems as P
+out = {{}}
+for wl, nx, ny in {cases!r}:
+    s = bmg.Solver(P.workload(wl, nx, ny))
+    for l in range(1, s.L):
+        out[f"{{wl}}_{{nx}}_{{ny}}_{{l}}"] = bmg.bmg_export_level(s.h, l)[0]
+    s.close()
+np.savez({path!r}, **out)
+'''
+
+
+def test_rap_tiled_bitwise_equals_gather(tmp_path):
+    """k_rap_tiled (shared-memory tiles, compile-time P lookups) evaluates exactly the
+    terms of the per-point gather k_rap in the same order: every coarse level bitwise equal
+    (BMG_RAP_REF=1 selects k_rap; the switch is read once per process, hence subprocesses)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cases = [("aniso", 255, 200), ("lognormal", 300, 257), ("random9", 131, 90), ("checker_off3", 95, 47),
+             ("poisson", 64, 30)]
+    outs = []
+    for ref in (0, 1):
+        path = str(tmp_path / f"rap{ref}.npz")
+        env = dict(os.environ)
+        env.pop("BMG_RAP_REF", None)
+        if ref:
+            env["BMG_RAP_REF"] = "1"
+        subprocess.run([sys.executable, "-c", _RAP_DUMP.format(root=root, cases=cases, path=path)], env=env,
+                       check=True)
+        outs.append(np.load(path))
+    assert set(outs[0].files) == set(outs[1].files) and outs[0].files
+    for k in outs[0].files:
+        assert np.array_equal(outs[0][k], outs[1][k]), (k, np.abs(outs[0][k] - outs[1][k]).max())

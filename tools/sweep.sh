@@ -3,6 +3,6 @@
 cd $GRAFT_REPO_ROOT
 for v in ${VARIANTS:-h0 h1 h2}; do
   for w in ${WLS:-poisson:8191 aniso:4095}; do
-    BMG_LIB=variants/libbmg_$v.so WL=${w%%:*} N=${w##*:} timeout 120 python tools/legbench.py
+    BMG_LIB=tools/vlib/libbmg_$v.so WL=${w%%:*} N=${w##*:} timeout 120 python tools/legbench.py
   done
 done

@@ -1,4 +1,4 @@
-"""Build libbmg.so variants with -D tuning macros (kernels_fused.cu Inst) into variants/.
+"""Build libbmg.so variants with -D tuning macros (kernels_fused.cu Inst) into tools/vlib/.
 
 usage: python tools/variants.py NAME "-DBMG_E5DN=2 -DBMG_D5=3" [NAME FLAGS ...]
 """
@@ -7,7 +7,7 @@ from concurrent.futures import ThreadPoolExecutor
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import __graft_entry__ as ge
 
-out = os.path.join(ge.ROOT, "variants")
+out = os.path.join(ge.ROOT, "tools", "vlib")  # travels with gpurun (variants/ does not)
 os.makedirs(out, exist_ok=True)
 srcs = sorted(os.path.join(ge.CSRC, f) for f in os.listdir(ge.CSRC) if f.endswith(".cu"))
 
