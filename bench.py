@@ -362,10 +362,12 @@ def main():
                  "mean_factor": float((hist[-1] / hist[0]) ** (1.0 / k)) if k > 0 and hist[0] > 0 else None,
                  "last_factor": float(hist[-1] / hist[-2]) if k > 0 and hist[-2] > 0 else None,
                  "setup_ms": solver.setup_ms,
+                 "setup_device_ms": bmg.bmg_setup_time(solver.h),
                  "note": "x0 = 0; ms = wall clock of bmg_solve (device-side loop: one graph launch whose conditional "
                          "WHILE node runs cycle + norm + stopping test; graph captured by an untimed warm-up solve); "
                          "setup_ms = wall clock of bmg_setup (S0-S3 + allocation, synchronised; kernels already loaded by a "
-                         "warm-up setup on 255^2)"}
+                         "warm-up setup on 255^2); setup_device_ms = device time of the S0-S3 kernels "
+                         "(bmg_setup_time)"}
         del xs
         if args.pcg > 0:
             # V-cycle-preconditioned CG (bmg_pcg) with the symmetric V(NU,NU) cycle

@@ -288,6 +288,11 @@ bmg_status_t bmg_cycle_kernel_count(bmg_solver_t h, int *count);
 bmg_status_t bmg_timing(bmg_solver_t h, int enable);
 bmg_status_t bmg_timing_read(bmg_solver_t h, double *ms_total, int *launches);
 
+/* Device time (ms) of the setup kernels of a single-GPU handle: S0 ingest through the
+ * S3 Cholesky factor (events around them; excludes allocation, which bmg_setup's wall
+ * clock includes).  Blocks until they have run.  EINVAL on a distributed handle. */
+bmg_status_t bmg_setup_time(bmg_solver_t h, double *device_ms);
+
 /* Per-leg breakdown of one cycle (SURVEY §5 per-level report, mirroring the
  * paper's per-level kernel timings, fig:kernel_timings P:492-500).  Captures a
  * variant of the cycle's graph with an event-record node between every two

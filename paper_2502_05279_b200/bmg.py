@@ -24,7 +24,7 @@ EXPORTS = (
     "bmg_params_default", "bmg_setup", "bmg_vcycle", "bmg_vcycle_host", "bmg_solve", "bmg_pcg", "bmg_residual_norm",
     "bmg_num_levels", "bmg_level_shape", "bmg_level_pitch", "bmg_export_level", "bmg_relax", "bmg_residual",
     "bmg_restrict", "bmg_interp_add", "bmg_smooth_restrict", "bmg_correct_smooth", "bmg_cycle_kernel_count", "bmg_timing",
-    "bmg_timing_read", "bmg_profile_legs", "bmg_destroy", "bmg_strerror",
+    "bmg_timing_read", "bmg_profile_legs", "bmg_setup_time", "bmg_destroy", "bmg_strerror",
     "bmg_last_error_detail", "bmg_partition", "bmg_setup_dist", "bmg_local_rows", "bmg_vcycle_block",
     "bmg_residual_norm_block", "bmg_solve_block", "bmg_pcg_block",
 )
@@ -97,6 +97,7 @@ def lib():
             "bmg_correct_smooth": (i, [vp, i, vp, vp, vp, vp, vp]),
             "bmg_cycle_kernel_count": (i, [vp, ip]),
             "bmg_profile_legs": (i, [vp, vp, vp, i, dp, i, ip, vp]),
+            "bmg_setup_time": (i, [vp, dp]),
             "bmg_destroy": (i, [vp]),
             "bmg_strerror": (ctypes.c_char_p, [i]),
             "bmg_last_error_detail": (ctypes.c_char_p, []),
@@ -306,6 +307,13 @@ def bmg_profile_legs(h, rhs, x, ncycles: int = 5, stream=None):
     v = list(out[: n.value])
     lt = (n.value - 1) // 2
     return v[:lt], v[lt], v[lt + 1:][::-1]
+
+
+def bmg_setup_time(h) -> float:
+    """Device time (ms) of the setup kernels S0-S3 of a single-GPU handle."""
+    ms = ctypes.c_double()
+    _check(lib().bmg_setup_time(h, ctypes.byref(ms)), "bmg_setup_time")
+    return ms.value
 
 
 def bmg_partition(nx: int, ny: int, nranks: int, params: bmg_params_t | None = None):

@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <chrono>
+#include <mutex>
 #include <map>
 #include <string>
 #include <utility>
@@ -31,6 +32,30 @@ std::string &bmg::abi_detail()
 {
     thread_local std::string d;
     return d;
+}
+
+// Pinned host slots (8 doubles) for the norms read back by the host: one
+// cudaMallocHost per 512 handles instead of one per handle (each costs ~ms).
+static std::mutex g_pin_mu;
+static std::vector<double *> g_pin_free;
+double *pinned_slot()
+{
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (g_pin_free.empty()) {
+        double *blk = nullptr;
+        if (cudaMallocHost(&blk, 512 * 8 * sizeof(double)) != cudaSuccess)
+            return nullptr;  // the block lives for the process
+        for (int i = 511; i >= 0; i--)
+            g_pin_free.push_back(blk + 8 * i);
+    }
+    double *p = g_pin_free.back();
+    g_pin_free.pop_back();
+    return p;
+}
+void pinned_release(double *p)
+{
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back(p);
 }
 
 extern "C" {
@@ -110,7 +135,10 @@ bmg_status_t bmg_destroy(bmg_solver_t h)
     if (h->sb_st_h)
         cudaFreeHost(h->sb_st_h);
     if (h->h_norm)
-        cudaFreeHost(h->h_norm);
+        pinned_release(h->h_norm);
+    for (cudaEvent_t e : h->setup_ev)
+        if (e)
+            cudaEventDestroy(e);
     if (h->cap)
         cudaStreamDestroy(h->cap);
     delete h;
@@ -197,19 +225,19 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
             for (int k = 0; k < 8; k++)
                 h->lv[l].ci[k] = blk ? blk + k * np : nullptr;
         }
+        // the error word (zeroed with the arena), the norm partials and result
+        h->d_err = (int *)take(64);
+        h->partials = take(NORM_BLOCKS + 8);
+        h->d_norm = take(8);
     }
-    {
-        void *q;
-        CK(cudaMalloc(&q, 64 * sizeof(int)));
-        h->allocs.push_back(q);
-        h->d_err = (int *)q;
-        CK(cudaMemsetAsync(h->d_err, 0, 64 * sizeof(int), s));
-    }
-    TRY(dalloc(h, &h->partials, NORM_BLOCKS + 8));
-    TRY(dalloc(h, &h->d_norm, 8));
-    CK(cudaMallocHost(&h->h_norm, 8 * sizeof(double)));
+    h->h_norm = pinned_slot();
+    if (!h->h_norm)
+        return fail(BMG_ENOMEM, "pinned host slot");
 
     setup_trace("allocate", s);
+    CK(cudaEventCreate(&h->setup_ev[0]));
+    CK(cudaEventCreate(&h->setup_ev[1]));
+    CK(cudaEventRecord(h->setup_ev[0], s));
     // S0 ingest
     {
         Level &v = h->lv[0];
@@ -238,6 +266,7 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
         launch_chol_factor(h->nco, h->chol, h->d_err, s);
         CK(cudaGetLastError());
     }
+    CK(cudaEventRecord(h->setup_ev[1], s));
     int herr = 0;
     CK(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -656,6 +685,17 @@ bmg_status_t bmg_timing_read(bmg_solver_t h, double *ms_total, int *launches)
     *ms_total = tot;
     *launches = (int)(h->tev_used / 2);
     h->tev_used = 0;
+    return BMG_OK;
+}
+
+bmg_status_t bmg_setup_time(bmg_solver_t h, double *device_ms)
+{
+    if (!h || h->dist || !device_ms || !h->setup_ev[0])
+        return fail(BMG_EINVAL, "bmg_setup_time: bad arguments");
+    float ms = 0.f;
+    CK(cudaEventSynchronize(h->setup_ev[1]));
+    CK(cudaEventElapsedTime(&ms, h->setup_ev[0], h->setup_ev[1]));
+    *device_ms = ms;
     return BMG_OK;
 }
 

@@ -191,8 +191,9 @@ struct Cfg {
     static constexpr int WC = (TX / 2 + 2 * CH + 15) / 16 * 16;  // coarse box width (128-B rows)
     static constexpr int NPG = HW / PPT;                       // threads per task group
     static constexpr int NSPLIT = 2;                           // split task groups
-    static constexpr int NG = UP ? (KIND == 5 ? NS + 3 + NSPLIT : 5 + NSPLIT)
-                                 : (KIND == 5 ? NS + 4 + NSPLIT : 6 + NSPLIT);
+    // one warp group per colour stage (a 9-point stage is active every other row step,
+    // so its group may take two steps per row), + residual/correction, store, restriction, split
+    static constexpr int NG = UP ? NS + 3 + NSPLIT : NS + 4 + NSPLIT;
     static constexpr int NTW = NG * NPG;                       // worker threads
     static constexpr int NT = NTW + 32;                        // + one TMA producer warp
     static constexpr size_t SMEM_DBL =
@@ -467,9 +468,9 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
     // Task groups (warp-aligned, one task per row step):
     //  5-point: 0..NS-1 colour stage k = grp+1; NS, NS+1 residual of even/odd columns;
     //           NS+2 store; NS+3 restriction; NS+4, NS+5 split.
-    //  9-point: 0,1 the two active row stages (phase A even columns, phase B odd);
-    //           2,3 residual; 4 store; 5 restriction; 6,7 split.
-    constexpr int NSG = KIND == 5 ? NS : 2;  // colour-stage groups
+    //  9-point: 0..NS-1 colour stage k = grp+1, active on every other row step (its row
+    //           parity), phase A even columns, phase B odd; then as 5-point.
+    constexpr int NSG = NS;  // colour-stage groups
     constexpr int G_RES = NSG, G_STORE = NSG + 2, G_SPLIT = NSG + 4;  // restriction: NSG + 3
     // Rings (waiter <- groups it depends on, at step t-1 unless noted):
     //  g < NSG  stage group g <- split (g = 0) or stage group g-1: row r+1 = t-2k+1
@@ -656,7 +657,8 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
     } else if (grp < NSG) {
         if (grp + 1 < NSG)
             a0 = grp + 1;
-        if (KIND == 9 || grp == NSG - 1)
+        // the stages that finalise rows: the last one (5-point) / the last sweep's two (9-point)
+        if (grp >= NSG - (KIND == 9 ? 2 : 1))
             a1 = R_RES, a2 = R_STORE;
     } else if (grp < G_STORE) {
         a0 = R_SPLIT, a1 = R_RESTR;
@@ -684,17 +686,18 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
                     colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1),
                                                    (((k - 1) & 1) - r) & 1, kc);
             } else {
-                // active 9-point row stages at step t: k with (t - 2k) & 1 == (k - 1) & 1, i.e. (t + k) odd
-                const int k = ((t & 1) ? 2 : 1) + 2 * grp, d = 2 * k, r = t - d;
-                const bool act = k <= NS && r > lo && r < hi && r >= 1 && r <= ny;
-                if (act)
+                // 9-point stage k is active at step t iff (t - 2k) & 1 == (k - 1) & 1, i.e. (t + k) odd
+                const int k = grp + 1, d = 2 * k, r = t - d;
+                const bool act = ((t + k) & 1) && r > lo && r < hi && r >= 1 && r <= ny;
+                if (act) {  // uniform over the group
                     colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), 0,
                                                    kc);
-                group_sync(1 + grp, NPG);
-                if (act)
+                    group_sync(1 + grp, NPG);  // phase B reads phase A's neighbours
                     colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), 1,
                                                    kc);
-                group_sync(1 + grp, NPG);
+                    // no trailing barrier: the group's next active step (two steps on) works
+                    // two rows higher; consumers wait on the per-warp ring arrivals
+                }
             }
         } else if (grp < G_STORE) {
             rg.wait(R_RES, t - 1);
@@ -750,9 +753,10 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
     // Task groups:
     //  5-point: 0,1 correction of even/odd columns; 2..NS+1 stage k = grp-1;
     //           NS+2 store; NS+3, NS+4 split.
-    //  9-point: 0,1 active row stage(s) (phase A, B); 2,3 correction; 4 store; 5, 6 split.
-    constexpr int NSG = KIND == 5 ? NS : 2;
-    constexpr int G_ST0 = KIND == 5 ? 2 : 0, G_CORR = KIND == 5 ? 0 : 2;
+    //  9-point: 0..NS-1 stage k = grp+1 (active every other row step; phase A, B);
+    //           NS, NS+1 correction; NS+2 store; NS+3, NS+4 split.
+    constexpr int NSG = NS;
+    constexpr int G_ST0 = KIND == 5 ? 2 : 0, G_CORR = KIND == 5 ? 0 : NSG;
     constexpr int G_SPLIT = NSG + 3;  // store: NSG + 2
     // Rings (waiter <- groups it depends on, at step t-1):
     //  g < NSG  stage group g <- correction groups (g = 0: row r+1 = t-2) or stage group g-1
@@ -909,7 +913,7 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
         const int g = grp - G_ST0;
         if (g + 1 < NSG)
             a0 = g + 1;
-        if (KIND == 9 || g == NSG - 1)
+        if (g >= NSG - (KIND == 9 ? 2 : 1))
             a1 = R_SPLIT, a2 = R_STORE;
     } else {
         a0 = R_SPLIT;
@@ -939,16 +943,15 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
             } else {
                 // active 9-point row stage(s): k with (t-1-2k) & 1 == (k-1) & 1, i.e. (t + k) even
                 // (REV: (t + k) odd -- odd rows first -- and odd columns before even)
-                const int k = ((t & 1) ? (REV ? 2 : 1) : (REV ? 1 : 2)) + 2 * grp, d = 2 * k + 1, r = t - d;
-                const bool act = k <= NS && r > lo && r < hi && r >= 1 && r <= ny;
-                if (act)
+                const int k = grp - G_ST0 + 1, d = 2 * k + 1, r = t - d;
+                const bool act = (((t + k) & 1) == (REV ? 1 : 0)) && r > lo && r < hi && r >= 1 && r <= ny;
+                if (act) {  // uniform over the group
                     colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1),
                                                    REV ? 1 : 0, kc);
-                group_sync(1 + grp, NPG);
-                if (act)
+                    group_sync(1 + grp, NPG);
                     colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1),
                                                    REV ? 0 : 1, kc);
-                group_sync(1 + grp, NPG);
+                }
             }
         } else {
             rg.wait(R_STORE, t - 1);

@@ -99,7 +99,8 @@ struct bmg_solver {
     double *chol = nullptr;  // coarsest factor
     int nco = 0;
     int *d_err = nullptr;
-    double *partials = nullptr, *d_norm = nullptr, *h_norm = nullptr;  // h_norm pinned
+    double *partials = nullptr, *d_norm = nullptr, *h_norm = nullptr;  // h_norm: a pinned slot (pinned_slot)
+    cudaEvent_t setup_ev[2] = {nullptr, nullptr};  // around the S0-S3 kernels (bmg_setup_time)
     double *stage_f = nullptr, *stage_x = nullptr;                     // bmg_vcycle_host staging
     cudaStream_t cap = nullptr;                                        // capture stream
     std::map<std::pair<const void *, const void *>, GraphRec> graphs, tgraphs;  // plain / timed
@@ -164,6 +165,9 @@ inline void join_pcg(bmg_solver *h, cudaStream_t s)
         h->pcg_pending = false;
     }
 }
+
+double *pinned_slot();
+void pinned_release(double *p);
 
 inline bmg_status_t dalloc(bmg_solver *h, double **p, size_t n)
 {
