@@ -40,7 +40,7 @@ typedef enum {
     BMG_EINVAL = 1,   /* bad sizes/pointers/kind, a_O <= 0, interpolation denominator <= 0 */
     BMG_ENOMEM = 2,   /* device allocation failed */
     BMG_ECUDA = 3,    /* CUDA runtime error (detail in bmg_last_error_detail) */
-    BMG_ENCCL = 4,    /* reserved for the multi-GPU path */
+    BMG_ENCCL = 4,    /* a NCCL call of the multi-GPU path failed (bmg_setup_dist, dist cycles) */
     BMG_ENOTSPD = 5,  /* coarsest-level Cholesky pivot <= 0, or a line-block pivot <= 0 */
     BMG_ENOTCONV = 6  /* bmg_solve reached maxiter; x and hist stay valid */
 } bmg_status_t;

@@ -25,6 +25,9 @@ long long round_pitch(int nx) { return ((long long)nx + 2 + 31) / 32 * 32; }
 // 1024: swept 256 .. 65536 with the 512-thread tail (8191^2 2.986 -> 2.970 ms,
 // 1023^2 0.233 -> 0.219 ms, 63^2 cycle 0.060 -> 0.056 ms against 4096)
 constexpr long long TAIL_POINTS = 1024;
+// levels above the tail with at most this many unknowns run the tile legs (kernels_tile.cu);
+// BMG_TILE_POINTS overrides (0: none)
+constexpr long long TILE_POINTS = 70000;  // swept 0 .. 1.1e6 (tools/tile_sweep.py): 255^2 and below
 
 }  // namespace
 
@@ -317,6 +320,11 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
                 tp.lv[l].u = h->lv[l].u;
                 tp.lv[l].r = h->lv[l].r;
             }
+            // every tail level in shared memory when it fits (k_tail_sm); BMG_TAIL_SM=0: k_tail
+            const char *tsm = getenv("BMG_TAIL_SM");
+            if (!(tsm && atoi(tsm) == 0))
+                tail_plan_smem(tp, h->nco, 200 * 1024 / 8);
+            h->tail_sm = tp.sm_doubles;
             double *d = nullptr;
             TRY(dalloc(h, &d, sizeof(TailPlan) / sizeof(double) + 1));
             CK(cudaMemcpyAsync(d, &tp, sizeof(TailPlan), cudaMemcpyHostToDevice, s));
@@ -324,11 +332,26 @@ static bmg_status_t setup_impl(bmg_solver *h, const bmg_stencil_t *st, cudaStrea
             h->tail_l0 = l0;
         }
     }
+    // small levels above the tail: the shared-memory tile legs
+    if (h->prm.fused && h->prm.relax == BMG_RELAX_POINT && !h->prm.affine) {
+        long long lim = TILE_POINTS;
+        if (const char *e = getenv("BMG_TILE_POINTS"))  // tuning knob (bench sweeps)
+            lim = atoll(e);
+        for (int l = 0; l + 1 < h->L && l < 32 && l < h->tail_l0; l++) {
+            Level &v = h->lv[l];
+            if ((long long)v.nx * v.ny <= lim && tile_supported(v.kind, h->prm.nu1, h->prm.nu2)) {
+                h->tile[l] = true;
+                h->fplan.tmp[l] = v.r;  // ping-pong partner, as for a fused level (ring zero)
+            }
+        }
+    }
     // fused streaming plan + ping-pong partner of u for every fused level above the tail
     for (int l = 0; l + 1 < h->L && l < 32 && l < h->tail_l0; l++) {
         Level &v = h->lv[l];
         if (!h->prm.fused || h->prm.relax != BMG_RELAX_POINT || h->prm.affine)
             break;
+        if (h->tile[l])
+            continue;
         TRY(fused_plan_level(h->fplan, l, v.nx, v.ny, v.pitch, v.kind, h->prm.nu1, h->prm.nu2, (v.pitch & 1) == 0,
                              h->prm.cycle_sym == 1));
         LevelPlan &lp = h->fplan.lv[l];
@@ -387,6 +410,8 @@ static bool use_fused(bmg_solver *h, int l, const void *f, const void *uin, cons
 {
     if (!h->prm.fused || l >= 32 || l + 1 >= h->L)
         return false;
+    if (h->tile[l])
+        return uin != uout && f && uout;
     const LevelPlan &lp = h->fplan.lv[l];
     return lp.down && lp.up && al16(f) && al16(uin) && al16(uout) && uin != uout;
 }
@@ -415,6 +440,12 @@ static void enqueue_down(bmg_solver *h, int l, bool fused, const double *f, cons
                          double *fc, double *uc, cudaStream_t s, int *n)
 {
     Level &v = h->lv[l];
+    if (fused && h->tile[l]) {
+        TileArgs t{v.op(), h->civ(l), f, uin, nullptr, uout, fc, uc, uin == nullptr};
+        launch_tile_down(t, h->prm.nu1, s);
+        *n += 1;
+        return;
+    }
     if (fused && fused_down(h->fplan, l, v.op(), h->civ(l), f, uin, uout, fc, uc, s, n))
         return;
     if (fused && uout == v.r) {  // the per-step path would need r, which is T here
@@ -437,6 +468,12 @@ static void enqueue_up(bmg_solver *h, int l, bool fused, const double *f, const 
                        double *uout, cudaStream_t s, int *n)
 {
     Level &v = h->lv[l];
+    if (fused && h->tile[l]) {
+        TileArgs t{v.op(), h->civ(l), f, uin, ec, uout, nullptr, nullptr, 0};
+        launch_tile_up(t, h->prm.nu2, h->prm.cycle_sym == 1, s);
+        *n += 1;
+        return;
+    }
     if (fused && fused_up(h->fplan, l, v.op(), h->civ(l), f, uin, ec, 0, h->lv[l + 1].ny + 2, uout, s, n))
         return;
     copy_level(h, l, uout, uin, s);
@@ -503,7 +540,7 @@ static int enqueue_cycle(bmg_solver *h, const double *f0, double *u0, cudaStream
     if (rec_here)
         cudaEventRecordWithFlags(rec[0], s, cudaEventRecordExternal);
     if (h->tail) {
-        launch_tail(h->tail, h->nco, F(0), U(0), s);
+        launch_tail(h->tail, h->nco, F(0), U(0), s, h->tail_sm);
         n += 1;
     } else {
         Level &c = h->lv[L - 1];

@@ -96,6 +96,44 @@ __device__ __forceinline__ double rcp_pos(double b)
     return fma(r, fma(-b, r, 1.0), r);
 }
 
+// (P e) at fine interior point (i, j) (DESIGN §3 c7); e's ring is 0.
+__device__ __forceinline__ double interp_pt(const CIv &ci, const double *__restrict__ e, int i, int j)
+{
+    long long C = ci.pitch;
+    int I = (i + 1) >> 1, J = (j + 1) >> 1;  // storage index of X/Y/Z weights; C point: (i/2, j/2)
+    long long c = J * C + I;
+    double s;
+    if (!(i & 1) && !(j & 1)) {
+        s = e[(j >> 1) * C + (i >> 1)];
+    } else if ((i & 1) && !(j & 1)) {  // X at (2I-1, 2J): J = j/2
+        c = (j >> 1) * C + I;
+        s = ci.w[CI_LL][c] * e[c - 1];
+        s += ci.w[CI_LR][c] * e[c];
+    } else if (!(i & 1) && (j & 1)) {  // Y at (2I, 2J-1): I = i/2
+        c = J * C + (i >> 1);
+        s = ci.w[CI_LB][c] * e[c - C];
+        s += ci.w[CI_LA][c] * e[c];
+    } else {  // Z
+        s = ci.w[CI_LSW][c] * e[c - C - 1];
+        s += ci.w[CI_LSE][c] * e[c - C];
+        s += ci.w[CI_LNW][c] * e[c - 1];
+        s += ci.w[CI_LNE][c] * e[c];
+    }
+    return s;
+}
+
+// The legs of the small levels, by tiles in shared memory (kernels_tile.cu)
+struct TileArgs {
+    Op A;
+    CIv ci;                       // weights to the next level
+    const double *f, *uin, *ec;   // uin: start (down: nullptr with uzero), ec: coarse correction (up)
+    double *uout, *fc, *uc;       // uc: the next level's zero start (nullptr: not read there)
+    int uzero;
+};
+bool tile_supported(int kind, int nu1, int nu2);
+void launch_tile_down(const TileArgs &t, int nu1, cudaStream_t s);
+void launch_tile_up(const TileArgs &t, int nu2, bool rev, cudaStream_t s);
+
 // CTA-wide sum in a fixed tree (warp shuffles, then one warp over the warp
 // sums): the deterministic reduction of the norms and dot products.
 __device__ __forceinline__ double block_sum(double v)
@@ -198,15 +236,23 @@ struct TailLevel {
     Op A;
     CIv ci;                // weights to level l+1 (unused on L-1)
     double *f, *u, *r;     // level arrays (l > 0); r: residual scratch
+    // shared-memory copy (k_tail_sm): compact pitch nx+2; offsets in doubles of u, f, r,
+    // the plane block and the 8 weight planes (on level l+1's compact grid)
+    int so_u, so_f, so_r, so_pl, so_ci;
 };
 struct TailPlan {
     int l0, L, nu1, nu2;
     int cycle_sym;         // 1: post-smoother colours reversed (c12)
     int affine;            // 1: affine interpolation-correction with the level's r (c14)
     const double *chol;    // coarsest Cholesky factor
+    int sm_doubles;        // k_tail_sm: shared memory (0: the levels do not fit, k_tail runs)
+    int so_chol, so_b;     // k_tail_sm: the Cholesky factor and the solve's scratch
     TailLevel lv[32];
 };
-void launch_tail(const TailPlan *tp_dev, int ncoarse, const double *f0, double *u0, cudaStream_t s);
+// fills the so_* fields and sm_doubles (host); returns false if they exceed `limit` doubles
+bool tail_plan_smem(TailPlan &tp, int ncoarse, long long limit);
+void launch_tail(const TailPlan *tp_dev, int ncoarse, const double *f0, double *u0, cudaStream_t s,
+                 int sm_doubles = 0);
 
 // Device-side solve loop (bmg_solve): state read and advanced by k_solve_step,
 // the last node of the body of a conditional WHILE graph node.

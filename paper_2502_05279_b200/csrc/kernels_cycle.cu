@@ -6,6 +6,8 @@
 // reads its operands once and writes its outputs once.  They run every level
 // in the unfused mode and the small levels in the fused mode; the fused
 // streaming kernels for large levels are in kernels_fused.cu.
+#include <mutex>
+
 #include "bmg_internal.cuh"
 
 namespace bmg {
@@ -195,32 +197,6 @@ void launch_restrict(const Op &A, const CIv &ci, const double *r, double *fc, do
 {
     dim3 b(32, 8), g((A.nx / 2 + 2 + 31) / 32, (A.ny / 2 + 2 + 7) / 8);
     k_restrict<<<g, b, 0, s>>>(A, ci, r, fc, uc, vanish);
-}
-
-// (P e) at fine interior point (i, j) (DESIGN §3 c7); e's ring is 0.
-__device__ __forceinline__ double interp_pt(const CIv &ci, const double *__restrict__ e, int i, int j)
-{
-    long long C = ci.pitch;
-    int I = (i + 1) >> 1, J = (j + 1) >> 1;  // storage index of X/Y/Z weights; C point: (i/2, j/2)
-    long long c = J * C + I;
-    double s;
-    if (!(i & 1) && !(j & 1)) {
-        s = e[(j >> 1) * C + (i >> 1)];
-    } else if ((i & 1) && !(j & 1)) {  // X at (2I-1, 2J): J = j/2
-        c = (j >> 1) * C + I;
-        s = ci.w[CI_LL][c] * e[c - 1];
-        s += ci.w[CI_LR][c] * e[c];
-    } else if (!(i & 1) && (j & 1)) {  // Y at (2I, 2J-1): I = i/2
-        c = J * C + (i >> 1);
-        s = ci.w[CI_LB][c] * e[c - C];
-        s += ci.w[CI_LA][c] * e[c];
-    } else {  // Z
-        s = ci.w[CI_LSW][c] * e[c - C - 1];
-        s += ci.w[CI_LSE][c] * e[c - C];
-        s += ci.w[CI_LNW][c] * e[c - 1];
-        s += ci.w[CI_LNE][c] * e[c];
-    }
-    return s;
 }
 
 // c14 affine term at a non-coarse fine point: r / a_O (0 at C points and without r)
@@ -598,10 +574,19 @@ __device__ __forceinline__ void tail_relax(const Op &A, const double *f, double 
 #ifndef BMG_TAIL_THREADS
 #define BMG_TAIL_THREADS 512  // 1024 spilled (64 registers); 512: none, config-1 cycle 68 -> 60 us
 #endif
-__global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail(const TailPlan *__restrict__ tp, const double *f0,
+__global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail(const TailPlan *__restrict__ tpg0, const double *f0,
                                                               double *u0)
 {
     extern __shared__ double b[];
+    __shared__ TailPlan tp_s;  // the plan in shared memory (one L2 read instead of one per phase)
+    {
+        const int *src = reinterpret_cast<const int *>(tpg0);
+        int *dst = reinterpret_cast<int *>(&tp_s);
+        for (int e = threadIdx.x; e < (int)(sizeof(TailPlan) / sizeof(int)); e += blockDim.x)
+            dst[e] = src[e];
+        __syncthreads();
+    }
+    const TailPlan *tp = &tp_s;
     const int l0 = tp->l0, L = tp->L, nt = blockDim.x;
     auto F = [&](int l) { return l == 0 ? f0 : (const double *)tp->lv[l].f; };
     auto U = [&](int l) { return l == 0 ? u0 : tp->lv[l].u; };
@@ -654,8 +639,203 @@ __global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail(const TailPlan *__
     }
 }
 
-void launch_tail(const TailPlan *tp_dev, int ncoarse, const double *f0, double *u0, cudaStream_t s)
+// ---- the tail with every level in SHARED memory: the small levels'
+// operators, weights and the Cholesky factor are copied in once (cp.async, all in
+// flight), level l0's f and u too; each phase then works in shared memory, and only
+// level l0's u goes back.  The k_tail phases each paid an L2 round trip (~0.7 us),
+// the coarse solve one per substitution step.  Same per-point functions (on Op / CIv
+// views of the shared copies), so the iterate is bitwise k_tail's.
+bool tail_plan_smem(TailPlan &tp, int ncoarse, long long limit)
 {
+    long long off = 0;
+    auto take = [&](long long n) {
+        long long o = off;
+        off += (n + 1) / 2 * 2;  // 16-byte aligned pieces
+        return (int)o;
+    };
+    for (int l = tp.l0; l < tp.L; l++) {
+        TailLevel &v = tp.lv[l];
+        const long long np = (long long)(v.A.ny + 2) * (v.A.nx + 2);
+        v.so_u = take(np);
+        v.so_f = take(np);
+        v.so_r = take(np);
+        v.so_pl = take(np * (v.A.kind == 9 ? 5 : 3));
+        if (l + 1 < tp.L) {
+            const TailLevel &c = tp.lv[l + 1];
+            v.so_ci = take(8LL * (c.A.ny + 2) * (c.A.nx + 2));
+        }
+    }
+    tp.so_chol = take((long long)ncoarse * ncoarse);
+    tp.so_b = take(ncoarse > 0 ? ncoarse : 1);
+    tp.sm_doubles = (int)off;
+    if (off > limit) {
+        tp.sm_doubles = 0;
+        return false;
+    }
+    return true;
+}
+
+__device__ __forceinline__ void tail_cp8(double *dst, const double *src)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+
+// copy rows 0..ny+1, cols 0..nx+1 of a pitched array into the compact shared copy
+__device__ __forceinline__ void tail_stage(double *dst, const double *src, long long pitch, int nx, int ny)
+{
+    const int w = nx + 2, n = w * (ny + 2);
+    for (int e = threadIdx.x; e < n; e += blockDim.x)
+        tail_cp8(dst + e, src + (long long)(e / w) * pitch + e % w);
+}
+
+__global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail_sm(const TailPlan *__restrict__ tpg0, const double *f0,
+                                                                 double *u0)
+{
+    extern __shared__ __align__(16) double tsm[];
+    // the plan itself in shared memory: every phase reads its level's views from it, and a
+    // global (L2) read per phase would cost more than the phase's work
+    __shared__ TailPlan tp_s;
+    {
+        const int *src = reinterpret_cast<const int *>(tpg0);
+        int *dst = reinterpret_cast<int *>(&tp_s);
+        for (int e = threadIdx.x; e < (int)(sizeof(TailPlan) / sizeof(int)); e += blockDim.x)
+            dst[e] = src[e];
+        __syncthreads();
+    }
+    const TailPlan *tpg = &tp_s;
+    const int l0 = tpg->l0, L = tpg->L, nt = blockDim.x;
+    const int nu1 = tpg->nu1, nu2 = tpg->nu2, rev = tpg->cycle_sym, affine = tpg->affine;
+    // copy in: operators and weights of every level, f and u of level l0, the factor
+    for (int l = l0; l < L; l++) {
+        const TailLevel &v = tpg->lv[l];
+        const Op A = v.A;
+        const long long np = (long long)(A.ny + 2) * (A.nx + 2);
+        const double *pls[5] = {A.O, A.W, A.S, A.SW, A.NW};
+        for (int k = 0; k < (A.kind == 9 ? 5 : 3); k++)
+            tail_stage(tsm + v.so_pl + k * np, pls[k], A.pitch, A.nx, A.ny);
+        if (l == l0) {
+            tail_stage(tsm + v.so_f, l0 == 0 ? f0 : v.f, A.pitch, A.nx, A.ny);
+            tail_stage(tsm + v.so_u, l0 == 0 ? u0 : v.u, A.pitch, A.nx, A.ny);
+        }
+        if (l + 1 < L) {
+            const Op Ac = tpg->lv[l + 1].A;
+            const long long npc = (long long)(Ac.ny + 2) * (Ac.nx + 2);
+            for (int k = 0; k < 8; k++)
+                tail_stage(tsm + v.so_ci + k * npc, v.ci.w[k], v.ci.pitch, Ac.nx, Ac.ny);
+        }
+    }
+    {
+        const Op Ac = tpg->lv[L - 1].A;
+        const int n = Ac.nx * Ac.ny;
+        for (int e = threadIdx.x; e < n * n; e += nt)
+            tail_cp8(tsm + tpg->so_chol + e, tpg->chol + e);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    // Op / CIv views of the shared copies
+    auto opv = [&](int l) {
+        const TailLevel &v = tpg->lv[l];
+        Op A = v.A;
+        const long long np = (long long)(A.ny + 2) * (A.nx + 2);
+        A.pitch = A.nx + 2;
+        A.O = tsm + v.so_pl;
+        A.W = tsm + v.so_pl + np;
+        A.S = tsm + v.so_pl + 2 * np;
+        A.SW = A.kind == 9 ? tsm + v.so_pl + 3 * np : nullptr;
+        A.NW = A.kind == 9 ? tsm + v.so_pl + 4 * np : nullptr;
+        return A;
+    };
+    auto civ = [&](int l) {
+        const TailLevel &v = tpg->lv[l];
+        const Op Ac = tpg->lv[l + 1].A;
+        const long long npc = (long long)(Ac.ny + 2) * (Ac.nx + 2);
+        CIv c;
+        c.pitch = Ac.nx + 2;
+        c.roff = 0;
+        c.nrows = Ac.ny + 2;
+        for (int k = 0; k < 8; k++)
+            c.w[k] = tsm + v.so_ci + k * npc;
+        return c;
+    };
+    auto U = [&](int l) { return tsm + tpg->lv[l].so_u; };
+    auto F = [&](int l) { return tsm + tpg->lv[l].so_f; };
+    auto R = [&](int l) { return tsm + tpg->lv[l].so_r; };
+    for (int l = l0; l + 1 < L; l++) {
+        const Op A = opv(l);
+        const CIv ci = civ(l);
+        double *u = U(l), *r = R(l);
+        const double *f = F(l);
+        if (A.kind == 5)
+            tail_relax<5>(A, f, u, nu1, false);
+        else
+            tail_relax<9>(A, f, u, nu1, false);
+        const int wx = A.nx + 2, cnt = wx * (A.ny + 2);
+        for (int k = threadIdx.x; k < cnt; k += nt) {
+            const int j = k / wx, i = k % wx;
+            r[(long long)j * A.pitch + i] =
+                (i == 0 || j == 0 || i > A.nx || j > A.ny) ? 0.0 : residual_pt(A, f, u, i, j);
+        }
+        __syncthreads();
+        const int cx = A.nx / 2 + 2, ccnt = cx * (A.ny / 2 + 2);
+        for (int k = threadIdx.x; k < ccnt; k += nt)
+            restrict_store(A, ci, r, F(l + 1), U(l + 1), k % cx, k / cx, nu1 > 0);
+        __syncthreads();
+    }
+    {
+        const Op Ac = opv(L - 1);
+        if (Ac.nx * Ac.ny <= 32) {
+            if (threadIdx.x < 32)
+                coarse_solve_warp(Ac, tsm + tpg->so_chol, F(L - 1), U(L - 1));
+        } else {
+            coarse_solve_cta(Ac, tsm + tpg->so_chol, F(L - 1), U(L - 1), tsm + tpg->so_b);
+        }
+    }
+    __syncthreads();
+    for (int l = L - 2; l >= l0; l--) {
+        const Op A = opv(l);
+        const CIv ci = civ(l);
+        double *u = U(l);
+        const double *e = U(l + 1);
+        const int cnt = A.nx * A.ny;
+        for (int k = threadIdx.x; k < cnt; k += nt) {
+            const int j = k / A.nx + 1, i = k % A.nx + 1;
+            double s = interp_pt(ci, e, i, j);
+            if (affine)
+                s += affine_pt(A, R(l), i, j);
+            u[(long long)j * A.pitch + i] += s;
+        }
+        __syncthreads();
+        if (A.kind == 5)
+            tail_relax<5>(A, F(l), u, nu2, rev);
+        else
+            tail_relax<9>(A, F(l), u, nu2, rev);
+    }
+    // level l0's iterate back to its array
+    {
+        const TailLevel &v = tpg->lv[l0];
+        double *ug = l0 == 0 ? u0 : v.u;
+        const int nx = v.A.nx, cnt = nx * v.A.ny;
+        const double *us = U(l0);
+        for (int k = threadIdx.x; k < cnt; k += nt) {
+            const int j = k / nx + 1, i = k % nx + 1;
+            ug[(long long)j * v.A.pitch + i] = us[j * (nx + 2) + i];
+        }
+    }
+}
+
+void launch_tail(const TailPlan *tp_dev, int ncoarse, const double *f0, double *u0, cudaStream_t s, int sm_doubles)
+{
+    if (sm_doubles > 0) {
+        static std::once_flag once[64];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::call_once(once[dev & 63], []() {
+            cudaFuncSetAttribute(k_tail_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
+        });
+        k_tail_sm<<<1, BMG_TAIL_THREADS, sizeof(double) * sm_doubles, s>>>(tp_dev, f0, u0);
+        return;
+    }
     k_tail<<<1, BMG_TAIL_THREADS, sizeof(double) * (ncoarse > 0 ? ncoarse : 1), s>>>(tp_dev, f0, u0);
 }
 

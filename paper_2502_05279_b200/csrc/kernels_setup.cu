@@ -342,27 +342,39 @@ __global__ void __launch_bounds__(RAP_TC *RAP_TR) k_rap_tiled(Op A, CIv ci, int 
     RapSm &sm = *reinterpret_cast<RapSm *>(rap_raw);
     const int I0 = blockIdx.x * RAP_TC + 1, Jt = J0 + blockIdx.y * RAP_TR;
     const int tid = threadIdx.x;
-    // stage the fine planes (zero outside the stored rows / the padded grid)
+    // stage the fine planes and the weights (zero outside the stored rows / the padded
+    // grid): one warp per row, lanes along it -- no index divisions, constant plane indices
     const int fx0 = 2 * I0 - 1, fy0 = 2 * Jt - 2;
     const int ylo = max(A.roff, 0), yhi = min(A.ny + 1, A.roff + A.nrows - 1);
-    const int kpl = A.kind == 9 ? 5 : 3;
-    const double *pls[5] = {A.O, A.W, A.S, A.SW, A.NW};
-    for (int e = tid; e < 5 * RAP_FH * RAP_FW; e += blockDim.x) {
-        const int k = e / (RAP_FH * RAP_FW), r = (e / RAP_FW) % RAP_FH, c = e % RAP_FW;
-        const int gy = fy0 + r, gx = fx0 + c;
-        double v = 0.0;
-        if (k < kpl && gy >= ylo && gy <= yhi && gx >= 0 && gx <= A.nx + 1)
-            v = pls[k][(long long)gy * A.pitch + gx];
-        sm.pl[k][r][c] = v;
-    }
+    const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+    auto stage_plane = [&](const double *src, double (*dst)[RAP_FW]) {
+        for (int r = warp; r < RAP_FH; r += nw) {
+            const int gy = fy0 + r;
+            const bool rin = src && gy >= ylo && gy <= yhi;
+            const double *row = rin ? src + (long long)gy * A.pitch : nullptr;
+            for (int c = lane; c < RAP_FW; c += 32) {
+                const int gx = fx0 + c;
+                dst[r][c] = (rin && gx <= A.nx + 1) ? row[gx] : 0.0;
+            }
+        }
+    };
+    stage_plane(A.O, sm.pl[0]);
+    stage_plane(A.W, sm.pl[1]);
+    stage_plane(A.S, sm.pl[2]);
+    stage_plane(A.kind == 9 ? A.SW : nullptr, sm.pl[3]);
+    stage_plane(A.kind == 9 ? A.NW : nullptr, sm.pl[4]);
     const int cylo = max(ci.roff, 0), cyhi = min(ncy + 1, ci.roff + ci.nrows - 1);
-    for (int e = tid; e < 8 * RAP_CH * RAP_CW; e += blockDim.x) {
-        const int k = e / (RAP_CH * RAP_CW), r = (e / RAP_CW) % RAP_CH, c = e % RAP_CW;
-        const int cy = Jt - 1 + r, cx = I0 - 1 + c;
-        double v = 0.0;
-        if (cy >= cylo && cy <= cyhi && cx >= 0 && cx <= ncx + 1)
-            v = ci.w[k][(long long)cy * ci.pitch + cx];
-        sm.ci[k][r][c] = v;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const double *src = ci.w[k];
+        for (int r = warp; r < RAP_CH; r += nw) {
+            const int cy = Jt - 1 + r;
+            const bool rin = cy >= cylo && cy <= cyhi;
+            for (int c = lane; c < RAP_CW; c += 32) {
+                const int cx = I0 - 1 + c;
+                sm.ci[k][r][c] = (rin && cx <= ncx + 1) ? src[(long long)cy * ci.pitch + cx] : 0.0;
+            }
+        }
     }
     __syncthreads();
     const int tx = tid % RAP_TC, ty = tid / RAP_TC;

@@ -123,7 +123,9 @@ struct bmg_solver {
     double *solve_hist = nullptr;     // device history, solve_cap doubles
     int solve_cap = 0;
     int tail_l0 = 1 << 30;            // first level of the tail kernel (none: > L)
+    bool tile[32] = {};               // level runs the shared-memory tile legs (kernels_tile.cu)
     TailPlan *tail = nullptr;         // its device-side plan
+    int tail_sm = 0;                  // > 0: k_tail_sm with this many doubles of shared memory
     bool timing = false;              // bmg_timing: timed graph variant, event pair per launch
     bool cycle_err = false;           // a planned fused leg was rejected while enqueuing a cycle
     std::vector<cudaEvent_t> tev;     // event pairs (start, end) per recorded launch
