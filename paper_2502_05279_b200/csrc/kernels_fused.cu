@@ -401,6 +401,86 @@ __device__ __forceinline__ void colour_pass(double *sm, int s0, int sm1, int sp1
         colour_pass<KIND, AM, WD, PPT, 0>(sm, s0, sm1, sp1, k);
 }
 
+// The two colour phases of a 9-point row stage (forward order: even columns, then odd),
+// phase B reusing what phase A of the same thread already holds.  A thread owns the
+// column pair (2h, 2h+1): phase A updates 2h, phase B 2h+1, and B's operands include
+// A's u at rows r-1 and r+1 (columns 2h, 2h+1), A's own new value u(2h) and the coupling
+// W(2h+1) (= E of 2h): 6 of B's 18 shared-memory loads.  Same terms in the same order
+// as colour_pass, so the same bits.  `bar`: the group's named barrier (B reads A's
+// results of the neighbouring lanes).
+template <int AM, int WD, int PPT>
+__device__ __forceinline__ void colour_pair9(double *sm, int s0, int sm1, int sp1, const Cols<PPT> &k, int bar,
+                                             int nthreads)
+{
+    constexpr int HW = WD / 2, OI = 7;
+    const int b0 = s0 * WD, bm = sm1 * WD, bp = sp1 * WD;
+    double keep[PPT][6];  // u(r-1,2h), u(r-1,2h+1), u(r+1,2h), u(r+1,2h+1), W(2h+1), new u(2h)
+#pragma unroll
+    for (int p = 0; p < PPT; p++) {
+        const Col c = k.c[0][p];  // same = h, left = HW+h-1 (2h-1), right = HW+h (2h+1)
+        double a[8], u[8];
+        a[0] = sm[A_SW * AM + b0 + c.same];
+        u[0] = sm[A_U * AM + bm + c.left];
+        a[1] = sm[A_S * AM + b0 + c.same];
+        u[1] = sm[A_U * AM + bm + c.same];
+        a[2] = sm[A_NW * AM + bm + c.right];
+        u[2] = sm[A_U * AM + bm + c.right];
+        a[3] = sm[A_W * AM + b0 + c.same];
+        u[3] = sm[A_U * AM + b0 + c.left];
+        a[4] = sm[A_W * AM + b0 + c.right];
+        u[4] = sm[A_U * AM + b0 + c.right];
+        a[5] = sm[A_NW * AM + b0 + c.same];
+        u[5] = sm[A_U * AM + bp + c.left];
+        a[6] = sm[A_S * AM + bp + c.same];
+        u[6] = sm[A_U * AM + bp + c.same];
+        a[7] = sm[A_SW * AM + bp + c.right];
+        u[7] = sm[A_U * AM + bp + c.right];
+        const double f = sm[A_F * AM + b0 + c.same], o = sm[OI * AM + b0 + c.same];
+        double acc = a[0] * u[0];
+#pragma unroll
+        for (int q = 1; q < 8; q++)
+            acc += a[q] * u[q];
+        const double v = (f - acc) * o;
+        if (k.on[0][p])
+            sm[A_U * AM + b0 + c.same] = v;
+        keep[p][0] = u[1];
+        keep[p][1] = u[2];
+        keep[p][2] = u[6];
+        keep[p][3] = u[7];
+        keep[p][4] = a[4];
+        keep[p][5] = k.on[0][p] ? v : sm[A_U * AM + b0 + c.same];
+    }
+    group_sync(bar, nthreads);
+#pragma unroll
+    for (int p = 0; p < PPT; p++) {
+        const Col c = k.c[1][p];  // same = HW+h (2h+1), left = h (2h), right = h+1 (2h+2)
+        double a[8], u[8];
+        a[0] = sm[A_SW * AM + b0 + c.same];
+        u[0] = keep[p][0];
+        a[1] = sm[A_S * AM + b0 + c.same];
+        u[1] = keep[p][1];
+        a[2] = sm[A_NW * AM + bm + c.right];
+        u[2] = sm[A_U * AM + bm + c.right];
+        a[3] = keep[p][4];
+        u[3] = keep[p][5];
+        a[4] = sm[A_W * AM + b0 + c.right];
+        u[4] = sm[A_U * AM + b0 + c.right];
+        a[5] = sm[A_NW * AM + b0 + c.same];
+        u[5] = keep[p][2];
+        a[6] = sm[A_S * AM + bp + c.same];
+        u[6] = keep[p][3];
+        a[7] = sm[A_SW * AM + bp + c.right];
+        u[7] = sm[A_U * AM + bp + c.right];
+        const double f = sm[A_F * AM + b0 + c.same], o = sm[OI * AM + b0 + c.same];
+        double acc = a[0] * u[0];
+#pragma unroll
+        for (int q = 1; q < 8; q++)
+            acc += a[q] * u[q];
+        if (k.on[1][p])
+            sm[A_U * AM + b0 + c.same] = (f - acc) * o;
+    }
+}
+
 // De-interleave staging row (natural order, slot ss) into main ring row (slot s0)
 // for arrays [q0, q1): even columns to the first half, odd to the second.
 // DI: also form 1/a_pp (rcp_pos) into main-ring array NA.
@@ -689,15 +769,11 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
                 // 9-point stage k is active at step t iff (t - 2k) & 1 == (k - 1) & 1, i.e. (t + k) odd
                 const int k = grp + 1, d = 2 * k, r = t - d;
                 const bool act = ((t + k) & 1) && r > lo && r < hi && r >= 1 && r <= ny;
-                if (act) {  // uniform over the group
-                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), 0,
-                                                   kc);
-                    group_sync(1 + grp, NPG);  // phase B reads phase A's neighbours
-                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), 1,
-                                                   kc);
-                    // no trailing barrier: the group's next active step (two steps on) works
-                    // two rows higher; consumers wait on the per-warp ring arrivals
-                }
+                if (act)  // uniform over the group; phase B waits on the group's barrier inside.
+                    // No trailing barrier: the group's next active step (two steps on) works two
+                    // rows higher; consumers wait on the per-warp ring arrivals
+                    colour_pair9<AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), kc,
+                                              1 + grp, NPG);
             }
         } else if (grp < G_STORE) {
             rg.wait(R_RES, t - 1);
@@ -946,11 +1022,16 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
                 const int k = grp - G_ST0 + 1, d = 2 * k + 1, r = t - d;
                 const bool act = (((t + k) & 1) == (REV ? 1 : 0)) && r > lo && r < hi && r >= 1 && r <= ny;
                 if (act) {  // uniform over the group
-                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1),
-                                                   REV ? 1 : 0, kc);
-                    group_sync(1 + grp, NPG);
-                    colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1),
-                                                   REV ? 0 : 1, kc);
+                    if (REV) {
+                        colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1),
+                                                       1, kc);
+                        group_sync(1 + grp, NPG);
+                        colour_pass<KIND, AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1),
+                                                       0, kc);
+                    } else {
+                        colour_pair9<AM, WD, PPT>(sm, back<RM>(tm, d), back<RM>(tm, d + 1), back<RM>(tm, d - 1), kc,
+                                                  1 + grp, NPG);
+                    }
                 }
             }
         } else {
@@ -1035,9 +1116,15 @@ struct Inst {
 #define BMG_PPT9DN 1
 #endif
     static constexpr int PPT_DN = KIND == 5 ? BMG_PPT5 : BMG_PPT9DN;
-    static constexpr int WD_UP = KIND == 5 ? BMG_WD5 : (NS == 4 ? 192 : BMG_WD9UP);
+#ifndef BMG_WD5UP
+#define BMG_WD5UP BMG_WD5
+#endif
+#ifndef BMG_PPT5UP
+#define BMG_PPT5UP BMG_PPT5
+#endif
+    static constexpr int WD_UP = KIND == 5 ? BMG_WD5UP : (NS == 4 ? 192 : BMG_WD9UP);
 
-    static constexpr int PPT_UP = KIND == 5 ? BMG_PPT5 : (NS == 4 ? 1 : 2);
+    static constexpr int PPT_UP = KIND == 5 ? BMG_PPT5UP : (NS == 4 ? 1 : 2);
 #ifndef BMG_E5DN
 #define BMG_E5DN 0
 #endif
