@@ -1117,7 +1117,8 @@ struct Inst {
 #endif
     static constexpr int PPT_DN = KIND == 5 ? BMG_PPT5 : BMG_PPT9DN;
 #ifndef BMG_WD5UP
-#define BMG_WD5UP BMG_WD5
+#define BMG_WD5UP 128  // 5-point up leg: 128-column strips (2 CTAs/SM); swept 64..256 x 1..4 pairs,
+                       // 8191^2 up leg 0.826 -> 0.815 ms against 256
 #endif
 #ifndef BMG_PPT5UP
 #define BMG_PPT5UP BMG_PPT5

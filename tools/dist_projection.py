@@ -12,7 +12,8 @@ On P GPUs each rank runs its slab concurrently, so the per-cycle time is about
 T_exch = 2K grouped NCCL ghost-row exchanges (8191^2, P=8: K levels; each a
 one-row-per-neighbour send/recv over NVLink) + one all-gather of level K's rhs --
 NOT measured here (one GPU); the printed projection takes them as a parameter.
-Prints one JSON line.
+Also the weak-scaling counterpart (BASELINE config 5: 4095 x 4096P-1 global, ~4096 rows
+x nx per GPU): E = T(1) / T_P.  Prints one JSON line.
 """
 import json
 import os
@@ -68,4 +69,36 @@ for nr in (2, 4, 8):
     out[f"p{nr}"] = {"kdist": K, "loopback_ms": t_lb, "inner_ms": t_in, "slabs_ms": slabs,
                      "slab_overhead_vs_single": slabs / (out["single_ms"] - t_in) if out["single_ms"] > t_in else None,
                      "projected_ms": t_p, "projected_efficiency": out["single_ms"] / (nr * t_p)}
+# weak scaling (BASELINE config 5): ~4096 rows x nx per GPU, 512-cell 1e6 checkerboard
+if os.environ.get("WEAK", "1") == "1":
+    weak = {}
+    t1 = None
+    for nr, (gx, gy) in ((1, (4095, 4095)), (2, (4095, 8191)), (4, (8191, 8191)), (8, (8191, 16383))):
+        stw = P.workload("checker512", gx, gy)
+        fw = P.rhs_const(gx, gy)
+        if nr == 1:
+            s1 = bmg.Solver(stw)
+            a, b = s1.grid(fw), s1.grid()
+            t1 = time_cycles(lambda: s1.vcycle(a, b, 1))
+            s1.close()
+            weak["p1"] = {"global": [gx, gy], "single_ms": t1}
+            continue
+        yb, K = bmg.bmg_partition(gx, gy, nr, prm)
+        d = D.DistSolver(stw, nr, 0, None, params=prm, loopback=True)
+        a, b = d.local(fw), d.local()
+        t_lb = time_cycles(lambda: d.vcycle(a, b, 1), ncyc=10)
+        d.close()
+        del d, a, b
+        torch.cuda.empty_cache()
+        ix, iy = gx >> K, gy >> K
+        si = bmg.Solver(P.workload("checker512", ix, iy))
+        fi, xi = si.grid(P.rhs_const(ix, iy)), si.grid()
+        t_in = time_cycles(lambda: si.vcycle(fi, xi, 1))
+        si.close()
+        slabs = t_lb - t_in
+        t_p = slabs / nr + t_in + (2 * K + 1) * EXCH_US / 1e3
+        weak[f"p{nr}"] = {"global": [gx, gy], "kdist": K, "loopback_ms": t_lb, "inner_ms": t_in,
+                          "slabs_per_gpu_ms": slabs / nr, "projected_ms": t_p,
+                          "projected_weak_efficiency": t1 / t_p}
+    out["weak_config5"] = weak
 print(json.dumps(out))
