@@ -171,6 +171,8 @@ WORKLOADS3 = {
     "poisson7": (lambda n: poisson7(n), "point", "7-point Poisson, D = 1"),
     "aniso7": (lambda n: fv7(d3_constant(n, n, n), az=1e-3), "planes",
                "7-point, z-coupling 1e-3 (strong xy planes)"),
+    "checkeraniso7": (lambda n: fv7(d3_checkerboard(n, n, n, max(1, (n + 1) // 8), 1e4), az=1e-3), "planes",
+                      "7-point, 1e4 checkerboard of (n+1)/8-cell cubes, z-coupling 1e-3"),
     "checker27": (lambda n: q1_27(d3_checkerboard(n, n, n, max(1, (n + 1) // 8), 1e4)), "point",
                   "27-point Q1, 1e4 checkerboard of (n+1)/8-cell cubes"),
     "lognormal7": (lambda n: fv7(d3_lognormal(n, n, n)), "point", "7-point, lognormal D (parity)"),

@@ -91,3 +91,47 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(bmg, "LIB_PATH", str(tmp_path / "nope.so"))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         bmg.lib()
+
+
+def header3_symbols():
+    with open(os.path.join(ROOT, "include", "bmg3.h")) as fh:
+        txt = fh.read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(bmg3_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_3d_header_exports_and_binding(libbmg):
+    """include/bmg3.h: every declared entry point is exported
+    unmangled and bound by paper_2502_05279_b200/bmg3.py."""
+    import subprocess
+
+    from paper_2502_05279_b200 import bmg, bmg3
+
+    syms = header3_symbols()
+    assert set(syms) == set(bmg3.EXPORTS3)
+    out = subprocess.run(["nm", "-D", "--defined-only", bmg.LIB_PATH], capture_output=True, text=True).stdout
+    defined = {ln.split()[-1] for ln in out.splitlines() if ln.strip()}
+    for s in syms:
+        assert s in defined, s
+    bmg3.lib()
+
+
+def test_3d_host_only_validation(libbmg):
+    from paper_2502_05279_b200 import bmg, bmg3
+
+    p = bmg3.bmg3_params_default()
+    assert (p.nu1, p.nu2, p.coarsest, p.max_levels, p.relax) == (2, 1, 3, 0, 0)
+    L = bmg3.lib()
+    st = bmg3.bmg3_stencil_t()
+    st.kind, st.nx, st.ny, st.nz, st.pitch, st.plane_stride = 9, 3, 3, 3, 5, 25
+    h = ctypes.c_void_p()
+    assert L.bmg3_setup(ctypes.byref(st), None, None, ctypes.byref(h)) == bmg.BMG_EINVAL
+    st.kind, st.plane_stride = 7, 20  # plane_stride < pitch*(ny+2)
+    assert L.bmg3_setup(ctypes.byref(st), None, None, ctypes.byref(h)) == bmg.BMG_EINVAL
+    st.plane_stride = 25  # planes NULL
+    assert L.bmg3_setup(ctypes.byref(st), None, None, ctypes.byref(h)) == bmg.BMG_EINVAL
+    assert b"NULL" in L.bmg_last_error_detail()
+    d = ctypes.c_double()
+    assert L.bmg3_vcycle(None, None, None, 1, None) == bmg.BMG_EINVAL
+    assert L.bmg3_residual_norm(None, None, None, ctypes.byref(d), None) == bmg.BMG_EINVAL
+    assert L.bmg3_destroy(None) == bmg.BMG_OK
