@@ -207,7 +207,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="poisson8193", choices=sorted(CONFIGS))
+    import bench3d
+
+    ap.add_argument("--config", default="poisson8193", choices=sorted(CONFIGS) + sorted(bench3d.WORKLOAD3),
+                    help="a BASELINE config, or a 3-D line (3d-*, SURVEY 8(f) row 4; bench3d.py)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="one kernel per method step (debug/comparison)")
@@ -222,6 +225,8 @@ def main():
                     help="also time the block multi-RHS cycle (c15, bmg_vcycle_block) with K right-hand sides")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.config in bench3d.WORKLOAD3:
+        return bench3d.run3d(args, args.config, ClockSampler, measured_peaks, host_info)
     if args.impl == "reference":
         return run_reference(args, args.config)
 

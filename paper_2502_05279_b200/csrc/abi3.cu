@@ -57,6 +57,8 @@ struct Level3 {
     double *ci[26] = {};  // weights from level l+1 (its grid)
     std::vector<PLevel> pv;  // plane hierarchy (relax = planes, non-coarsest levels)
     double *pr = nullptr;    // plane level-0 residual scratch (3-D sized)
+    double *rc27 = nullptr;  // 27-point point relaxation: colour-major full rows (kernels3.cu)
+    double *tmp = nullptr;   // 7-point point relaxation: the second buffer of the one-pass sweep (k3_rb7)
     Op3 op() const
     {
         Op3 A;
@@ -219,10 +221,30 @@ void relax_planes(Level3 &v, const double *f, double *u, int nsweeps, cudaStream
         }
 }
 
+// 7-point point relaxation, nsweeps one-pass sweeps alternating between u and v.tmp,
+// starting from the iterate in `from`; returns where the result is
+double *rb7_sweeps(Level3 &v, const double *f, double *from, double *u, int nsweeps, cudaStream_t s)
+{
+    double *a = from, *b = from == u ? v.tmp : u;
+    for (int sw = 0; sw < nsweeps; sw++) {
+        launch3_rb7(v.op(), f, a, b, s);
+        std::swap(a, b);
+    }
+    return a;
+}
+
 void relax_level(bmg3_solver *h, Level3 &v, const double *f, double *u, int nsweeps, cudaStream_t s)
 {
+    if (v.tmp) {
+        double *end = rb7_sweeps(v, f, u, u, nsweeps, s);
+        if (end != u)
+            cudaMemcpyAsync(u, end, gsize(v.g) * sizeof(double), cudaMemcpyDeviceToDevice, s);
+        return;
+    }
     if (h->prm.relax == BMG3_RELAX_PLANES)
         relax_planes(v, f, u, nsweeps, s);
+    else if (v.rc27)
+        launch3_relax27c(v.g, v.rc27, f, u, nsweeps, s);
     else
         launch3_relax_point(v.op(), f, u, nsweeps, s, nullptr);
 }
@@ -233,17 +255,31 @@ void enqueue_cycle(bmg3_solver *h, const double *rhs, double *x, cudaStream_t s)
     const int L = h->L;
     auto F = [&](int l) -> const double * { return l == 0 ? rhs : h->lv[l].f; };
     auto U = [&](int l) -> double * { return l == 0 ? x : h->lv[l].u; };
+    // 7-point levels with the one-pass sweep keep the iterate in u or tmp (cur[l]);
+    // the up leg's interpolation writes where its nu2 sweeps then end in u
+    std::vector<double *> cur(L);
     for (int l = 0; l + 1 < L; l++) {
         Level3 &v = h->lv[l];
-        relax_level(h, v, F(l), U(l), h->prm.nu1, s);
-        launch3_residual(v.op(), F(l), U(l), v.r, s);
+        if (v.tmp)
+            cur[l] = rb7_sweeps(v, F(l), U(l), U(l), h->prm.nu1, s);
+        else {
+            relax_level(h, v, F(l), U(l), h->prm.nu1, s);
+            cur[l] = U(l);
+        }
+        launch3_residual(v.op(), F(l), cur[l], v.r, s);
         launch3_restrict(v.op(), ci_view(v, h->lv[l + 1]), v.r, h->lv[l + 1].f, h->lv[l + 1].u, s);
     }
     launch3_coarse_solve(h->lv[L - 1].op(), h->chol, F(L - 1), U(L - 1), s);
     for (int l = L - 2; l >= 0; l--) {
         Level3 &v = h->lv[l];
-        launch3_interp_add(v.g, ci_view(v, h->lv[l + 1]), h->lv[l + 1].u, U(l), s);
-        relax_level(h, v, F(l), U(l), h->prm.nu2, s);
+        if (v.tmp) {
+            double *start = (h->prm.nu2 % 2 == 0) ? U(l) : v.tmp;
+            launch3_interp_add(v.g, ci_view(v, h->lv[l + 1]), h->lv[l + 1].u, cur[l], start, s);
+            rb7_sweeps(v, F(l), start, U(l), h->prm.nu2, s);
+        } else {
+            launch3_interp_add(v.g, ci_view(v, h->lv[l + 1]), h->lv[l + 1].u, U(l), U(l), s);
+            relax_level(h, v, F(l), U(l), h->prm.nu2, s);
+        }
     }
 }
 
@@ -431,6 +467,21 @@ bmg_status_t bmg3_setup(const bmg3_stencil_t *st, const bmg3_params_t *params, v
         launch3_rap(v.op(), ci_view(v, c), c.pl, h->d_err, s);
         CKH(cudaGetLastError());
     }
+    // the one-pass 7-point sweep's second buffer (relaxed 7-point levels)
+    if (prm.relax == BMG3_RELAX_POINT)
+        for (int l = 0; l + 1 < h->L; l++)
+            if (h->lv[l].kind == 7)
+                TRYH(alloc(h, gsize(h->lv[l].g), &h->lv[l].tmp, s));
+    // colour-major rows for the 27-point point smoother (relaxed levels only)
+    if (prm.relax == BMG3_RELAX_POINT)
+        for (int l = 0; l + 1 < h->L; l++) {
+            Level3 &v = h->lv[l];
+            if (v.kind != 27)
+                continue;
+            TRYH(alloc(h, (size_t)relax27_doubles(v.g), &v.rc27, s));
+            launch3_build_relax27(v.op(), v.rc27, s);
+            CKH(cudaGetLastError());
+        }
     // plane hierarchies
     if (prm.relax == BMG3_RELAX_PLANES)
         for (int l = 0; l + 1 < h->L; l++) {

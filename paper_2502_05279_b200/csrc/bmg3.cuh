@@ -85,9 +85,17 @@ void launch3_rap(const Op3 &A, const CI3 &ci, double *const dst[14], int *err, c
 void launch3_assemble_dense(const Op3 &A, double *M, cudaStream_t s);
 void launch3_coarse_solve(const Op3 &A, const double *Lf, const double *f, double *u, cudaStream_t s);
 void launch3_relax_point(const Op3 &A, const double *f, double *u, int nsweeps, cudaStream_t s, int *nlaunch);
+// 27-point levels: colour-major full-row copy (relax27_doubles(g) doubles) and its sweeps
+long long relax27_doubles(const Grid3 &g);
+void launch3_build_relax27(const Op3 &A, double *cf, cudaStream_t s);
+void launch3_relax27c(const Grid3 &g, const double *cf, const double *f, double *u, int nsweeps, cudaStream_t s);
 void launch3_residual(const Op3 &A, const double *f, const double *u, double *r, cudaStream_t s);
 void launch3_restrict(const Op3 &A, const CI3 &ci, const double *r, double *fc, double *uc, cudaStream_t s);
-void launch3_interp_add(const Grid3 &fine, const CI3 &ci, const double *ec, double *u, cudaStream_t s);
+// u = uin + P ec (uin may equal u)
+void launch3_interp_add(const Grid3 &fine, const CI3 &ci, const double *ec, const double *uin, double *u,
+                        cudaStream_t s);
+// 7-point levels: one red-black sweep uout = GS(uin) in one pass (uin != uout)
+void launch3_rb7(const Op3 &A, const double *f, const double *uin, double *uout, cudaStream_t s);
 // ||f - A u||_2 (or ||g||_2 when A == nullptr: pass f = g, u = nullptr) into *result (device)
 void launch3_resid_norm(const Op3 *A, const Grid3 &g, const double *f, const double *u, double *partials,
                         double *result, cudaStream_t s);

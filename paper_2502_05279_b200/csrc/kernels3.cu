@@ -3,6 +3,10 @@
 // RAP, coarsest dense factor/solve, multicolour point Gauss-Seidel, residual,
 // restriction, interpolation-correction and the residual norm.  One thread per
 // point (x fastest, so every warp reads consecutive doubles of a row).
+#include <cstdio>
+#include <cstdlib>
+#include <utility>
+
 #include "bmg3.cuh"
 #include "bmg_internal.cuh"
 
@@ -407,12 +411,203 @@ void launch3_relax_point(const Op3 &A, const double *f, double *u, int nsweeps, 
     }
 }
 
+
+// 27-point levels, colour-major copy: per colour c its sub-lattice
+// points q = (kk*cy + jj)*cx + ii hold the full row, cf[e*Nc + q] = A[p, p+off_e]
+// for e != 13 and cf[13*Nc + q] = rcp_pos(a_O), so a colour pass streams exactly its
+// own coefficients once (the symmetric half would re-read every plane in all 8 passes).
+struct Sub {
+    int i0, j0, k0, cx, cy, cz;
+};
+
+__host__ __device__ inline Sub sub_of(const Grid3 &g, int c)
+{
+    Sub b;
+    b.i0 = (c & 1) ? 1 : 2;
+    b.j0 = (c & 2) ? 1 : 2;
+    b.k0 = (c & 4) ? 1 : 2;
+    b.cx = (c & 1) ? (g.nx + 1) / 2 : g.nx / 2;
+    b.cy = (c & 2) ? (g.ny + 1) / 2 : g.ny / 2;
+    b.cz = (c & 4) ? (g.nz + 1) / 2 : g.nz / 2;
+    return b;
+}
+
+long long relax27_doubles(const Grid3 &g)
+{
+    long long n = 0;
+    for (int c = 0; c < 8; c++) {
+        const Sub b = sub_of(g, c);
+        n += 27LL * b.cx * b.cy * b.cz;
+    }
+    return n;
+}
+
+__global__ void k3_build_relax27(Op3 A, Sub b, double *__restrict__ cf)
+{
+    const int ii = blockIdx.x * blockDim.x + threadIdx.x, jj = blockIdx.y, kk = blockIdx.z;
+    if (ii >= b.cx)
+        return;
+    const long long Nc = (long long)b.cx * b.cy * b.cz, q = ((long long)kk * b.cy + jj) * b.cx + ii;
+    const long long p = at3(A.g, b.i0 + 2 * ii, b.j0 + 2 * jj, b.k0 + 2 * kk);
+    for (int e = 0; e < 27; e++)
+        cf[e * Nc + q] = e == 13 ? rcp_pos(A.O[p]) : row_entry(A, p, e);
+}
+
+void launch3_build_relax27(const Op3 &A, double *cf, cudaStream_t s)
+{
+    for (int c = 0; c < 8; c++) {
+        const Sub b = sub_of(A.g, c);
+        if (b.cx * b.cy * b.cz == 0)
+            continue;
+        k3_build_relax27<<<dim3((b.cx + 127) / 128, b.cy, b.cz), 128, 0, s>>>(A, b, cf);
+        cf += 27LL * b.cx * b.cy * b.cz;
+    }
+}
+
+__global__ void __launch_bounds__(128) k3_relax27c(Grid3 g, Sub b, const double *__restrict__ cf,
+                                                   const double *__restrict__ f, double *__restrict__ u)
+{
+    const int ii = blockIdx.x * 32 + threadIdx.x, jj = blockIdx.y * 4 + threadIdx.y, kk = blockIdx.z;
+    if (ii >= b.cx || jj >= b.cy)
+        return;
+    const long long Nc = (long long)b.cx * b.cy * b.cz, q = ((long long)kk * b.cy + jj) * b.cx + ii;
+    const long long p = at3(g, b.i0 + 2 * ii, b.j0 + 2 * jj, b.k0 + 2 * kk);
+    const long long Y = g.px, Z = g.ps;
+    double s = 0.0;
+#pragma unroll
+    for (int e = 0; e < 27; e++) {
+        if (e == 13)
+            continue;
+        const long long o = (long long)(e / 9 - 1) * Z + (long long)((e / 3) % 3 - 1) * Y + (e % 3 - 1);
+        s += __ldg(cf + e * Nc + q) * u[p + o];
+    }
+    u[p] = (f[p] - s) * __ldg(cf + 13 * Nc + q);
+}
+
+void launch3_relax27c(const Grid3 &g, const double *cf, const double *f, double *u, int nsweeps, cudaStream_t s)
+{
+    for (int sw = 0; sw < nsweeps; sw++) {
+        const double *c = cf;
+        for (int col = 0; col < 8; col++) {
+            const Sub b = sub_of(g, col);
+            if (b.cx * b.cy * b.cz == 0)
+                continue;
+            k3_relax27c<<<dim3((b.cx + 31) / 32, (b.cy + 3) / 4, b.cz), dim3(32, 4), 0, s>>>(g, b, c, f, u);
+            c += 27LL * b.cx * b.cy * b.cz;
+        }
+    }
+}
+
+
+// ---------------------------------------------------------------- C1 on 7-point levels: one pass per sweep
+// A red-black sweep u_out = GS(u_in) in ONE kernel.  A CTA owns a
+// 64 x 8 column tile and a chunk of RB_KC planes and marches in z: at step k it
+// updates the red points of plane k on the tile plus a one-point ring (their
+// neighbours are old black values, read from u_in, which nobody writes), keeps
+// them in a 4-plane shared ring, and after one barrier updates the black points of
+// plane k-1 on the tile from the red values of planes k-2, k-1, k.  Ring red points
+// are recomputed by every CTA that needs them, so no CTA waits for another; u_in
+// is read-only and u_out written once, i.e. one pass over the level per sweep
+// (the two colour launches read every array twice).  Same per-point expression as
+// k3_relax7, so the iterate is that of the two-launch sweep.
+constexpr int RB_TX = 64;
+
+__device__ __forceinline__ double gs7(const Op3 &A, long long p, double f, double uw, double ue, double us, double un,
+                                      double ub, double ut)
+{
+    const long long X = 1, Y = A.g.px, Z = A.g.ps;
+    const double *W = A.a[12], *S = A.a[10], *B = A.a[4];
+    const double s = W[p] * uw + W[p + X] * ue + S[p] * us + S[p + Y] * un + B[p] * ub + B[p + Z] * ut;
+    return (f - s) * rcp_pos(A.O[p]);
+}
+
+template <int RB_TY, int RB_KC>
+__global__ void __launch_bounds__(32 * RB_TY) k3_rb7(Op3 A, const double *__restrict__ f, const double *__restrict__ uin,
+                                              double *__restrict__ uout)
+{
+    constexpr int RB_RX = RB_TX + 2, RB_RY = RB_TY + 2, NT = 32 * RB_TY;
+    __shared__ double red[4][RB_RY][RB_RX];
+    const int nx = A.g.nx, ny = A.g.ny, nz = A.g.nz;
+    const long long Y = A.g.px, Z = A.g.ps;
+    const int i0 = blockIdx.x * RB_TX + 1, j0 = blockIdx.y * RB_TY + 1;
+    const int kb = blockIdx.z * RB_KC + 1, ke = min(kb + RB_KC, nz + 1);
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    for (int k = kb - 1; k <= ke; k++) {
+        // red points of plane k on the tile + ring: 10 rows x 33 per row
+        double(*rk)[RB_RX] = red[k & 3];
+        for (int t = tid; t < RB_RY * (RB_RX / 2); t += NT) {
+            const int row = t / (RB_RX / 2), c = t % (RB_RX / 2);
+            const int j = j0 - 1 + row;
+            const int ib = i0 - 1;
+            const int i = ib + 2 * c + ((ib + j + k) & 1);
+            double v = 0.0;
+            if (k >= 1 && k <= nz && j >= 1 && j <= ny && i >= 1 && i <= nx) {
+                const long long p = (long long)k * Z + (long long)j * Y + i;
+                v = gs7(A, p, f[p], uin[p - 1], uin[p + 1], uin[p - Y], uin[p + Y], uin[p - Z], uin[p + Z]);
+                if (k >= kb && k < ke && j >= j0 && j < j0 + RB_TY && i >= i0 && i < i0 + RB_TX)
+                    uout[p] = v;
+            }
+            rk[row][i - ib] = v;  // black slots are never read
+        }
+        __syncthreads();
+        const int kk = k - 1;
+        if (kk >= kb && kk < ke) {
+            const int j = j0 + threadIdx.y;
+            const int ia = i0 + 2 * threadIdx.x;
+            const int i = ia + ((ia + j + kk + 1) & 1);  // the black point of the pair (ia, ia+1)
+            if (j <= ny && i <= nx) {
+                const long long p = (long long)kk * Z + (long long)j * Y + i;
+                const int r = threadIdx.y + 1, c = i - (i0 - 1);
+                const double(*rm)[RB_RX] = red[kk & 3];
+                uout[p] = gs7(A, p, f[p], rm[r][c - 1], rm[r][c + 1], rm[r - 1][c], rm[r + 1][c],
+                              red[(kk - 1) & 3][r][c], red[(kk + 1) & 3][r][c]);
+            }
+        }
+    }
+}
+
+// tile height x z-chunk: BMG3_RB="TY,KC" (a tuning knob read once; default measured)
+static int rb_variant()
+{
+    static int v = -1;
+    if (v < 0) {
+        v = 4;  // 16 x 32: measured best of 4..16 x 32..128 (255^3, B200)
+        if (const char *e = getenv("BMG3_RB")) {
+            int ty = 0, kc = 0;
+            if (sscanf(e, "%d,%d", &ty, &kc) == 2)
+                v = ty == 4 ? (kc == 32 ? 0 : 6) : ty == 8 ? (kc == 32 ? 1 : kc == 64 ? 2 : 3) : (kc == 32 ? 4 : 5);
+        }
+    }
+    return v;
+}
+
+template <int TY, int KC>
+static void rb7_launch(const Op3 &A, const double *f, const double *uin, double *uout, cudaStream_t s)
+{
+    dim3 grid((A.g.nx + RB_TX - 1) / RB_TX, (A.g.ny + TY - 1) / TY, (A.g.nz + KC - 1) / KC);
+    k3_rb7<TY, KC><<<grid, dim3(32, TY), 0, s>>>(A, f, uin, uout);
+}
+
+void launch3_rb7(const Op3 &A, const double *f, const double *uin, double *uout, cudaStream_t s)
+{
+    switch (rb_variant()) {
+    case 0: rb7_launch<4, 32>(A, f, uin, uout, s); break;
+    case 6: rb7_launch<4, 64>(A, f, uin, uout, s); break;
+    case 2: rb7_launch<8, 64>(A, f, uin, uout, s); break;
+    case 3: rb7_launch<8, 128>(A, f, uin, uout, s); break;
+    case 4: rb7_launch<16, 32>(A, f, uin, uout, s); break;
+    case 5: rb7_launch<16, 64>(A, f, uin, uout, s); break;
+    case 1: rb7_launch<8, 32>(A, f, uin, uout, s); break;
+    default: rb7_launch<16, 32>(A, f, uin, uout, s); break;
+    }
+}
+
 // ---------------------------------------------------------------- C2 residual
 template <int KIND>
 __global__ void k3_residual(Op3 A, const double *__restrict__ f, const double *__restrict__ u, double *__restrict__ r)
 {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x + 1, j = blockIdx.y + 1, k = blockIdx.z + 1;
-    if (i > A.g.nx)
+    const int i = blockIdx.x * 32 + threadIdx.x + 1, j = blockIdx.y * 4 + threadIdx.y + 1, k = blockIdx.z + 1;
+    if (i > A.g.nx || j > A.g.ny)
         return;
     const long long p = at3(A.g, i, j, k);
     r[p] = f[p] - (A.O[p] * u[p] + offdiag<KIND>(A, u, p));
@@ -420,27 +615,58 @@ __global__ void k3_residual(Op3 A, const double *__restrict__ f, const double *_
 
 void launch3_residual(const Op3 &A, const double *f, const double *u, double *r, cudaStream_t s)
 {
-    dim3 grid((A.g.nx + 127) / 128, A.g.ny, A.g.nz);
+    dim3 grid((A.g.nx + 31) / 32, (A.g.ny + 3) / 4, A.g.nz);
     if (A.kind == 7)
-        k3_residual<7><<<grid, 128, 0, s>>>(A, f, u, r);
+        k3_residual<7><<<grid, dim3(32, 4), 0, s>>>(A, f, u, r);
     else
-        k3_residual<27><<<grid, 128, 0, s>>>(A, f, u, r);
+        k3_residual<27><<<grid, dim3(32, 4), 0, s>>>(A, f, u, r);
 }
 
 // ---------------------------------------------------------------- C3 restriction (c21) + C4
+// Gather at coarse C over the 27 fine points f = 2C + o: the weight of f toward C
+// sits at coarse index Q = C + [o == +1] in slot slot_base(mask(o != 0)) + corner,
+// corner bit = [o_d == -1] on each odd axis -- all compile-time per o.  Fine points
+// on the ring contribute r = 0 (the ring of r is never written).
+template <int E>
+struct ROff {
+    static constexpr int dx = E % 3 - 1, dy = (E / 3) % 3 - 1, dz = E / 9 - 1;
+    static constexpr int m = (dx != 0) | (dy != 0) << 1 | (dz != 0) << 2;
+    static constexpr int c0 = dx != 0 ? (dx == -1) : 0;
+    static constexpr int nb0 = dx != 0;
+    static constexpr int c1 = dy != 0 ? (dy == -1) << nb0 : 0;
+    static constexpr int nb1 = nb0 + (dy != 0);
+    static constexpr int c2 = dz != 0 ? (dz == -1) << nb1 : 0;
+    static constexpr int slot = m == 0 ? -1 : slot_base(m) + c0 + c1 + c2;
+};
+
+template <int E>
+__device__ __forceinline__ double rterm(const CI3 &ci, const Grid3 &fg, const double *__restrict__ r, int Ci, int Cj,
+                                        int Ck)
+{
+    using O = ROff<E>;
+    const double rv = r[at3(fg, 2 * Ci + O::dx, 2 * Cj + O::dy, 2 * Ck + O::dz)];
+    if (O::m == 0)
+        return rv;
+    const double w = ci.w[O::slot][at3(ci.c, Ci + (O::dx == 1), Cj + (O::dy == 1), Ck + (O::dz == 1))];
+    return w * rv;
+}
+
+template <int... Es>
+__device__ __forceinline__ double rsum(const CI3 &ci, const Grid3 &fg, const double *__restrict__ r, int Ci, int Cj,
+                                       int Ck, std::integer_sequence<int, Es...>)
+{
+    double s = 0.0;
+    ((s += rterm<Es>(ci, fg, r, Ci, Cj, Ck)), ...);
+    return s;
+}
+
 __global__ void k3_restrict(Grid3 fg, CI3 ci, const double *__restrict__ r, double *__restrict__ fc,
                             double *__restrict__ uc)
 {
-    const int Ci = blockIdx.x * blockDim.x + threadIdx.x + 1, Cj = blockIdx.y + 1, Ck = blockIdx.z + 1;
-    if (Ci > ci.c.nx)
+    const int Ci = blockIdx.x * 32 + threadIdx.x + 1, Cj = blockIdx.y * 4 + threadIdx.y + 1, Ck = blockIdx.z + 1;
+    if (Ci > ci.c.nx || Cj > ci.c.ny)
         return;
-    double s = 0.0;
-    for (int e = 0; e < 27; e++) {
-        const int fi = 2 * Ci + e % 3 - 1, fj = 2 * Cj + (e / 3) % 3 - 1, fk = 2 * Ck + e / 9 - 1;
-        if (!inside3(fg, fi, fj, fk))
-            continue;
-        s += pw3(ci, fi, fj, fk, Ci, Cj, Ck) * r[at3(fg, fi, fj, fk)];
-    }
+    const double s = rsum(ci, fg, r, Ci, Cj, Ck, std::make_integer_sequence<int, 27>{});
     const long long pc = at3(ci.c, Ci, Cj, Ck);
     fc[pc] = s;
     if (uc)
@@ -449,48 +675,78 @@ __global__ void k3_restrict(Grid3 fg, CI3 ci, const double *__restrict__ r, doub
 
 void launch3_restrict(const Op3 &A, const CI3 &ci, const double *r, double *fc, double *uc, cudaStream_t s)
 {
-    dim3 grid((ci.c.nx + 127) / 128, ci.c.ny, ci.c.nz);
-    k3_restrict<<<grid, 128, 0, s>>>(A.g, ci, r, fc, uc);
+    dim3 grid((ci.c.nx + 31) / 32, (ci.c.ny + 3) / 4, ci.c.nz);
+    k3_restrict<<<grid, dim3(32, 4), 0, s>>>(A.g, ci, r, fc, uc);
 }
 
 // ---------------------------------------------------------------- C6 interpolation + correction (c21)
-// u(f) += sum_c w_c e(C_c), corners in the oracle's order (x fastest), no contraction
-__global__ void k3_interp_add(Grid3 fg, CI3 ci, const double *__restrict__ ec, double *__restrict__ u)
+// One thread per coarse cell (I,J,K): the eight fine points (2I-1..2I) x (2J-1..2J) x
+// (2K-1..2K) share the weight index Q = (I,J,K) and the eight coarse corners, so every
+// e value and weight is loaded once.  u(f) += sum_c w_c e(C_c), corners in the
+// oracle's order (x fastest), no contraction -> bitwise the oracle's update.
+template <int M>
+__device__ __forceinline__ void iterm(const CI3 &ci, const double (&e)[8], long long q, const double *uin,
+                                      double *u, long long p)
 {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x + 1, j = blockIdx.y + 1, k = blockIdx.z + 1;
-    if (i > fg.nx)
-        return;
-    const int odd[3] = {i & 1, j & 1, k & 1};
-    const int m = odd[0] | odd[1] << 1 | odd[2] << 2;
-    const long long p = at3(fg, i, j, k);
+    constexpr int ox = M & 1, oy = (M >> 1) & 1, oz = (M >> 2) & 1;
     double s;
-    if (m == 0) {
-        s = __dmul_rn(1.0, ec[at3(ci.c, i >> 1, j >> 1, k >> 1)]);
+    if (M == 0) {
+        s = __dmul_rn(1.0, e[7]);
     } else {
-        const int Q[3] = {odd[0] ? (i + 1) >> 1 : i >> 1, odd[1] ? (j + 1) >> 1 : j >> 1,
-                          odd[2] ? (k + 1) >> 1 : k >> 1};
-        const long long q = at3(ci.c, Q[0], Q[1], Q[2]);
-        const int base = slot_base(m), nc = 1 << __popc(m);
+        constexpr int nc = 1 << (ox + oy + oz);
         s = 0.0;
-        for (int c = 0; c < nc; c++) {
-            int C[3] = {Q[0], Q[1], Q[2]}, nb = 0;
 #pragma unroll
-            for (int d = 0; d < 3; d++)
-                if (odd[d]) {
-                    if (!((c >> nb) & 1))
-                        C[d] -= 1;
-                    nb++;
-                }
-            s = __dadd_rn(s, __dmul_rn(ci.w[base + c][q], ec[at3(ci.c, C[0], C[1], C[2])]));
+        for (int c = 0; c < nc; c++) {
+            int b = 0, cx = 1, cy = 1, cz = 1;  // corner coordinate: 1 = upper (I), 0 = lower (I-1)
+            if (ox)
+                cx = (c >> b++) & 1;
+            if (oy)
+                cy = (c >> b++) & 1;
+            if (oz)
+                cz = (c >> b++) & 1;
+            s = __dadd_rn(s, __dmul_rn(ci.w[slot_base(M) + c][q], e[cz * 4 + cy * 2 + cx]));
         }
     }
-    u[p] = __dadd_rn(u[p], s);
+    u[p] = __dadd_rn(uin[p], s);
 }
 
-void launch3_interp_add(const Grid3 &fine, const CI3 &ci, const double *ec, double *u, cudaStream_t s)
+__global__ void k3_interp_add(Grid3 fg, CI3 ci, const double *__restrict__ ec, const double *uin, double *u)
 {
-    dim3 grid((fine.nx + 127) / 128, fine.ny, fine.nz);
-    k3_interp_add<<<grid, 128, 0, s>>>(fine, ci, ec, u);
+    const int I = blockIdx.x * 32 + threadIdx.x + 1, J = blockIdx.y * 4 + threadIdx.y + 1, K = blockIdx.z + 1;
+    if (2 * I - 1 > fg.nx || 2 * J - 1 > fg.ny)
+        return;
+    const long long q = at3(ci.c, I, J, K);
+    const long long X = 1, Y = ci.c.px, Z = ci.c.ps;
+    const double e[8] = {ec[q - Z - Y - X], ec[q - Z - Y], ec[q - Z - X], ec[q - Z],
+                         ec[q - Y - X],     ec[q - Y],     ec[q - X],     ec[q]};
+    const int i1 = 2 * I - 1, j1 = 2 * J - 1, k1 = 2 * K - 1;
+    const bool xe = 2 * I <= fg.nx, ye = 2 * J <= fg.ny, ze = 2 * K <= fg.nz;
+    const long long p = at3(fg, i1, j1, k1), FY = fg.px, FZ = fg.ps;
+    // fine (i1 + a, j1 + b, k1 + c): odd coordinate where the offset is 0
+    iterm<7>(ci, e, q, uin, u, p);
+    if (xe)
+        iterm<6>(ci, e, q, uin, u, p + 1);
+    if (ye)
+        iterm<5>(ci, e, q, uin, u, p + FY);
+    if (xe && ye)
+        iterm<4>(ci, e, q, uin, u, p + FY + 1);
+    if (ze) {
+        iterm<3>(ci, e, q, uin, u, p + FZ);
+        if (xe)
+            iterm<2>(ci, e, q, uin, u, p + FZ + 1);
+        if (ye)
+            iterm<1>(ci, e, q, uin, u, p + FZ + FY);
+        if (xe && ye)
+            iterm<0>(ci, e, q, uin, u, p + FZ + FY + 1);
+    }
+}
+
+void launch3_interp_add(const Grid3 &fine, const CI3 &ci, const double *ec, const double *uin, double *u,
+                        cudaStream_t s)
+{
+    const int hx = (fine.nx + 1) / 2, hy = (fine.ny + 1) / 2, hz = (fine.nz + 1) / 2;
+    dim3 grid((hx + 31) / 32, (hy + 3) / 4, hz);
+    k3_interp_add<<<grid, dim3(32, 4), 0, s>>>(fine, ci, ec, uin, u);
 }
 
 // ---------------------------------------------------------------- C7 residual norm (fixed-tree, deterministic)
