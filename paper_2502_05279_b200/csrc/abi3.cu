@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <utility>
@@ -57,6 +58,7 @@ struct Level3 {
     double *ci[26] = {};  // weights from level l+1 (its grid)
     std::vector<PLevel> pv;  // plane hierarchy (relax = planes, non-coarsest levels)
     double *pr = nullptr;    // plane level-0 residual scratch (3-D sized)
+    int ptail = 1 << 30;     // first plane level run by the plane tail (kernels_plane.cu)
     double *rc27 = nullptr;  // 27-point point relaxation: colour-major full rows (kernels3.cu)
     double *tmp = nullptr;   // 7-point point relaxation: the second buffer of the one-pass sweep (k3_rb7)
     Op3 op() const
@@ -175,6 +177,11 @@ bmg_status_t plane_setup(bmg3_solver *h, Level3 &v, cudaStream_t s)
         TRY(check_err(h, s, "bmg3_setup (plane interpolation)"));
         launchP_rap(a.op(), a.cip(c.g), c.pl, s);
     }
+    for (int m = 0; m < M; m++)
+        if ((long long)v.pv[m].g.nx * v.pv[m].g.ny <= PTAIL_MAX && getenv("BMG3_NO_PTAIL") == nullptr) {
+            v.ptail = m;
+            break;
+        }
     PLevel &cl = v.pv[M - 1];
     const long long n = (long long)cl.g.nx * cl.g.ny;
     if (n > MAX_DENSE)
@@ -186,11 +193,33 @@ bmg_status_t plane_setup(bmg3_solver *h, Level3 &v, cudaStream_t s)
     return BMG_OK;
 }
 
+// the plane tail from plane level m (u, f: that level's iterate and right-hand side)
+void plane_tail(Level3 &v, int m, double *u, const double *f, Batch b, cudaStream_t s)
+{
+    PTail T;
+    T.nlev = (int)v.pv.size() - m;
+    for (int t = 0; t < T.nlev; t++) {
+        PLevel &a = v.pv[m + t];
+        T.lv[t].op = a.op();
+        if (m + t + 1 < (int)v.pv.size())
+            T.lv[t].ci = a.cip(v.pv[m + t + 1].g);
+        T.lv[t].u = t == 0 ? u : a.u;
+        T.lv[t].f = t == 0 ? const_cast<double *>(f) : a.f;
+        T.lv[t].r = (m + t == 0) ? v.pr : a.r;
+    }
+    T.chol = v.pv.back().chol;
+    launchP_tail(T, b, s);
+}
+
 // one 2-D V(1,1) cycle (c23, c9 on the plane hierarchy) on the planes of batch b
 void plane_vcycle(Level3 &v, int m, double *u, const double *f, Batch b, cudaStream_t s)
 {
     PLevel &a = v.pv[m];
     const OpP A = a.op();
+    if (m >= v.ptail && (int)v.pv.size() - m <= PTAIL_LEVELS) {
+        plane_tail(v, m, u, f, b, s);
+        return;
+    }
     if (m + 1 == (int)v.pv.size()) {
         launchP_coarse_solve(A, a.chol, f, u, b, s);
         return;

@@ -114,4 +114,19 @@ void launchP_restrict(const OpP &A, const CIP &ci, const double *r, double *fc, 
 void launchP_interp_add(const Grid3 &fine, const CIP &ci, const double *ec, double *u, Batch b, cudaStream_t s);
 void launchP_coarse_solve(const OpP &A, const double *L, const double *f, double *u, Batch b, cudaStream_t s);
 
+// the plane tail: the small plane levels of one V(1,1) in one launch (one CTA per plane)
+constexpr int PTAIL_MAX = 1024;  // unknowns per plane of a tail level
+constexpr int PTAIL_LEVELS = 8;
+struct PTailLevel {
+    OpP op;
+    CIP ci;  // to the next tail level (unused on the last)
+    double *u, *f, *r;
+};
+struct PTail {
+    int nlev;
+    PTailLevel lv[PTAIL_LEVELS];
+    const double *chol;
+};
+void launchP_tail(const PTail &T, Batch b, cudaStream_t s);
+
 }  // namespace bmg3

@@ -472,3 +472,155 @@ void launchP_coarse_solve(const OpP &A, const double *L, const double *f, double
 }
 
 }  // namespace bmg3
+
+namespace bmg3 {
+
+// ---------------------------------------------------------------- the plane tail
+// The small 2-D levels m0..M-1 of a plane V(1,1) cycle (each plane at most
+// PTAIL_MAX unknowns) in ONE launch, one CTA per plane of the batch: the steps
+// are the batched kernels' per-point expressions, ordered by __syncthreads
+// instead of launch boundaries (within a colour the updates are independent), so
+// the plane iterate is that of the batched path.  The levels are a few KB each and
+// stay in L2; ~12 launches per level become barriers.
+__device__ void pt_relax(const OpP &A, const double *f, double *u, long long base)
+{
+    const int nx = A.g.nx, ny = A.g.ny, ncol = A.kind == 5 ? 2 : 4;
+    for (int c = 0; c < ncol; c++) {
+        const int hx = (nx + 1) / 2;
+        const int rows = A.kind == 5 ? ny : (ny + 1) / 2;
+        for (int t = threadIdx.x; t < hx * rows; t += blockDim.x) {
+            int i, j;
+            if (A.kind == 5) {
+                j = t / hx + 1;
+                i = (((c + j) & 1) ? 1 : 2) + 2 * (t % hx);
+            } else {
+                i = ((c & 1) ? 1 : 2) + 2 * (t % hx);
+                j = ((c & 2) ? 1 : 2) + 2 * (t / hx);
+            }
+            if (i > nx || j > ny)
+                continue;
+            const long long p = base + (long long)j * A.g.px + i;
+            const R9 a = rowP(A, p);
+            u[p] = (f[p] - offP(a, u, p, A.g.px)) * rcp_pos(a.o);
+        }
+        __syncthreads();
+    }
+}
+
+__device__ void pt_residual(const OpP &A, const double *f, const double *u, double *r, long long base)
+{
+    const int nx = A.g.nx, n = nx * A.g.ny;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        const long long p = base + (long long)(t / nx + 1) * A.g.px + t % nx + 1;
+        const R9 a = rowP(A, p);
+        r[p] = f[p] - (a.o * u[p] + offP(a, u, p, A.g.px));
+    }
+    __syncthreads();
+}
+
+__device__ void pt_restrict(const Grid3 &fg, const CIP &ci, const double *r, double *fc, double *uc, int k)
+{
+    const int nx = ci.c.nx, n = nx * ci.c.ny;
+    const long long fk = (long long)k * fg.ps, ck = (long long)k * ci.c.ps;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        const int Ci = t % nx + 1, Cj = t / nx + 1;
+        double s = 0.0;
+        for (int e = 0; e < 9; e++) {
+            const int fi = 2 * Ci + e % 3 - 1, fj = 2 * Cj + e / 3 - 1;
+            if (!inside2(fg, fi, fj))
+                continue;
+            s += pwP(ci, ck, fi, fj, Ci, Cj) * r[fk + (long long)fj * fg.px + fi];
+        }
+        const long long pc = ck + (long long)Cj * ci.c.px + Ci;
+        fc[pc] = s;
+        uc[pc] = 0.0;
+    }
+    __syncthreads();
+}
+
+__device__ void pt_interp_add(const Grid3 &fg, const CIP &ci, const double *ec, double *u, int k)
+{
+    const int nx = fg.nx, n = nx * fg.ny;
+    const long long ck = (long long)k * ci.c.ps, Y = ci.c.px;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        const int i = t % nx + 1, j = t / nx + 1;
+        const int oi = i & 1, oj = j & 1;
+        double s;
+        if (!oi && !oj) {
+            s = ec[ck + (long long)(j >> 1) * Y + (i >> 1)];
+        } else if (oi && !oj) {
+            const long long q = ck + (long long)(j >> 1) * Y + ((i + 1) >> 1);
+            s = ci.w[P_LL][q] * ec[q - 1] + ci.w[P_LR][q] * ec[q];
+        } else if (!oi && oj) {
+            const long long q = ck + (long long)((j + 1) >> 1) * Y + (i >> 1);
+            s = ci.w[P_LB][q] * ec[q - Y] + ci.w[P_LA][q] * ec[q];
+        } else {
+            const long long q = ck + (long long)((j + 1) >> 1) * Y + ((i + 1) >> 1);
+            s = ci.w[P_LSW][q] * ec[q - Y - 1] + ci.w[P_LSE][q] * ec[q - Y] + ci.w[P_LNW][q] * ec[q - 1] +
+                ci.w[P_LNE][q] * ec[q];
+        }
+        u[(long long)k * fg.ps + (long long)j * fg.px + i] += s;
+    }
+    __syncthreads();
+}
+
+__device__ void pt_coarse(const OpP &A, const double *Lall, const double *f, double *u, int k, double *b)
+{
+    const int nx = A.g.nx, n = nx * A.g.ny;
+    const double *L = Lall + (long long)(k - 1) * n * n;
+    const long long base = (long long)k * A.g.ps;
+    for (int t = threadIdx.x; t < n; t += blockDim.x)
+        b[t] = f[base + (long long)(t / nx + 1) * A.g.px + t % nx + 1];
+    __syncthreads();
+    for (int r = 0; r < n; r++) {
+        if (threadIdx.x == 0)
+            b[r] /= L[(long long)r * n + r];
+        __syncthreads();
+        const double br = b[r];
+        for (int t = r + 1 + threadIdx.x; t < n; t += blockDim.x)
+            b[t] -= L[(long long)t * n + r] * br;
+        __syncthreads();
+    }
+    for (int r = n - 1; r >= 0; r--) {
+        if (threadIdx.x == 0)
+            b[r] /= L[(long long)r * n + r];
+        __syncthreads();
+        const double br = b[r];
+        for (int t = threadIdx.x; t < r; t += blockDim.x)
+            b[t] -= L[(long long)r * n + t] * br;
+        __syncthreads();
+    }
+    for (int t = threadIdx.x; t < n; t += blockDim.x)
+        u[base + (long long)(t / nx + 1) * A.g.px + t % nx + 1] = b[t];
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) kP_tail(PTail T, Batch bt)
+{
+    extern __shared__ double sb[];
+    const int k = bt.k0 + 2 * blockIdx.x;
+    const int M = T.nlev;
+    // down: relax, residual, restrict on levels 0..M-2 of the tail
+    for (int m = 0; m + 1 < M; m++) {
+        const PTailLevel &a = T.lv[m];
+        const long long base = (long long)k * a.op.g.ps;
+        pt_relax(a.op, a.f, a.u, base);
+        pt_residual(a.op, a.f, a.u, a.r, base);
+        pt_restrict(a.op.g, a.ci, a.r, T.lv[m + 1].f, T.lv[m + 1].u, k);
+    }
+    pt_coarse(T.lv[M - 1].op, T.chol, T.lv[M - 1].f, T.lv[M - 1].u, k, sb);
+    for (int m = M - 2; m >= 0; m--) {
+        const PTailLevel &a = T.lv[m];
+        pt_interp_add(a.op.g, a.ci, T.lv[m + 1].u, a.u, k);
+        pt_relax(a.op, a.f, a.u, (long long)k * a.op.g.ps);
+    }
+}
+
+void launchP_tail(const PTail &T, Batch b, cudaStream_t s)
+{
+    const OpP &c = T.lv[T.nlev - 1].op;
+    const int n = c.g.nx * c.g.ny;
+    kP_tail<<<b.nb, 256, sizeof(double) * n, s>>>(T, b);
+}
+
+}  // namespace bmg3
