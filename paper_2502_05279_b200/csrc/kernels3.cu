@@ -602,6 +602,7 @@ void launch3_rb7(const Op3 &A, const double *f, const double *uin, double *uout,
     }
 }
 
+
 // ---------------------------------------------------------------- C2 residual
 template <int KIND>
 __global__ void k3_residual(Op3 A, const double *__restrict__ f, const double *__restrict__ u, double *__restrict__ r)
