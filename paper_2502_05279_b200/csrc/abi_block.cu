@@ -68,11 +68,25 @@ static int enqueue_cycle_block(bmg_solver *h, int K, const double *f0, double *u
     const int L = h->L;
     auto F = [&](int l) { return l == 0 ? f0 : (const double *)h->blk_f[l]; };
     auto U = [&](int l) { return l == 0 ? u0 : h->blk_u[l]; };
+    // 5-point levels (forward order, no affine term): the one-pass sweep kb_rb5, the
+    // iterate ping-ponging between U(l) and blk_r[l] (r is never stored on this path)
+    auto onepass = [&](int l) { return h->lv[l].kind == 5 && !h->prm.affine && h->prm.cycle_sym == 0; };
+    std::vector<double *> cur(L);
     for (int l = 0; l + 1 < L; l++) {
         const Op A = h->lv[l].op();
-        launch_relax_block(K, A, F(l), U(l), h->prm.nu1, s, &n);
+        cur[l] = U(l);
+        if (onepass(l)) {
+            for (int sw = 0; sw < h->prm.nu1; sw++) {
+                double *to = cur[l] == U(l) ? h->blk_r[l] : U(l);
+                launch_rb5_block(K, A, F(l), cur[l], to, s);
+                cur[l] = to;
+                n += 1;
+            }
+        } else {
+            launch_relax_block(K, A, F(l), U(l), h->prm.nu1, s, &n);
+        }
         if (h->prm.nu1 > 0 && !h->prm.affine) {  // the vanishing restriction, residual fused in (r not stored)
-            launch_resid_restrict_block(K, A, h->civ(l), F(l), U(l), h->blk_f[l + 1], h->blk_u[l + 1], s);
+            launch_resid_restrict_block(K, A, h->civ(l), F(l), cur[l], h->blk_f[l + 1], h->blk_u[l + 1], s);
             n += 1;
         } else {  // c14 needs r on the up leg; nu1 = 0 restricts every residual
             launch_residual_block(K, A, F(l), U(l), h->blk_r[l], s);
@@ -87,6 +101,24 @@ static int enqueue_cycle_block(bmg_solver *h, int K, const double *f0, double *u
         // the post-smoother's first colour overwrites its points from their neighbours
         // alone: those need no correction (exact; DESIGN §5.2 / §5.7)
         const int skip = (h->prm.nu2 > 0 && !h->prm.affine) ? (h->prm.cycle_sym == 1 ? 2 : 1) : 0;
+        if (onepass(l)) {
+            // the corrected iterate goes where the nu2 sweeps then end in U(l); the points
+            // the first colour overwrites are skipped (kb_rb5 never reads them from uin)
+            double *start = (h->prm.nu2 % 2 == 0) ? U(l) : h->blk_r[l];
+            if (h->prm.nu2 == 0 && cur[l] != U(l))
+                start = U(l);
+            launch_interp_add_block(K, A, h->civ(l), U(l + 1), cur[l], s, nullptr, h->prm.nu2 > 0 ? skip : 0,
+                                    start);
+            n += 1;
+            double *it = start;
+            for (int sw = 0; sw < h->prm.nu2; sw++) {
+                double *to = it == U(l) ? h->blk_r[l] : U(l);
+                launch_rb5_block(K, A, F(l), it, to, s);
+                it = to;
+                n += 1;
+            }
+            continue;
+        }
         launch_interp_add_block(K, A, h->civ(l), U(l + 1), U(l), s, h->prm.affine ? h->blk_r[l] : nullptr, skip);
         n += 1;
         launch_relax_block(K, A, F(l), U(l), h->prm.nu2, s, &n, h->prm.cycle_sym == 1);

@@ -213,7 +213,9 @@ void launch_resid_restrict_block(int K, const Op &A, const CIv &ci, const double
 // skip = 1 / 2: leave the points the post-smoother's first colour (forward / reversed
 // order) overwrites uncorrected
 void launch_interp_add_block(int K, const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s,
-                             const double *r = nullptr, int skip = 0);
+                             const double *r, int skip, double *uout = nullptr);
+// 5-point levels: one red-black sweep uout = GS(uin) of K columns in one pass (kb_rb5; uin != uout)
+void launch_rb5_block(int K, const Op &A, const double *f, const double *uin, double *uout, cudaStream_t s);
 void launch_coarse_solve_block(int K, const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s);
 void launch_resid_norm_block(int K, const Op &A, const double *f, const double *u, double *partials, double *result,
                              cudaStream_t s);

@@ -205,6 +205,103 @@ __global__ void kb_relax9(Op A, const double *__restrict__ f, double *__restrict
     stk<W>(u + sub * W + p * K, sm);
 }
 
+// ------------------------------------------------------------------ one-pass red-black sweep (5-point levels)
+// uout = GS(uin), both colours in ONE pass over the level (kb_relax5 makes two, each
+// reading every K-column block).  A CTA owns a strip of TX points and RC rows and
+// marches up the rows: the red points of row j on the strip plus a one-point ring
+// (their neighbours are old black values in uin, which nobody writes) go to a 4-row
+// shared ring; one barrier later the black points of row j-1 take their neighbours
+// from the ring, and row j-1 is written out whole.  Ring points are recomputed by
+// each CTA that needs them (no inter-CTA waits).  Per point and column the
+// expression is kb_relax5's, pinned (__dmul_rn/__fma_rn): bitwise its result.
+template <int K>
+struct RB5 {
+    static constexpr int W = Split<K>::W, TP = Split<K>::TP, NT = 256, NPT = NT / TP;
+    static constexpr int TX = 2 * NPT, RX = TX + 2, RC = 32;
+};
+
+template <int W>
+__device__ __forceinline__ void gs5w(const double *__restrict__ A_O, const double *__restrict__ A_W,
+                                     const double *__restrict__ A_S, long long p, long long P, const double (&us)[W],
+                                     const double (&uw)[W], const double (&ue)[W], const double (&un)[W],
+                                     const double (&fp)[W], double (&out)[W])
+{
+    const double o = A_O[p], w = A_W[p], e = A_W[p + 1], s = A_S[p], n = A_S[p + P];
+    const double rc = rcp_pos(o);
+#pragma unroll
+    for (int c = 0; c < W; c++) {
+        double acc = __dmul_rn(s, us[c]);
+        acc = __fma_rn(w, uw[c], acc);
+        acc = __fma_rn(e, ue[c], acc);
+        acc = __fma_rn(n, un[c], acc);
+        out[c] = (fp[c] - acc) * rc;
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) kb_rb5(Op A, const double *__restrict__ f, const double *__restrict__ uin,
+                                              double *__restrict__ uout)
+{
+    using R = RB5<K>;
+    constexpr int W = R::W, TP = R::TP, NT = R::NT, NPT = R::NPT, RX = R::RX;
+    __shared__ __align__(16) double red[4][RX * K];
+    const long long P = A.pitch;
+    const int i0 = blockIdx.x * R::TX + 1, jb = blockIdx.y * R::RC + 1, je = min(jb + R::RC, A.ny + 1);
+    const int tid = threadIdx.x;
+    for (int j = jb - 1; j <= je; j++) {
+        double *rj = red[j & 3];
+        const int base = i0 - 1;
+        for (int t = tid; t < (NPT + 1) * TP; t += NT) {
+            const int pt = t / TP, sb = t % TP;
+            const int i = base + 2 * pt + ((base + j) & 1);
+            double v[W];
+#pragma unroll
+            for (int c = 0; c < W; c++)
+                v[c] = 0.0;
+            if (j >= 1 && j <= A.ny && i >= 1 && i <= A.nx) {
+                const long long p = j * P + i;
+                const double *ub = uin + sb * W;
+                double us[W], uw[W], ue[W], un[W], fp[W];
+                ldk<W>(ub + (p - P) * K, us);
+                ldk<W>(ub + (p - 1) * K, uw);
+                ldk<W>(ub + (p + 1) * K, ue);
+                ldk<W>(ub + (p + P) * K, un);
+                ldk<W>(f + sb * W + p * K, fp);
+                gs5w<W>(A.O, A.W, A.S, p, P, us, uw, ue, un, fp, v);
+            }
+            if (i - base < RX)
+                stk<W>(rj + (i - base) * K + sb * W, v);
+        }
+        __syncthreads();
+        const int jj = j - 1;
+        if (jj >= jb && jj < je && tid < NPT * TP) {
+            const int pt = tid / TP, sb = tid % TP;
+            const int ia = i0 + 2 * pt;
+            const int odd_a = (ia + jj) & 1;  // 1: ia is black
+            const int ib = odd_a ? ia : ia + 1, ir = odd_a ? ia + 1 : ia;
+            const double *rl = red[(jj - 1) & 3], *rm = red[jj & 3], *rh = red[j & 3];
+            double vb[W];
+            if (ib <= A.nx) {
+                const long long p = jj * P + ib;
+                const int cb = ib - base;
+                double us[W], uw[W], ue[W], un[W], fp[W];
+                ldk<W>(rl + cb * K + sb * W, us);
+                ldk<W>(rm + (cb - 1) * K + sb * W, uw);
+                ldk<W>(rm + (cb + 1) * K + sb * W, ue);
+                ldk<W>(rh + cb * K + sb * W, un);
+                ldk<W>(f + sb * W + p * K, fp);
+                gs5w<W>(A.O, A.W, A.S, p, P, us, uw, ue, un, fp, vb);
+                stk<W>(uout + sb * W + p * K, vb);
+            }
+            if (ir <= A.nx) {
+                double vr[W];
+                ldk<W>(rm + (ir - base) * K + sb * W, vr);
+                stk<W>(uout + sb * W + (jj * P + ir) * K, vr);
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ residual
 template <int K>
 __global__ void kb_residual(Op A, const double *__restrict__ f, const double *__restrict__ u, double *__restrict__ r)
@@ -452,7 +549,7 @@ __global__ void kb_coarse_ring0(int ncx, int ncy, long long C, double *__restric
 // ------------------------------------------------------------------ interpolation + correction (c7, c14)
 template <int K>
 __global__ void kb_interp_add(Op A, CIv ci, const double *__restrict__ e, const double *__restrict__ r,
-                              double *__restrict__ u, int skip)
+                              const double *u, double *uout, int skip)
 {
     constexpr int W = Split<K>::W, TP = Split<K>::TP;
     const int j = blockIdx.y * blockDim.y + threadIdx.y + 1;
@@ -521,7 +618,7 @@ __global__ void kb_interp_add(Op A, CIv ci, const double *__restrict__ e, const 
 #pragma unroll
     for (int c = 0; c < W; c++)
         up[c] += s[c];
-    stk<W>(u + sub * W + p * K, up);
+    stk<W>(uout + sub * W + p * K, up);
 }
 
 // ------------------------------------------------------------------ coarsest solve (c8)
@@ -771,12 +868,18 @@ struct Launch {
             kb_resid_restrict_tiled<K, 9><<<g, 256, 0, s>>>(A, ci, f, u, fc, uc);
         kb_coarse_ring0<K><<<(ncx + ncy + 4 + 255) / 256, 256, 0, s>>>(ncx, ncy, ci.pitch, fc, uc);
     }
-    static void interp_add(const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s, const double *r,
-                           int skip)
+    static void interp_add(const Op &A, const CIv &ci, const double *ec, const double *u, double *uout, cudaStream_t s,
+                           const double *r, int skip)
     {
         const int gxn = ((A.nx + 1) / 2 * TP + 31) / 32;  // CTAs per row for one parity of i
         const dim3 b(32, 8), g(skip && A.kind == 5 ? gxn : 2 * gxn, (A.ny + 7) / 8);
-        kb_interp_add<K><<<g, b, 0, s>>>(A, ci, ec, r, u, skip);
+        kb_interp_add<K><<<g, b, 0, s>>>(A, ci, ec, r, u, uout, skip);
+    }
+    static void rb5(const Op &A, const double *f, const double *uin, double *uout, cudaStream_t s)
+    {
+        using R = RB5<K>;
+        const dim3 g((A.nx + R::TX - 1) / R::TX, (A.ny + R::RC - 1) / R::RC);
+        kb_rb5<K><<<g, R::NT, 0, s>>>(A, f, uin, uout);
     }
     static void coarse(const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s)
     {
@@ -855,9 +958,14 @@ void launch_resid_restrict_block(int K, const Op &A, const CIv &ci, const double
 }
 
 void launch_interp_add_block(int K, const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s,
-                             const double *r, int skip)
+                             const double *r, int skip, double *uout)
 {
-    BMG_BLOCK_DISPATCH(K, interp_add(A, ci, ec, u, s, r, skip));
+    BMG_BLOCK_DISPATCH(K, interp_add(A, ci, ec, u, uout ? uout : u, s, r, skip));
+}
+
+void launch_rb5_block(int K, const Op &A, const double *f, const double *uin, double *uout, cudaStream_t s)
+{
+    BMG_BLOCK_DISPATCH(K, rb5(A, f, uin, uout, s));
 }
 
 void launch_coarse_solve_block(int K, const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s)
