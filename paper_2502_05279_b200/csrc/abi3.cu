@@ -61,6 +61,7 @@ struct Level3 {
     int ptail = 1 << 30;     // first plane level run by the plane tail (kernels_plane.cu)
     double *rc27 = nullptr;  // 27-point point relaxation: colour-major full rows (kernels3.cu)
     double *tmp = nullptr;   // 7-point point relaxation: the second buffer of the one-pass sweep (k3_rb7)
+    double *ro = nullptr;    // and its reciprocal plane rcp_pos(a_O)
     Op3 op() const
     {
         Op3 A;
@@ -256,7 +257,7 @@ double *rb7_sweeps(Level3 &v, const double *f, double *from, double *u, int nswe
 {
     double *a = from, *b = from == u ? v.tmp : u;
     for (int sw = 0; sw < nsweeps; sw++) {
-        launch3_rb7(v.op(), f, a, b, s);
+        launch3_rb7(v.op(), f, a, b, s, v.ro);
         std::swap(a, b);
     }
     return a;
@@ -499,8 +500,11 @@ bmg_status_t bmg3_setup(const bmg3_stencil_t *st, const bmg3_params_t *params, v
     // the one-pass 7-point sweep's second buffer (relaxed 7-point levels)
     if (prm.relax == BMG3_RELAX_POINT)
         for (int l = 0; l + 1 < h->L; l++)
-            if (h->lv[l].kind == 7)
+            if (h->lv[l].kind == 7) {
                 TRYH(alloc(h, gsize(h->lv[l].g), &h->lv[l].tmp, s));
+                TRYH(alloc(h, gsize(h->lv[l].g), &h->lv[l].ro, s));
+                launch3_recip(h->lv[l].op(), h->lv[l].ro, s);
+            }
     // colour-major rows for the 27-point point smoother (relaxed levels only)
     if (prm.relax == BMG3_RELAX_POINT)
         for (int l = 0; l + 1 < h->L; l++) {

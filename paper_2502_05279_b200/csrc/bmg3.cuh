@@ -95,7 +95,10 @@ void launch3_restrict(const Op3 &A, const CI3 &ci, const double *r, double *fc, 
 void launch3_interp_add(const Grid3 &fine, const CI3 &ci, const double *ec, const double *uin, double *u,
                         cudaStream_t s);
 // 7-point levels: one red-black sweep uout = GS(uin) in one pass (uin != uout)
-void launch3_rb7(const Op3 &A, const double *f, const double *uin, double *uout, cudaStream_t s);
+void launch3_rb7(const Op3 &A, const double *f, const double *uin, double *uout, cudaStream_t s,
+                 const double *ro = nullptr);
+// ro = rcp_pos(a_O) on the interior (the one-pass sweep's reciprocal plane)
+void launch3_recip(const Op3 &A, double *ro, cudaStream_t s);
 // ||f - A u||_2 (or ||g||_2 when A == nullptr: pass f = g, u = nullptr) into *result (device)
 void launch3_resid_norm(const Op3 *A, const Grid3 &g, const double *f, const double *u, double *partials,
                         double *result, cudaStream_t s);

@@ -3,7 +3,11 @@
 // RAP, coarsest dense factor/solve, multicolour point Gauss-Seidel, residual,
 // restriction, interpolation-correction and the residual norm.  One thread per
 // point (x fastest, so every warp reads consecutive doubles of a row).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdio>
+#include <mutex>
 #include <cstdlib>
 #include <utility>
 
@@ -566,15 +570,222 @@ __global__ void __launch_bounds__(32 * RB_TY) k3_rb7(Op3 A, const double *__rest
     }
 }
 
+
+// ---------------------------------------------------------------- k3_rb7t: the one-pass sweep fed by TMA
+// k3_rb7's schedule with every input plane staged ONCE per CTA in shared memory by
+// the tensor engine: one thread issues, per step, six 2-D tile boxes of (3-D tensor
+// maps; out-of-range rows/columns/planes zero-filled) -- u_in(k+2), f/O/W/S(k+1),
+// B(k+2) -- that land one step ahead on an mbarrier (complete_tx), so the 256 threads
+// only compute (k3_rb7 re-read halo and next-plane data through L1/L2, 1.42x the
+// arrays from DRAM; the cp.async variant was issue-bound, tools/archive/k3_rb7s.cu.txt).
+namespace rbt {
+constexpr int TX = 64, TY = 8, KC = 32, NT = 32 * TY;
+constexpr int UX = TX + 6, UY = TY + 4;  // u_in box: origin (i0-3, j0-2) (TMA needs a 16-B aligned x start)
+constexpr int RX = TX + 2, RY = TY + 2;  // f, O, B, red: origin (i0-1, j0-1)
+constexpr int WX = TX + 4;               // W box: 68 wide (16-B multiple), origin (i0-1, j0-1)
+constexpr int SY = TY + 3;               // S box: RX x 11
+constexpr int al(int n) { return (n + 15) / 16 * 16; }  // 128-byte slots
+constexpr int SU = al(UX * UY), SF = al(RX * RY), SW = al(WX * RY), SS = al(RX * SY), SR = RX * RY;
+constexpr int OFF_U = 0, OFF_F = OFF_U + 4 * SU, OFF_O = OFF_F + 3 * SF, OFF_W = OFF_O + 3 * SF,
+              OFF_S = OFF_W + 3 * SW, OFF_B = OFF_S + 3 * SS, OFF_R = OFF_B + 4 * SF, TOTAL = OFF_R + 4 * SR;
+constexpr unsigned BU = UX * UY * 8, BF = RX * RY * 8, BW = WX * RY * 8, BS = RX * SY * 8;
+}  // namespace rbt
+
+struct Maps7 {
+    CUtensorMap u, f, o, w, s, b;
+};
+
+__device__ __forceinline__ unsigned s32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void tma3(double *dst, const CUtensorMap *m, int x, int y, int z, unsigned long long *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(s32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(m)), "r"(x), "r"(y), "r"(z), "r"(s32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mb_expect(unsigned long long *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mb_wait(unsigned long long *bar, unsigned parity)
+{
+    asm volatile(
+        "{\n .reg .pred P1;\n RB7W:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        " @!P1 bra RB7W;\n}\n" ::"r"(s32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+template <bool RCP>
+__global__ void __launch_bounds__(rbt::NT, 1) k3_rb7t(Op3 A, double *__restrict__ uout,
+                                                      const __grid_constant__ Maps7 M)
+{
+    using namespace rbt;
+    extern __shared__ __align__(1024) double sm[];
+    unsigned long long *bar = reinterpret_cast<unsigned long long *>(sm + TOTAL);  // no static smem: slots stay 128-B aligned
+    const Grid3 &G = A.g;
+    const int nx = G.nx, ny = G.ny, nz = G.nz;
+    const int i0 = blockIdx.x * TX + 1, j0 = blockIdx.y * TY + 1;
+    const int kb = blockIdx.z * KC + 1, ke = min(kb + KC, nz + 1);
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    auto U_ = [&](int k) { return sm + OFF_U + (k & 3) * SU; };
+    auto F_ = [&](int k) { return sm + OFF_F + ((k + 3) % 3) * SF; };
+    auto O_ = [&](int k) { return sm + OFF_O + ((k + 3) % 3) * SF; };
+    auto W_ = [&](int k) { return sm + OFF_W + ((k + 3) % 3) * SW; };
+    auto S_ = [&](int k) { return sm + OFF_S + ((k + 3) % 3) * SS; };
+    auto B_ = [&](int k) { return sm + OFF_B + (k & 3) * SF; };
+    auto R_ = [&](int k) { return sm + OFF_R + (k & 3) * SR; };
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&bar[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&bar[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int xu = i0 - 3, yu = j0 - 2, xr = i0 - 1, yr = j0 - 1;  // even x starts (i0 = 64 bx + 1)
+    if (tid == 0) {  // prologue: what step kb-1 reads (planes < 0 are zero-filled boxes)
+        mb_expect(&bar[0], 3 * BU + 3 * BF + BW + BS + BF);
+        for (int k = kb - 2; k <= kb; k++)
+            tma3(U_(k), &M.u, xu, yu, k, &bar[0]);
+        tma3(F_(kb - 1), &M.f, xr, yr, kb - 1, &bar[0]);
+        tma3(O_(kb - 1), &M.o, xr, yr, kb - 1, &bar[0]);
+        tma3(W_(kb - 1), &M.w, xr, yr, kb - 1, &bar[0]);
+        tma3(S_(kb - 1), &M.s, xr, yr, kb - 1, &bar[0]);
+        tma3(B_(kb - 1), &M.b, xr, yr, kb - 1, &bar[0]);
+        tma3(B_(kb), &M.b, xr, yr, kb, &bar[0]);
+    }
+    mb_wait(&bar[0], 0);
+    for (int k = kb - 1, st = 0; k <= ke; k++, st++) {
+        if (tid == 0 && k < ke) {  // step st+1's new planes, one step ahead
+            unsigned long long *b = &bar[(st + 1) & 1];
+            mb_expect(b, BU + 3 * BF + BW + BS);
+            tma3(U_(k + 2), &M.u, xu, yu, k + 2, b);
+            tma3(F_(k + 1), &M.f, xr, yr, k + 1, b);
+            tma3(O_(k + 1), &M.o, xr, yr, k + 1, b);
+            tma3(W_(k + 1), &M.w, xr, yr, k + 1, b);
+            tma3(S_(k + 1), &M.s, xr, yr, k + 1, b);
+            tma3(B_(k + 2), &M.b, xr, yr, k + 2, b);
+        }
+        double *rk = R_(k);
+        {
+            const double *u0 = U_(k), *um = U_(k - 1), *up = U_(k + 1), *fk = F_(k), *ok = O_(k), *wk = W_(k),
+                         *sk = S_(k), *bk = B_(k), *bp = B_(k + 1);
+            const bool kin = k >= 1 && k <= nz;
+            for (int t = tid; t < RY * (RX / 2); t += NT) {
+                const int r = t / (RX / 2), cc = t % (RX / 2);
+                const int j = j0 - 1 + r;
+                const int c = 2 * cc + ((i0 - 1 + j + k) & 1), i = i0 - 1 + c;
+                double v = 0.0;
+                if (kin && j >= 1 && j <= ny && i >= 1 && i <= nx) {
+                    const int q = r * RX + c, qc = (r + 1) * UX + (c + 2);  // (r+1, c+2) in u_in's box
+                    const double s = wk[r * WX + c] * u0[qc - 1] + wk[r * WX + c + 1] * u0[qc + 1] +
+                                     sk[r * RX + c] * u0[qc - UX] + sk[(r + 1) * RX + c] * u0[qc + UX] +
+                                     bk[q] * um[qc] + bp[q] * up[qc];
+                    v = (fk[q] - s) * (RCP ? ok[q] : rcp_pos(ok[q]));
+                }
+                rk[r * RX + c] = v;
+            }
+        }
+        __syncthreads();
+        const int kk = k - 1;
+        if (kk >= kb && kk < ke) {
+            const int j = j0 + threadIdx.y, r = threadIdx.y + 1;
+            const int ia = i0 + 2 * threadIdx.x;
+            const int par = (ia + j + kk + 1) & 1;  // 0: ia is black
+            const int ib = ia + par, c = ib - (i0 - 1);
+            const double *rm = R_(kk), *rl = R_(kk - 1), *rh = R_(kk + 1), *fk = F_(kk), *ok = O_(kk), *wk = W_(kk),
+                         *sk = S_(kk), *bk = B_(kk), *bp = B_(kk + 1);
+            const int q = r * RX + c;
+            double vb = 0.0;
+            if (j <= ny && ib <= nx) {
+                const double s = wk[r * WX + c] * rm[q - 1] + wk[r * WX + c + 1] * rm[q + 1] +
+                                 sk[r * RX + c] * rm[q - RX] + sk[(r + 1) * RX + c] * rm[q + RX] + bk[q] * rl[q] +
+                                 bp[q] * rh[q];
+                vb = (fk[q] - s) * (RCP ? ok[q] : rcp_pos(ok[q]));
+            }
+            if (j <= ny) {
+                const long long p = (long long)kk * G.ps + (long long)j * G.px + ia;
+                const int cr = ia - (i0 - 1);
+                const double va = par ? rm[r * RX + cr] : vb, vn = par ? vb : rm[r * RX + cr + 1];
+                if (ia <= nx)
+                    uout[p] = va;
+                if (ia + 1 <= nx)
+                    uout[p + 1] = vn;
+            }
+        }
+        if (k < ke)
+            mb_wait(&bar[(st + 1) & 1], ((st + 1) >> 1) & 1);
+        __syncthreads();
+    }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode3()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+        cudaGetLastError();
+    });
+    return fn;
+}
+
+static bool map3(CUtensorMap *m, const double *base, const Grid3 &g, int bx, int by)
+{
+    auto fn = encode3();
+    if (!fn)
+        return false;
+    cuuint64_t dims[3] = {(cuuint64_t)g.px, (cuuint64_t)(g.ny + 2), (cuuint64_t)(g.nz + 2)};
+    cuuint64_t strides[2] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.ps * 8};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)base, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// false: a tensor map could not be encoded (the caller falls back to k3_rb7)
+bool launch3_rb7t(const Op3 &A, const double *f, const double *uin, double *uout, const double *ro, cudaStream_t s)
+{
+    using namespace rbt;
+    Maps7 M;
+    if (((uintptr_t)uin | (uintptr_t)f | (uintptr_t)(ro ? ro : A.O) | (uintptr_t)A.a[12] | (uintptr_t)A.a[10] |
+         (uintptr_t)A.a[4]) & 15 || (A.g.px * 8) % 16 || (A.g.ps * 8) % 16)
+        return false;
+    if (!map3(&M.u, uin, A.g, UX, UY) || !map3(&M.f, f, A.g, RX, RY) || !map3(&M.o, ro ? ro : A.O, A.g, RX, RY) ||
+        !map3(&M.w, A.a[12], A.g, WX, RY) || !map3(&M.s, A.a[10], A.g, RX, SY) || !map3(&M.b, A.a[4], A.g, RX, RY))
+        return false;
+    const size_t smem = sizeof(double) * TOTAL + 16;
+    dim3 grid((A.g.nx + TX - 1) / TX, (A.g.ny + TY - 1) / TY, (A.g.nz + KC - 1) / KC);
+    if (ro) {
+        cudaFuncSetAttribute(k3_rb7t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k3_rb7t<true><<<grid, dim3(32, TY), smem, s>>>(A, uout, M);
+    } else {
+        cudaFuncSetAttribute(k3_rb7t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k3_rb7t<false><<<grid, dim3(32, TY), smem, s>>>(A, uout, M);
+    }
+    return true;
+}
+
 // tile height x z-chunk: BMG3_RB="TY,KC" (a tuning knob read once; default measured)
 static int rb_variant()
 {
     static int v = -1;
     if (v < 0) {
-        v = 4;  // 16 x 32: measured best of 4..16 x 32..128 (255^3, B200)
+        v = 7;  // the TMA-fed sweep (k3_rb7t); k3_rb7 16 x 32 if a tensor map cannot be encoded
         if (const char *e = getenv("BMG3_RB")) {
             int ty = 0, kc = 0;
-            if (sscanf(e, "%d,%d", &ty, &kc) == 2)
+            if (e[0] == 't')
+                v = 7;
+            else if (sscanf(e, "%d,%d", &ty, &kc) == 2)
                 v = ty == 4 ? (kc == 32 ? 0 : 6) : ty == 8 ? (kc == 32 ? 1 : kc == 64 ? 2 : 3) : (kc == 32 ? 4 : 5);
         }
     }
@@ -588,8 +799,23 @@ static void rb7_launch(const Op3 &A, const double *f, const double *uin, double 
     k3_rb7<TY, KC><<<grid, dim3(32, TY), 0, s>>>(A, f, uin, uout);
 }
 
-void launch3_rb7(const Op3 &A, const double *f, const double *uin, double *uout, cudaStream_t s)
+// the reciprocal plane ro = rcp_pos(a_O) of a 7-point level (same value the sweeps form)
+__global__ void k3_recip(Grid3 g, const double *__restrict__ O, double *__restrict__ ro)
 {
+    const int i = blockIdx.x * 32 + threadIdx.x + 1, j = blockIdx.y * 4 + threadIdx.y + 1, k = blockIdx.z + 1;
+    if (i <= g.nx && j <= g.ny)
+        ro[at3(g, i, j, k)] = rcp_pos(O[at3(g, i, j, k)]);
+}
+
+void launch3_recip(const Op3 &A, double *ro, cudaStream_t s)
+{
+    k3_recip<<<dim3((A.g.nx + 31) / 32, (A.g.ny + 3) / 4, A.g.nz), dim3(32, 4), 0, s>>>(A.g, A.O, ro);
+}
+
+void launch3_rb7(const Op3 &A, const double *f, const double *uin, double *uout, cudaStream_t s, const double *ro)
+{
+    if (rb_variant() == 7 && launch3_rb7t(A, f, uin, uout, ro, s))
+        return;
     switch (rb_variant()) {
     case 0: rb7_launch<4, 32>(A, f, uin, uout, s); break;
     case 6: rb7_launch<4, 64>(A, f, uin, uout, s); break;
@@ -598,7 +824,7 @@ void launch3_rb7(const Op3 &A, const double *f, const double *uin, double *uout,
     case 4: rb7_launch<16, 32>(A, f, uin, uout, s); break;
     case 5: rb7_launch<16, 64>(A, f, uin, uout, s); break;
     case 1: rb7_launch<8, 32>(A, f, uin, uout, s); break;
-    default: rb7_launch<16, 32>(A, f, uin, uout, s); break;
+    default: rb7_launch<16, 32>(A, f, uin, uout, s); break;  // 4, and 7's fallback
     }
 }
 
