@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(32 * RB_TY) k3_rb7(Op3 A, const double *__rest
 // only compute (k3_rb7 re-read halo and next-plane data through L1/L2, 1.42x the
 // arrays from DRAM; the cp.async variant was issue-bound, tools/archive/k3_rb7s.cu.txt).
 namespace rbt {
-constexpr int TX = 64, TY = 8, KC = 32, NT = 32 * TY;
+constexpr int TX = 64, TY = 6, KC = 32, NT = 32 * TY;
 constexpr int UX = TX + 6, UY = TY + 4;  // u_in box: origin (i0-3, j0-2) (TMA needs a 16-B aligned x start)
 constexpr int RX = TX + 2, RY = TY + 2;  // f, O, B, red: origin (i0-1, j0-1)
 constexpr int WX = TX + 4;               // W box: 68 wide (16-B multiple), origin (i0-1, j0-1)
@@ -622,7 +622,7 @@ __device__ __forceinline__ void mb_wait(unsigned long long *bar, unsigned parity
 }
 
 template <bool RCP>
-__global__ void __launch_bounds__(rbt::NT, 1) k3_rb7t(Op3 A, double *__restrict__ uout,
+__global__ void __launch_bounds__(rbt::NT, 2) k3_rb7t(Op3 A, double *__restrict__ uout,
                                                       const __grid_constant__ Maps7 M)
 {
     using namespace rbt;
