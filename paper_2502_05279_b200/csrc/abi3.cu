@@ -178,8 +178,11 @@ bmg_status_t plane_setup(bmg3_solver *h, Level3 &v, cudaStream_t s)
         TRY(check_err(h, s, "bmg3_setup (plane interpolation)"));
         launchP_rap(a.op(), a.cip(c.g), c.pl, s);
     }
+    long long ptmax = PTAIL_MAX;  // tuning knob BMG3_PTAIL_MAX (default measured)
+    if (const char *e = getenv("BMG3_PTAIL_MAX"))
+        ptmax = atoll(e);
     for (int m = 0; m < M; m++)
-        if ((long long)v.pv[m].g.nx * v.pv[m].g.ny <= PTAIL_MAX && getenv("BMG3_NO_PTAIL") == nullptr) {
+        if ((long long)v.pv[m].g.nx * v.pv[m].g.ny <= ptmax && getenv("BMG3_NO_PTAIL") == nullptr) {
             v.ptail = m;
             break;
         }
@@ -288,7 +291,8 @@ void enqueue_cycle(bmg3_solver *h, const double *rhs, double *x, cudaStream_t s)
     // 7-point levels with the one-pass sweep keep the iterate in u or tmp (cur[l]);
     // the up leg's interpolation writes where its nu2 sweeps then end in u
     std::vector<double *> cur(L);
-    for (int l = 0; l + 1 < L; l++) {
+    const int ld = L - 1;
+    for (int l = 0; l < ld; l++) {
         Level3 &v = h->lv[l];
         if (v.tmp)
             cur[l] = rb7_sweeps(v, F(l), U(l), U(l), h->prm.nu1, s);
@@ -300,7 +304,7 @@ void enqueue_cycle(bmg3_solver *h, const double *rhs, double *x, cudaStream_t s)
         launch3_restrict(v.op(), ci_view(v, h->lv[l + 1]), v.r, h->lv[l + 1].f, h->lv[l + 1].u, s);
     }
     launch3_coarse_solve(h->lv[L - 1].op(), h->chol, F(L - 1), U(L - 1), s);
-    for (int l = L - 2; l >= 0; l--) {
+    for (int l = ld - 1; l >= 0; l--) {
         Level3 &v = h->lv[l];
         if (v.tmp) {
             double *start = (h->prm.nu2 % 2 == 0) ? U(l) : v.tmp;

@@ -937,11 +937,9 @@ __device__ __forceinline__ void iterm(const CI3 &ci, const double (&e)[8], long 
     u[p] = __dadd_rn(uin[p], s);
 }
 
-__global__ void k3_interp_add(Grid3 fg, CI3 ci, const double *__restrict__ ec, const double *uin, double *u)
+__device__ __forceinline__ void interp_cell(const Grid3 &fg, const CI3 &ci, const double *__restrict__ ec,
+                                            const double *uin, double *u, int I, int J, int K)
 {
-    const int I = blockIdx.x * 32 + threadIdx.x + 1, J = blockIdx.y * 4 + threadIdx.y + 1, K = blockIdx.z + 1;
-    if (2 * I - 1 > fg.nx || 2 * J - 1 > fg.ny)
-        return;
     const long long q = at3(ci.c, I, J, K);
     const long long X = 1, Y = ci.c.px, Z = ci.c.ps;
     const double e[8] = {ec[q - Z - Y - X], ec[q - Z - Y], ec[q - Z - X], ec[q - Z],
@@ -968,6 +966,14 @@ __global__ void k3_interp_add(Grid3 fg, CI3 ci, const double *__restrict__ ec, c
     }
 }
 
+__global__ void k3_interp_add(Grid3 fg, CI3 ci, const double *__restrict__ ec, const double *uin, double *u)
+{
+    const int I = blockIdx.x * 32 + threadIdx.x + 1, J = blockIdx.y * 4 + threadIdx.y + 1, K = blockIdx.z + 1;
+    if (2 * I - 1 > fg.nx || 2 * J - 1 > fg.ny)
+        return;
+    interp_cell(fg, ci, ec, uin, u, I, J, K);
+}
+
 void launch3_interp_add(const Grid3 &fine, const CI3 &ci, const double *ec, const double *uin, double *u,
                         cudaStream_t s)
 {
@@ -975,6 +981,7 @@ void launch3_interp_add(const Grid3 &fine, const CI3 &ci, const double *ec, cons
     dim3 grid((hx + 31) / 32, (hy + 3) / 4, hz);
     k3_interp_add<<<grid, dim3(32, 4), 0, s>>>(fine, ci, ec, uin, u);
 }
+
 
 // ---------------------------------------------------------------- C7 residual norm (fixed-tree, deterministic)
 constexpr int NT3 = 256;
