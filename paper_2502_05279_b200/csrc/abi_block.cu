@@ -68,9 +68,10 @@ static int enqueue_cycle_block(bmg_solver *h, int K, const double *f0, double *u
     const int L = h->L;
     auto F = [&](int l) { return l == 0 ? f0 : (const double *)h->blk_f[l]; };
     auto U = [&](int l) { return l == 0 ? u0 : h->blk_u[l]; };
-    // 5-point levels (forward order, no affine term): the one-pass sweep kb_rb5, the
+    // forward colour order, no affine term: kb_rb5 (5-point, one pass) / kb_r9pair (9-point,
+    // two launches) sweeps, the
     // iterate ping-ponging between U(l) and blk_r[l] (r is never stored on this path)
-    auto onepass = [&](int l) { return h->lv[l].kind == 5 && !h->prm.affine && h->prm.cycle_sym == 0; };
+    auto onepass = [&](int l) { return !h->prm.affine && h->prm.cycle_sym == 0; };
     std::vector<double *> cur(L);
     for (int l = 0; l + 1 < L; l++) {
         const Op A = h->lv[l].op();
@@ -80,7 +81,7 @@ static int enqueue_cycle_block(bmg_solver *h, int K, const double *f0, double *u
                 double *to = cur[l] == U(l) ? h->blk_r[l] : U(l);
                 launch_rb5_block(K, A, F(l), cur[l], to, s);
                 cur[l] = to;
-                n += 1;
+                n += A.kind == 5 ? 1 : 2;
             }
         } else {
             launch_relax_block(K, A, F(l), U(l), h->prm.nu1, s, &n);
@@ -115,7 +116,7 @@ static int enqueue_cycle_block(bmg_solver *h, int K, const double *f0, double *u
                 double *to = it == U(l) ? h->blk_r[l] : U(l);
                 launch_rb5_block(K, A, F(l), it, to, s);
                 it = to;
-                n += 1;
+                n += A.kind == 5 ? 1 : 2;
             }
             continue;
         }

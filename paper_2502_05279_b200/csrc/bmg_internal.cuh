@@ -214,7 +214,8 @@ void launch_resid_restrict_block(int K, const Op &A, const CIv &ci, const double
 // order) overwrites uncorrected
 void launch_interp_add_block(int K, const Op &A, const CIv &ci, const double *ec, double *u, cudaStream_t s,
                              const double *r, int skip, double *uout = nullptr);
-// 5-point levels: one red-black sweep uout = GS(uin) of K columns in one pass (kb_rb5; uin != uout)
+// one GS sweep uout = GS(uin) of K columns (5-point: kb_rb5, one pass; 9-point: kb_r9pair, even then
+// odd rows; uin != uout)
 void launch_rb5_block(int K, const Op &A, const double *f, const double *uin, double *uout, cudaStream_t s);
 void launch_coarse_solve_block(int K, const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s);
 void launch_resid_norm_block(int K, const Op &A, const double *f, const double *u, double *partials, double *result,

@@ -302,6 +302,98 @@ __global__ void __launch_bounds__(256) kb_rb5(Op A, const double *__restrict__ f
     }
 }
 
+// one point, W columns: u = (f - sum_{q != p} a_pq u_q) * rcp(a_pp), neighbour values
+// given in fig:stencil_operator order SW,S,SE,W,E,NW,N,NE (offdiag_w's order)
+template <int W>
+__device__ __forceinline__ void gs9w(const Row9 &a, const double (&n)[8][W], const double (&fp)[W], double (&out)[W])
+{
+    const double rc = rcp_pos(a.o);
+#pragma unroll
+    for (int c = 0; c < W; c++) {
+        double s = __dmul_rn(a.sw, n[0][c]);
+        s = __fma_rn(a.s, n[1][c], s);
+        s = __fma_rn(a.se, n[2][c], s);
+        s = __fma_rn(a.w, n[3][c], s);
+        s = __fma_rn(a.e, n[4][c], s);
+        s = __fma_rn(a.nw, n[5][c], s);
+        s = __fma_rn(a.n, n[6][c], s);
+        s = __fma_rn(a.ne, n[7][c], s);
+        out[c] = (fp[c] - s) * rc;
+    }
+}
+
+// ------------------------------------------------------------------ 9-point levels: a sweep in two launches
+// The four colours of a 9-point level pair up by rows: colours 0, 1 live on the even
+// rows and, within a row, 1 depends only on 0 (its x-neighbours) and on the odd rows
+// (old); colours 2, 3 likewise on the odd rows given the even rows (new).  So a sweep
+// uout = GS(uin) is two launches: even rows (neighbour rows from uin), then odd rows
+// (neighbour rows from uout), each CTA a row segment whose first colour is recomputed
+// on a one-point ring from uin (read-only), the second colour taking its x-neighbours
+// from shared memory, both written out.  Per point kb_relax9's expression: bitwise.
+template <int K>
+struct R9P {
+    static constexpr int W = Split<K>::W, TP = Split<K>::TP, NT = 256, NPT = NT / TP, TX = 2 * NPT;
+};
+
+template <int K>
+__global__ void __launch_bounds__(256) kb_r9pair(Op A, const double *__restrict__ f, const double *__restrict__ uin,
+                                                 double *uout, int odd)
+{
+    using R = R9P<K>;
+    constexpr int W = R::W, TP = R::TP, NT = R::NT, NPT = R::NPT;
+    __shared__ __align__(16) double c1[(NPT + 1) * K];  // the first colour, even i in [x0-1, x0+TX]
+    const long long P = A.pitch;
+    const int j = 2 * blockIdx.y + (odd ? 1 : 2);
+    if (j > A.ny)
+        return;
+    const int x0 = blockIdx.x * R::TX + 1;
+    const double *nb = odd ? uout : uin;  // rows j +- 1: old (even-row pass) or new (odd-row pass)
+    const int tid = threadIdx.x;
+    for (int t = tid; t < (NPT + 1) * TP; t += NT) {
+        const int pt = t / TP, sb = t % TP, i = x0 - 1 + 2 * pt;
+        double v[W];
+#pragma unroll
+        for (int c = 0; c < W; c++)
+            v[c] = 0.0;
+        if (i >= 1 && i <= A.nx) {
+            const long long q = j * P + i;
+            double n[8][W], fp[W];
+            ldk<W>(nb + sb * W + (q - P - 1) * K, n[0]);
+            ldk<W>(nb + sb * W + (q - P) * K, n[1]);
+            ldk<W>(nb + sb * W + (q - P + 1) * K, n[2]);
+            ldk<W>(uin + sb * W + (q - 1) * K, n[3]);
+            ldk<W>(uin + sb * W + (q + 1) * K, n[4]);
+            ldk<W>(nb + sb * W + (q + P - 1) * K, n[5]);
+            ldk<W>(nb + sb * W + (q + P) * K, n[6]);
+            ldk<W>(nb + sb * W + (q + P + 1) * K, n[7]);
+            ldk<W>(f + sb * W + q * K, fp);
+            gs9w<W>(load_row9(A, q), n, fp, v);
+            if (i >= x0 && i < x0 + R::TX)
+                stk<W>(uout + sb * W + q * K, v);
+        }
+        stk<W>(c1 + pt * K + sb * W, v);
+    }
+    __syncthreads();
+    if (tid < NPT * TP) {
+        const int pt = tid / TP, sb = tid % TP, i = x0 + 2 * pt;
+        if (i <= A.nx) {
+            const long long q = j * P + i;
+            double n[8][W], fp[W], v[W];
+            ldk<W>(nb + sb * W + (q - P - 1) * K, n[0]);
+            ldk<W>(nb + sb * W + (q - P) * K, n[1]);
+            ldk<W>(nb + sb * W + (q - P + 1) * K, n[2]);
+            ldk<W>(c1 + pt * K + sb * W, n[3]);        // i-1 = x0-1+2pt
+            ldk<W>(c1 + (pt + 1) * K + sb * W, n[4]);  // i+1
+            ldk<W>(nb + sb * W + (q + P - 1) * K, n[5]);
+            ldk<W>(nb + sb * W + (q + P) * K, n[6]);
+            ldk<W>(nb + sb * W + (q + P + 1) * K, n[7]);
+            ldk<W>(f + sb * W + q * K, fp);
+            gs9w<W>(load_row9(A, q), n, fp, v);
+            stk<W>(uout + sb * W + q * K, v);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ residual
 template <int K>
 __global__ void kb_residual(Op A, const double *__restrict__ f, const double *__restrict__ u, double *__restrict__ r)
@@ -875,6 +967,13 @@ struct Launch {
         const dim3 b(32, 8), g(skip && A.kind == 5 ? gxn : 2 * gxn, (A.ny + 7) / 8);
         kb_interp_add<K><<<g, b, 0, s>>>(A, ci, ec, r, u, uout, skip);
     }
+    static void r9pair(const Op &A, const double *f, const double *uin, double *uout, cudaStream_t s)
+    {
+        using R = R9P<K>;
+        const int gx = (A.nx + R::TX - 1) / R::TX;
+        kb_r9pair<K><<<dim3(gx, A.ny / 2 + 1), R::NT, 0, s>>>(A, f, uin, uout, 0);
+        kb_r9pair<K><<<dim3(gx, (A.ny + 1) / 2), R::NT, 0, s>>>(A, f, uin, uout, 1);
+    }
     static void rb5(const Op &A, const double *f, const double *uin, double *uout, cudaStream_t s)
     {
         using R = RB5<K>;
@@ -965,7 +1064,11 @@ void launch_interp_add_block(int K, const Op &A, const CIv &ci, const double *ec
 
 void launch_rb5_block(int K, const Op &A, const double *f, const double *uin, double *uout, cudaStream_t s)
 {
-    BMG_BLOCK_DISPATCH(K, rb5(A, f, uin, uout, s));
+    if (A.kind == 5) {
+        BMG_BLOCK_DISPATCH(K, rb5(A, f, uin, uout, s));
+    } else {
+        BMG_BLOCK_DISPATCH(K, r9pair(A, f, uin, uout, s));
+    }
 }
 
 void launch_coarse_solve_block(int K, const Op &A, const double *Lf, const double *f, double *u, cudaStream_t s)
