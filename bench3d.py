@@ -6,14 +6,15 @@ on a problems3d workload, f = h^2, x0 = 0, replayed as the captured CUDA graph.
 Not a BASELINE.json configuration (BASELINE's five are 2-D): these lines
 measure the 3-D row to the same bar (parity in tests/test_gpu3d.py).
 
-roofline: the dominant kernel of a point-relaxation cycle is the fine-level
-7-point Gauss-Seidel sweep (bmg3_relax, red + black launches); it is timed
-live with CUDA events on the launching stream, `sweeps` sweeps between the
-events, against SURVEY §8(d)'s model B share of a sweep, (s+3)*8 B per
-unknown with s = 4 stored planes (O, W, S, B read once; u, f read, u
-written) = 56 B.  For plane relaxation the same is reported for one zebra
-plane sweep against the same 56 B (plane solves re-read the plane data:
-the fraction then says how far the plane smoother is from one pass).
+roofline: the dominant step of a cycle is the fine-level smoother sweep
+(bmg3_relax), timed live with CUDA events on the launching stream, `sweeps`
+sweeps between the events, against SURVEY §8(d)'s model B bytes of that sweep:
+point GS (k3_rb7t): (s+3)*8 B per unknown with s = 4 stored planes (a_O, W,
+S, B read once; u, f read, u written) = 56 B; zebra plane GS: the plane
+right-hand side (f, u, B read, g written: 4 doubles) plus one 2-D V(1,1) per
+plane -- on the in-plane 5-point level 2(s+3) + (s+3) + 3.25 + 4.25 = 25.5
+doubles (s = 3), on the 9-point plane levels below 23.5 doubles per their
+unknowns (N/4 + N/16 + ... = N/3: 7.8) -- = 37.3 doubles = 298 B per unknown.
 """
 from __future__ import annotations
 
@@ -134,7 +135,8 @@ def run3d(args, name, clocks_cls, peaks, host_info):
     clocks.stop()
     peak, peak_src = peaks()
     N = float(n) ** 3
-    alg = 56.0 * N
+    bpu = 56.0 if relax == "point" else 298.0
+    alg = bpu * N
     L = S.L
     kpc = bmg3.bmg3_cycle_kernel_count(S.h)
     B = model_bytes3(n, s.kind, L)
@@ -191,7 +193,7 @@ def run3d(args, name, clocks_cls, peaks, host_info):
         "roofline": {"bound": "hbm", "kernel": f"fine-level {relax} GS sweep (bmg3_relax)",
                      "achieved": alg / (sweep_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": alg / (sweep_ms / 1e3) / 1e9 / peak, "traffic": None,
-                     "algorithmic_bytes_per_unknown": 56.0, "sweep_ms": sweep_ms,
+                     "algorithmic_bytes_per_unknown": bpu, "sweep_ms": sweep_ms,
                      "share_of_step": 3 * sweep_ms / ms, "peak_source": peak_src},
         "clocks": {"sm_mhz": cs["sm_mhz"], "sm_max_mhz": cs["sm_max_mhz"], "reasons": cs["reasons"],
                    "samples": cs["samples"]},
