@@ -340,6 +340,30 @@ __global__ void k3_coarse_solve(Op3 A, const double *__restrict__ L, const doubl
 {
     extern __shared__ double b[];
     const int nx = A.g.nx, ny = A.g.ny, n = nx * ny * A.g.nz;
+    if (n <= 32) {  // one warp: no barriers (the CTA loop pays two per unknown)
+        if (threadIdx.x < 32) {
+            const int i = threadIdx.x;
+            const long long q = at3(A.g, i % nx + 1, (i / nx) % ny + 1, i / (nx * ny) + 1);
+            double x = i < n ? f[q] : 0.0;
+            for (int r = 0; r < n; r++) {
+                const double br = __shfl_sync(0xffffffffu, x, r) / L[(long long)r * n + r];
+                if (i == r)
+                    x = br;
+                else if (i > r && i < n)
+                    x -= L[(long long)i * n + r] * br;
+            }
+            for (int r = n - 1; r >= 0; r--) {
+                const double br = __shfl_sync(0xffffffffu, x, r) / L[(long long)r * n + r];
+                if (i == r)
+                    x = br;
+                else if (i < r)
+                    x -= L[(long long)r * n + i] * br;
+            }
+            if (i < n)
+                u[q] = x;
+        }
+        return;
+    }
     for (int t = threadIdx.x; t < n; t += blockDim.x)
         b[t] = f[at3(A.g, t % nx + 1, (t / nx) % ny + 1, t / (nx * ny) + 1)];
     __syncthreads();

@@ -48,6 +48,30 @@ __device__ __forceinline__ double offP(const R9 &a, const double *__restrict__ u
            a.nw * u[p + Y - 1] + a.n * u[p + Y] + a.ne * u[p + Y + 1];
 }
 
+
+// The two substitutions by ONE warp for n <= 32 unknowns (lane i holds b_i, x_k
+// broadcast by a shuffle): the CTA loops pay two barriers per unknown.  Same
+// operations in the same order as the CTA loops, so the same result.
+__device__ __forceinline__ double warp_chol_solve(const double *__restrict__ L, int n, double b)
+{
+    const int i = threadIdx.x & 31;
+    for (int k = 0; k < n; k++) {
+        const double bk = __shfl_sync(0xffffffffu, b, k) / L[(long long)k * n + k];
+        if (i == k)
+            b = bk;
+        else if (i > k && i < n)
+            b -= L[(long long)i * n + k] * bk;
+    }
+    for (int k = n - 1; k >= 0; k--) {
+        const double bk = __shfl_sync(0xffffffffu, b, k) / L[(long long)k * n + k];
+        if (i == k)
+            b = bk;
+        else if (i < k)
+            b -= L[(long long)k * n + i] * bk;
+    }
+    return b;
+}
+
 // ---------------------------------------------------------------- plane right-hand side (3-D)
 // g = f - sum over the dz = -1, +1 couplings of A u, on the planes of the batch
 template <int KIND>
@@ -439,6 +463,16 @@ __global__ void kP_coarse_solve(OpP A, const double *__restrict__ Lall, const do
     const int k = bt.k0 + 2 * blockIdx.x, nx = A.g.nx, n = nx * A.g.ny;
     const double *L = Lall + (long long)(k - 1) * n * n;
     const long long base = (long long)k * A.g.ps;
+    if (n <= 32) {
+        if (threadIdx.x < 32) {
+            const int i = threadIdx.x;
+            const long long q = base + (long long)(i / nx + 1) * A.g.px + i % nx + 1;
+            const double x = warp_chol_solve(L, n, i < n ? f[q] : 0.0);
+            if (i < n)
+                u[q] = x;
+        }
+        return;
+    }
     for (int t = threadIdx.x; t < n; t += blockDim.x)
         b[t] = f[base + (long long)(t / nx + 1) * A.g.px + t % nx + 1];
     __syncthreads();
@@ -569,6 +603,17 @@ __device__ void pt_coarse(const OpP &A, const double *Lall, const double *f, dou
     const int nx = A.g.nx, n = nx * A.g.ny;
     const double *L = Lall + (long long)(k - 1) * n * n;
     const long long base = (long long)k * A.g.ps;
+    if (n <= 32) {  // one warp, no barriers inside
+        if (threadIdx.x < 32) {
+            const int i = threadIdx.x;
+            const long long q = base + (long long)(i / nx + 1) * A.g.px + i % nx + 1;
+            const double x = warp_chol_solve(L, n, i < n ? f[q] : 0.0);
+            if (i < n)
+                u[q] = x;
+        }
+        __syncthreads();
+        return;
+    }
     for (int t = threadIdx.x; t < n; t += blockDim.x)
         b[t] = f[base + (long long)(t / nx + 1) * A.g.px + t % nx + 1];
     __syncthreads();
