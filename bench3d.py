@@ -96,9 +96,9 @@ def run3d(args, name, clocks_cls, peaks, host_info):
                                       "d2h_bytes_per_step": 0}}), flush=True)
         return
     s = p3.WORKLOADS3[wl][0](n)
-    t0 = time.perf_counter()
+    bmg3.Solver3(p3.WORKLOADS3[wl][0](15), relax=relax).close()  # loads the kernels (not timed)
     S = bmg3.Solver3(s, relax=relax)
-    setup_ms = (time.perf_counter() - t0) * 1e3
+    setup_ms = S.setup_ms  # bmg3_setup wall clock (planes already on the device)
     f = S.grid(p3.rhs_const(n, n, n))
     x = S.grid()
     stream = torch.cuda.current_stream()
@@ -201,7 +201,9 @@ def run3d(args, name, clocks_cls, peaks, host_info):
                 "d2h_bytes_per_step": nb, "note": "pinned host rhs/x copied in, 1 cycle (bmg3_vcycle), x copied "
                                                    "out; host wall clock"},
         "solve": {"tol": 1e-8, "iterations": it, "converged": rc == 0, "ms": solve_ms,
-                  "mean_factor": float((hist[-1] / hist[0]) ** (1.0 / max(it, 1))), "setup_ms": setup_ms},
+                  "mean_factor": float((hist[-1] / hist[0]) ** (1.0 / max(it, 1))), "setup_ms": setup_ms,
+                  "note": "setup_ms = bmg3_setup wall clock (allocation + S0-S3 + plane hierarchies, "
+                          "synchronised; planes already on the device, kernels loaded by a 15^3 warm-up)"},
         "cpu_baseline": cpu,
     }
     if rank == 0:

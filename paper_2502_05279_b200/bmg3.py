@@ -165,7 +165,14 @@ class Solver3:
         self.device = device
         planes = [to_device3(p, self.pitch, device) for p in stencil.plane_list()]
         prm = bmg3_params_default(nu1=nu1, nu2=nu2, coarsest=coarsest, max_levels=max_levels, relax=relax)
-        self.h = bmg3_setup(planes, self.kind, self.nx, self.ny, self.nz, self.pitch, self.stride, prm)
+        import time
+
+        import torch
+
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        self.h = bmg3_setup(planes, self.kind, self.nx, self.ny, self.nz, self.pitch, self.stride, prm)  # synchronises
+        self.setup_ms = (time.perf_counter() - t0) * 1e3
         self.L = bmg3_num_levels(self.h)
 
     def grid(self, a: np.ndarray | None = None):
