@@ -1,6 +1,7 @@
 // abi_block.cu -- the c15 block multi-RHS entry points of libbmg.so
 // (include/bmg.h: bmg_vcycle_block, bmg_residual_norm_block, bmg_solve_block,
 // bmg_pcg_block): workspace, the block cycle's graph, its solve loop and PCG.
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
