@@ -203,3 +203,23 @@ def test_rejection_matches_oracle():
     with pytest.raises(BmgError) as ei:
         bmg3.Solver3(s)
     assert ei.value.status == 1 and "denominator" in str(ei.value)
+
+
+@pytest.mark.parametrize("nu", [(1, 1), (1, 2), (3, 1), (2, 0), (0, 2)])
+@pytest.mark.parametrize("name,relax", [("lognormal7", "point"), ("checker27", "point"), ("aniso7", "planes")])
+def test_vcycle_nu_parity(name, relax, nu):
+    """Every parity of nu1 / nu2: the one-pass 7-point sweep's ping-pong between x and its
+    second buffer, and the up leg's out-of-place interpolation, end in x."""
+    nx, ny, nz = 31, 27, 33
+    s = _wl(name, nx, ny, nz)
+    f = p3.random_interior(nx, ny, nz, seed=11)
+    x0 = p3.random_interior(nx, ny, nz, seed=12)
+    S = bmg3.Solver3(s, relax=relax, nu1=nu[0], nu2=nu[1])
+    x = S.grid(x0)
+    S.vcycle(S.grid(f), x, 2)
+    S.relax(S.grid(f), x, 3)  # an odd number of sweeps through bmg3_relax
+    torch.cuda.synchronize()
+    H = o3.Hierarchy3(s, relax=relax, nu1=nu[0], nu2=nu[1])
+    ref = H.relax_fine(f, H.vcycle(f, x0, 2), 3)
+    assert_iterate_close(bmg3.from_device3(x, nx), ref)
+    S.close()

@@ -89,7 +89,9 @@ def test_block_vcycle_oracle(orc, wl, nx, ny, K):
 
 
 @pytest.mark.parametrize("opt", [dict(cycle_sym=1, nu1=1, nu2=1), dict(affine=1), dict(nu1=0, nu2=2),
-                                 dict(cycle_sym=1, nu1=2, nu2=2)])
+                                 dict(cycle_sym=1, nu1=2, nu2=2),
+                                 # the one-pass sweeps' ping-pong for every parity of nu1 / nu2
+                                 dict(nu1=1, nu2=2), dict(nu1=3, nu2=1), dict(nu1=2, nu2=0), dict(nu1=1, nu2=1)])
 @pytest.mark.parametrize("wl,nx,ny", [("lognormal", 63, 63), ("random9", 65, 47)])
 def test_block_variants_vs_single(orc, wl, nx, ny, opt):
     """c12 reversed post-smoother, c14 affine correction, nu1 = 0 (no vanishing
