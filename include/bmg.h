@@ -328,6 +328,16 @@ typedef struct {
     int loopback;         /* 1: all nranks slabs simulated in THIS process on the current
                              GPU, ghost rows copied device-to-device (tests); stencil,
                              rhs and x are then GLOBAL arrays */
+    int peer;             /* 1: the ghost rows of the distributed legs move by in-kernel peer
+                             stores (SURVEY §8(e) lever 3): each fused leg's store and
+                             restriction tasks also write the rows within BMG_HALO of the
+                             slab edges into the neighbours' arrays (CUDA-IPC mapped peer
+                             memory over NVLink; other ranks' slabs in loopback), and a
+                             one-thread signal / wait pair per leg orders the neighbours
+                             (system-scope flags in peer memory) -- instead of a grouped
+                             NCCL send/recv between legs.  The level-0 u/f ghost rows at the
+                             start of a cycle, the level-K all-gather and the norm stay NCCL.
+                             NCCL mode needs the ranks on one node (CUDA IPC). */
 } bmg_comm_t;
 
 /* Host-only: slab boundaries ybounds[0..nranks] (y_0 = 1, y_nranks = ny+1) and the

@@ -50,7 +50,7 @@ class bmg_params_t(ctypes.Structure):
 
 class bmg_comm_t(ctypes.Structure):
     _fields_ = [("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_comm", ctypes.c_void_p),
-                ("nccl_lib", ctypes.c_char_p), ("loopback", ctypes.c_int)]
+                ("nccl_lib", ctypes.c_char_p), ("loopback", ctypes.c_int), ("peer", ctypes.c_int)]
 
 
 class BmgError(RuntimeError):

@@ -21,7 +21,7 @@ namespace bmg {
 enum { CI_LNE = 0, CI_LNW = 1, CI_LSE = 2, CI_LSW = 3, CI_LR = 4, CI_LL = 5, CI_LA = 6, CI_LB = 7 };
 
 // error bits raised by setup kernels (device int, OR-ed)
-enum { ERR_DIAG = 1, ERR_DEN = 2, ERR_PIVOT = 4, ERR_LINE = 8 };
+enum { ERR_DIAG = 1, ERR_DEN = 2, ERR_PIVOT = 4, ERR_LINE = 8, ERR_PEER = 16 };
 
 // relaxation modes (bmg_params_t.relax): c6 point GS, c11 zebra line GS
 enum { RELAX_POINT = 0, RELAX_XLINES = 1, RELAX_YLINES = 2, RELAX_ALTLINES = 3 };

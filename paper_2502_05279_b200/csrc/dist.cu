@@ -121,6 +121,18 @@ struct DistSolver {
     int my_rank = 0;  // NCCL mode
     double *h_norm = nullptr;
     std::vector<void *> allocs;
+    // peer mode (bmg_comm_t.peer): per rank index, per distributed level, the neighbours'
+    // T / u / f ([0] lower, [1] upper neighbour; global-row indexed), the flag arrays
+    // (mine: [0] signals of the lower neighbour, [1] of the upper one, [2] the next
+    // expected count) and the IPC mappings to close
+    bool peer = false;
+    struct PeerPtrs {
+        double *T[2] = {nullptr, nullptr}, *u[2] = {nullptr, nullptr}, *f[2] = {nullptr, nullptr};
+    };
+    std::vector<std::vector<PeerPtrs>> pp;
+    unsigned long long *flags = nullptr, *nflags[2] = {nullptr, nullptr};
+    int *d_perr = nullptr;
+    std::vector<void *> ipc;
 };
 
 // ------------------------------------------------------------------ partition
@@ -429,6 +441,184 @@ bmg_status_t dist_partition(int nx, int ny, int nranks, const bmg_params_t *prm,
     return BMG_OK;
 }
 
+// ------------------------------------------------------------------ peer mode (in-kernel ghost rows)
+// One thread signals: after a leg, increment my count in each neighbour's flag array
+// (system scope: the pushes of the leg, ordered before by the leg kernel's own system
+// fences, are visible to the neighbour before it sees the count).
+__global__ void k_peer_signal(unsigned long long *lo, unsigned long long *hi)
+{
+    __threadfence_system();
+    if (lo)
+        atomicAdd_system(&lo[1], 1ULL);  // I am my lower neighbour's upper neighbour
+    if (hi)
+        atomicAdd_system(&hi[0], 1ULL);
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Before a leg: wait until each neighbour has signalled as many legs as I have waited
+// for before (SPMD: every rank runs the same leg sequence), then count this wait.
+// Bounded: a neighbour that never signals sets ERR_PEER instead of hanging the GPU.
+__global__ void k_peer_wait(unsigned long long *mine, int has_lo, int has_hi, int *err)
+{
+    const unsigned long long e = mine[2];
+    long long spins = 0;
+    while ((has_lo && ld_acquire_sys(&mine[0]) < e) || (has_hi && ld_acquire_sys(&mine[1]) < e)) {
+        __nanosleep(200);
+        if (++spins > 50000000LL) {  // ~10 s
+            atomicOr(err, ERR_PEER);
+            break;
+        }
+    }
+    __threadfence_system();
+    mine[2] = e + 1;
+}
+
+static void peer_wait(DistSolver *d, cudaStream_t s)
+{
+    if (d->loopback)
+        return;  // the ranks' legs run in stream order
+    const int p = d->my_rank;
+    k_peer_wait<<<1, 1, 0, s>>>(d->flags, p > 0, p + 1 < d->P, d->d_perr);
+}
+
+static void peer_signal(DistSolver *d, cudaStream_t s)
+{
+    if (d->loopback)
+        return;
+    k_peer_signal<<<1, 1, 0, s>>>(d->nflags[0], d->nflags[1]);
+}
+
+// Map the neighbours' T (every distributed level) and u, f (levels >= 1) arrays and flag
+// arrays: loopback -- the other slabs of this process; NCCL -- CUDA IPC handles of the
+// allocations, swapped with the neighbours by one grouped send/recv.
+static bmg_status_t peer_setup(DistSolver *d, cudaStream_t s, std::string &err)
+{
+    const int K = d->K;
+    if (K > 32) {
+        err = "peer mode: more than 32 distributed levels";
+        return BMG_EINVAL;
+    }
+    d->pp.assign(d->ranks.size(), std::vector<DistSolver::PeerPtrs>(K));
+    if (d->loopback) {
+        const int P = (int)d->ranks.size();
+        for (int p = 0; p < P; p++)
+            for (int l = 0; l < K; l++)
+                for (int side = 0; side < 2; side++) {
+                    const int q = side == 0 ? p - 1 : p + 1;
+                    if (q < 0 || q >= P)
+                        continue;
+                    SLevel &v = d->ranks[q].lv[l];
+                    d->pp[p][l].T[side] = v.T;
+                    if (l > 0) {
+                        d->pp[p][l].u[side] = v.u;
+                        d->pp[p][l].f[side] = v.f;
+                    }
+                }
+        return BMG_OK;
+    }
+    DCK(cudaMalloc(&d->flags, 4 * sizeof(unsigned long long)));
+    d->allocs.push_back(d->flags);
+    DCK(cudaMemsetAsync(d->flags, 0, 4 * sizeof(unsigned long long), s));
+    DCK(cudaMalloc(&d->d_perr, sizeof(int)));
+    d->allocs.push_back(d->d_perr);
+    DCK(cudaMemsetAsync(d->d_perr, 0, sizeof(int), s));
+    struct Msg {
+        cudaIpcMemHandle_t T[32], u[32], f[32], flags;
+        int roff[32];
+    };
+    Msg mine;
+    memset(&mine, 0, sizeof mine);
+    SRank &R = d->ranks[0];
+    for (int l = 0; l < K; l++) {
+        SLevel &v = R.lv[l];
+        const long long sh = (long long)v.roff * v.pitch;
+        mine.roff[l] = v.roff;
+        DCK(cudaIpcGetMemHandle(&mine.T[l], v.T + sh));
+        if (l > 0) {
+            DCK(cudaIpcGetMemHandle(&mine.u[l], v.u + sh));
+            DCK(cudaIpcGetMemHandle(&mine.f[l], v.f + sh));
+        }
+    }
+    DCK(cudaIpcGetMemHandle(&mine.flags, d->flags));
+    const size_t nd = (sizeof(Msg) + 7) / 8;  // as doubles
+    double *buf = nullptr;
+    DTRY(dmalloc(d, &buf, 3 * nd, err));
+    DCK(cudaMemcpyAsync(buf, &mine, sizeof(Msg), cudaMemcpyHostToDevice, s));
+    const int p = d->my_rank, P = d->P;
+    ncclResult_t r = d->nccl.groupStart();
+    for (int side = 0; side < 2 && r == ncclSuccess; side++) {
+        const int q = side == 0 ? p - 1 : p + 1;
+        if (q < 0 || q >= P)
+            continue;
+        r = d->nccl.recv(buf + (1 + side) * nd, nd, ncclDouble, q, d->comm, s);
+        if (r == ncclSuccess)
+            r = d->nccl.send(buf, nd, ncclDouble, q, d->comm, s);
+    }
+    ncclResult_t r2 = d->nccl.groupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess) {
+        err = std::string("peer handle exchange: ") + d->nccl.errstr(r != ncclSuccess ? r : r2);
+        return BMG_ENCCL;
+    }
+    Msg nb[2];
+    DCK(cudaMemcpyAsync(&nb[0], buf + nd, sizeof(Msg), cudaMemcpyDeviceToHost, s));
+    DCK(cudaMemcpyAsync(&nb[1], buf + 2 * nd, sizeof(Msg), cudaMemcpyDeviceToHost, s));
+    DCK(cudaStreamSynchronize(s));
+    auto open = [&](const cudaIpcMemHandle_t &h, void **out) -> bmg_status_t {
+        DCK(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+        d->ipc.push_back(*out);
+        return BMG_OK;
+    };
+    for (int side = 0; side < 2; side++) {
+        const int q = side == 0 ? p - 1 : p + 1;
+        if (q < 0 || q >= P)
+            continue;
+        void *m = nullptr;
+        DTRY(open(nb[side].flags, &m));
+        d->nflags[side] = (unsigned long long *)m;
+        for (int l = 0; l < K; l++) {
+            const long long sh = (long long)nb[side].roff[l] * R.lv[l].pitch;
+            DTRY(open(nb[side].T[l], &m));
+            d->pp[0][l].T[side] = (double *)m - sh;
+            if (l > 0) {
+                DTRY(open(nb[side].u[l], &m));
+                d->pp[0][l].u[side] = (double *)m - sh;
+                DTRY(open(nb[side].f[l], &m));
+                d->pp[0][l].f[side] = (double *)m - sh;
+            }
+        }
+    }
+    return BMG_OK;
+}
+
+// the push of rank index ri's leg at level l: `fine` its output array's neighbour copies,
+// `coarse` those of f_{l+1} (down legs, l+1 < K) -- nullptr: no push of that kind
+static Push make_push(DistSolver *d, int ri, int l, double *const fine[2], double *const coarse[2])
+{
+    Push q;
+    const SLevel &v = d->ranks[ri].lv[l];
+    q.halo = BMG_HALO;
+    q.ylo = v.ylo;
+    q.yhi = v.yhi;
+    if (fine) {
+        q.lo = fine[0];
+        q.hi = fine[1];
+    }
+    if (coarse && l + 1 < d->K) {
+        const SLevel &c = d->ranks[ri].lv[l + 1];
+        q.clo = coarse[0];
+        q.chi = coarse[1];
+        q.cylo = c.ylo;
+        q.cyhi = c.yhi;
+    }
+    return q;
+}
+
 bmg_status_t dist_setup(const bmg_stencil_t *st, const bmg_comm_t *cm, const bmg_params_t *prm, cudaStream_t s,
                         DistSolver **out, std::string &err)
 {
@@ -444,6 +634,7 @@ bmg_status_t dist_setup(const bmg_stencil_t *st, const bmg_comm_t *cm, const bmg
         bmg_params_default(&d->prm);
     d->P = cm->nranks;
     d->loopback = cm->loopback != 0;
+    d->peer = cm->peer != 0;
     d->nx = st->nx;
     d->ny = st->ny;
     d->kind0 = st->kind;
@@ -595,6 +786,11 @@ bmg_status_t dist_setup(const bmg_stencil_t *st, const bmg_comm_t *cm, const bmg
             return fail(rc);
         }
     }
+    if (d->peer) {
+        bmg_status_t rc = peer_setup(d, s, err);
+        if (rc != BMG_OK)
+            return fail(rc);
+    }
     *out = d;
     return BMG_OK;
 }
@@ -606,6 +802,8 @@ void dist_destroy(DistSolver *d)
     cudaDeviceSynchronize();
     if (d->inner)
         bmg_destroy(d->inner);
+    for (void *p : d->ipc)
+        cudaIpcCloseMemHandle(p);
     for (void *p : d->allocs)
         cudaFree(p);
     if (d->h_norm)
@@ -659,21 +857,30 @@ static bmg_status_t one_cycle(DistSolver *d, cudaStream_t s, std::string &err)
     int n = 0;
     for (int l = 0; l < K; l++) {
         // level 0: u and f in one group; a coarse level starts from zero (c9), which
-        // its fused down leg does not read -- only f's ghost rows move
+        // its fused down leg does not read -- only f's ghost rows move (peer mode: pushed
+        // by the level above's restriction; wait for the neighbours' previous leg)
         if (l == 0)
             DTRY(exchange2(d, 0, F_U, 0, F_F, s, err));
-        else
+        else if (!d->peer)
             DTRY(exchange(d, l, F_F, s, err));
-        for (auto &R : d->ranks) {
+        if (d->peer)
+            peer_wait(d, s);
+        for (size_t ri = 0; ri < d->ranks.size(); ri++) {
+            SRank &R = d->ranks[ri];
             SLevel &v = R.lv[l];
             const bool last = l + 1 == K;
             double *fc = last ? d->fK : R.lv[l + 1].f;
-            if (!fused_down(R.fp, l, v.op(), civ_of(R, l), v.f, l == 0 ? v.u : nullptr, v.T, fc, nullptr, s,
-                            &n)) {
+            Push q;
+            if (d->peer)
+                q = make_push(d, (int)ri, l, d->pp[ri][l].T, last ? nullptr : d->pp[ri][l + 1].f);
+            if (!fused_down(R.fp, l, v.op(), civ_of(R, l), v.f, l == 0 ? v.u : nullptr, v.T, fc, nullptr, s, &n,
+                            d->peer ? &q : nullptr)) {
                 err = "fused down leg rejected a slab level";
                 return BMG_EINVAL;
             }
         }
+        if (d->peer)
+            peer_signal(d, s);
     }
     // level K: all-gather f_K, one inner V-cycle from a zero guess
     if (!d->loopback) {
@@ -683,21 +890,31 @@ static bmg_status_t one_cycle(DistSolver *d, cudaStream_t s, std::string &err)
     cudaMemsetAsync(d->xK, 0, sizeof(double) * (size_t)(d->nyK + 2) * d->pitchK, s);
     DTRY(bmg_vcycle(d->inner, d->fK, d->xK, 1, s));
     for (int l = K - 1; l >= 0; l--) {
-        if (l + 1 < K)
+        if (d->peer)
+            peer_wait(d, s);  // T_l and u_{l+1} were pushed by the neighbours' earlier legs
+        else if (l + 1 < K)
             DTRY(exchange2(d, l, F_T, l + 1, F_U, s, err));
         else
             DTRY(exchange(d, l, F_T, s, err));
-        for (auto &R : d->ranks) {
+        for (size_t ri = 0; ri < d->ranks.size(); ri++) {
+            SRank &R = d->ranks[ri];
             SLevel &v = R.lv[l];
             const bool last = l + 1 == K;
             const double *ec = last ? d->xK : R.lv[l + 1].u;
             const int eroff = last ? 0 : R.lv[l + 1].roff;
             const int enrows = last ? d->nyK + 2 : R.lv[l + 1].nrows;
-            if (!fused_up(R.fp, l, v.op(), civ_of(R, l), v.f, v.T, ec, eroff, enrows, v.u, s, &n)) {
+            // level 0's u is the caller's array: its ghost rows move with the cycle-start exchange
+            Push q;
+            if (d->peer && l > 0)
+                q = make_push(d, (int)ri, l, d->pp[ri][l].u, nullptr);
+            if (!fused_up(R.fp, l, v.op(), civ_of(R, l), v.f, v.T, ec, eroff, enrows, v.u, s, &n,
+                          d->peer && l > 0 ? &q : nullptr)) {
                 err = "fused up leg rejected a slab level";
                 return BMG_EINVAL;
             }
         }
+        if (d->peer)
+            peer_signal(d, s);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -764,6 +981,14 @@ bmg_status_t dist_resid_norm(DistSolver *d, const double *rhs, const double *x, 
     if (e != cudaSuccess) {
         err = std::string("distributed norm: ") + cudaGetErrorString(e);
         return BMG_ECUDA;
+    }
+    if (d->peer && d->d_perr) {  // a peer wait that gave up (a neighbour never signalled)
+        int pe = 0;
+        cudaMemcpy(&pe, d->d_perr, sizeof(int), cudaMemcpyDeviceToHost);
+        if (pe & ERR_PEER) {
+            err = "peer mode: a neighbour's leg signal never arrived (wait timed out)";
+            return BMG_ENCCL;
+        }
     }
     *norm = sqrt(acc);
     return BMG_OK;

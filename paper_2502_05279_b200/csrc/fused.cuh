@@ -48,14 +48,30 @@ struct FusedPlan {
 bmg_status_t fused_plan_level(FusedPlan &fp, int l, int nx, int ny, long long pitch, int kind, int nu1, int nu2,
                               bool aligned, bool rev = false);
 
+// In-kernel ghost-row push (the row-slab solver's peer mode, dist.cu; SURVEY §8(e)
+// lever 3): the leg's store task also writes each owned row within `halo` rows of the
+// slab's lower / upper edge into the neighbour's copy of the output array (peer
+// pointers, global-row indexed), and the restriction task likewise each coarse row of
+// f_c within `halo` rows of the coarse slab's edges -- the ghost rows the neighbours'
+// next legs read, moved by the kernel that produces them instead of a separate
+// send/recv.  A null pointer: no neighbour on that side.
+struct Push {
+    double *lo = nullptr, *hi = nullptr;
+    int ylo = 0, yhi = 0;
+    double *clo = nullptr, *chi = nullptr;
+    int cylo = 0, cyhi = 0;
+    int halo = 0;
+};
+
 // Down leg of level l: nu1 sweeps on (f, uin) -> uout, fc = P^T(f - A uout), uc = 0 (if non-null).
 // uin == nullptr: a zero start (the correction scheme's coarse levels, c9) that is not read.
 // Returns false if level l is not fused.
 bool fused_down(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const double *f, const double *uin,
-                double *uout, double *fc, double *uc, cudaStream_t s, int *nlaunch);
+                double *uout, double *fc, double *uc, cudaStream_t s, int *nlaunch, const Push *push = nullptr);
 // Up leg: uout = relax^nu2(uin + P ec).
 // ec: coarse correction, global-row indexed, stored rows [eroff, eroff+enrows).
 bool fused_up(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const double *f, const double *uin,
-              const double *ec, int eroff, int enrows, double *uout, cudaStream_t s, int *nlaunch);
+              const double *ec, int eroff, int enrows, double *uout, cudaStream_t s, int *nlaunch,
+              const Push *push = nullptr);
 
 }  // namespace bmg

@@ -263,6 +263,7 @@ struct FArgs {
     int nstrips, chunk, ncx, ncy;
     int eroff;  // stored-row offset of the coarse correction e (up leg)
     int uzero;  // down leg: u_in == 0 (a coarse level's zero start, c9) -- not read
+    Push push;  // ghost rows also stored into the neighbours' arrays (peer mode)
 };
 
 // TMA descriptors of one launch (kernel parameter, __grid_constant__):
@@ -653,15 +654,26 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
             const int h = m + p * NPG, sc = 2 * h, c = xl + sc;
             if (sc < H || sc >= H + TX)
                 continue;
-            double *dst = a.uout + (long long)w * P + c;
             const double ve = urow[h], vo = urow[HW + h];
-            if (c >= 1 && c + 1 <= nx)
-                *reinterpret_cast<double2 *>(dst) = make_double2(ve, vo);
-            else {
-                if (c >= 1 && c <= nx)
-                    dst[0] = ve;
-                if (c + 1 >= 1 && c + 1 <= nx)
-                    dst[1] = vo;
+            auto put = [&](double *base) {
+                double *dst = base + (long long)w * P + c;
+                if (c >= 1 && c + 1 <= nx)
+                    *reinterpret_cast<double2 *>(dst) = make_double2(ve, vo);
+                else {
+                    if (c >= 1 && c <= nx)
+                        dst[0] = ve;
+                    if (c + 1 >= 1 && c + 1 <= nx)
+                        dst[1] = vo;
+                }
+            };
+            put(a.uout);
+            if (a.push.lo && w < a.push.ylo + a.push.halo) {
+                put(a.push.lo);  // the lower neighbour's upper ghost rows
+                __threadfence_system();
+            }
+            if (a.push.hi && w >= a.push.yhi - a.push.halo) {
+                put(a.push.hi);  // the upper neighbour's lower ghost rows
+                __threadfence_system();
             }
         }
     };
@@ -700,6 +712,14 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
                 v += c1[(CI_LB - P0) * WC + ic] * rp[h];
             }
             a.fc[(long long)J * CP + I] = v;
+            if (a.push.clo && J < a.push.cylo + a.push.halo) {
+                a.push.clo[(long long)J * CP + I] = v;
+                __threadfence_system();
+            }
+            if (a.push.chi && J >= a.push.cyhi - a.push.halo) {
+                a.push.chi[(long long)J * CP + I] = v;
+                __threadfence_system();
+            }
             if (a.uc)
                 a.uc[(long long)J * CP + I] = 0.0;
         }
@@ -946,15 +966,26 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
             const int h = m + p * NPG, sc = 2 * h, c = xl + sc;
             if (sc < H || sc >= H + TX)
                 continue;
-            double *dst = a.uout + (long long)w * P + c;
             const double ve = urow[h], vo = urow[HW + h];
-            if (c >= 1 && c + 1 <= nx)
-                *reinterpret_cast<double2 *>(dst) = make_double2(ve, vo);
-            else {
-                if (c >= 1 && c <= nx)
-                    dst[0] = ve;
-                if (c + 1 >= 1 && c + 1 <= nx)
-                    dst[1] = vo;
+            auto put = [&](double *base) {
+                double *dst = base + (long long)w * P + c;
+                if (c >= 1 && c + 1 <= nx)
+                    *reinterpret_cast<double2 *>(dst) = make_double2(ve, vo);
+                else {
+                    if (c >= 1 && c <= nx)
+                        dst[0] = ve;
+                    if (c + 1 >= 1 && c + 1 <= nx)
+                        dst[1] = vo;
+                }
+            };
+            put(a.uout);
+            if (a.push.lo && w < a.push.ylo + a.push.halo) {
+                put(a.push.lo);  // the lower neighbour's upper ghost rows
+                __threadfence_system();
+            }
+            if (a.push.hi && w >= a.push.yhi - a.push.halo) {
+                put(a.push.hi);  // the upper neighbour's lower ghost rows
+                __threadfence_system();
             }
         }
     };
@@ -1374,7 +1405,7 @@ static FArgs make_args(const FusedGeom &g, const Op &A, const CIv &ci)
 }
 
 bool fused_down(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const double *f, const double *uin,
-                double *uout, double *fc, double *uc, cudaStream_t s, int *nlaunch)
+                double *uout, double *fc, double *uc, cudaStream_t s, int *nlaunch, const Push *push)
 {
     if (l >= 32 || !fp.lv[l].down || !ptrs_ok(A, ci, {f, uin, uout, fc, uc}))
         return false;
@@ -1386,6 +1417,8 @@ bool fused_down(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const do
     a.fc = fc;
     a.uc = uc;
     a.uzero = uin == nullptr;
+    if (push)
+        a.push = *push;
     TMaps tm;
     if (!make_maps(tm, g, A, ci, uin ? uin : f, f, nullptr, 0, 0))  // uzero: u map unused
         return false;
@@ -1399,7 +1432,7 @@ bool fused_down(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const do
 }
 
 bool fused_up(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const double *f, const double *uin,
-              const double *ec, int eroff, int enrows, double *uout, cudaStream_t s, int *nlaunch)
+              const double *ec, int eroff, int enrows, double *uout, cudaStream_t s, int *nlaunch, const Push *push)
 {
     if (l >= 32 || !fp.lv[l].up || !ptrs_ok(A, ci, {f, uin, uout, ec}))
         return false;
@@ -1409,6 +1442,8 @@ bool fused_up(const FusedPlan &fp, int l, const Op &A, const CIv &ci, const doub
     a.uin = uin;
     a.ec = ec;
     a.uout = uout;
+    if (push)
+        a.push = *push;
     TMaps tm;
     a.eroff = eroff;
     if (!make_maps(tm, g, A, ci, uin, f, ec, eroff, enrows))

@@ -77,13 +77,14 @@ class DistSolver:
     """One rank of the slab-partitioned solver for a problems.Stencil (global)."""
 
     def __init__(self, stencil, world: int, rank: int, comm, params=None, pitch: int | None = None,
-                 device="cuda", loopback: bool = False, nccl_lib: str | None = None):
+                 device="cuda", loopback: bool = False, nccl_lib: str | None = None, peer: bool = False):
         self.nx, self.ny, self.kind = stencil.nx, stencil.ny, stencil.kind
         self.pitch = pitch or bmg.default_pitch(self.nx)
         self.device = device
         self.loopback = loopback
         c = bmg.bmg_comm_t()
         c.nranks, c.rank, c.loopback = world, rank, 1 if loopback else 0
+        c.peer = 1 if peer else 0
         c.nccl_comm = comm.value if comm is not None else None
         # nccl_lib: another libnccl ABI implementation to dlopen (tests: the one-GPU CUDA-IPC shim)
         c.nccl_lib = (nccl_lib or nccl_lib_path()).encode() if not loopback else None

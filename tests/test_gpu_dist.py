@@ -23,10 +23,11 @@ def _gpu():
     ge.build_lib()
 
 
-def loopback(st, nranks, prm, pitch):
+def loopback(st, nranks, prm, pitch, peer=0):
     planes = [bmg.to_device(p, pitch) for p in st.plane_list()]
     comm = bmg.bmg_comm_t()
     comm.nranks, comm.rank, comm.nccl_comm, comm.nccl_lib, comm.loopback = nranks, 0, None, None, 1
+    comm.peer = peer
     h = bmg.bmg_setup_dist(planes, st.kind, st.nx, st.ny, pitch, comm, prm)
     return h
 
@@ -35,14 +36,17 @@ CASES = [("checker_off3", 255, 2, 16), ("lognormal", 300, 2, 16), ("poisson", 51
          ("aniso", 255, 2, 16), ("lognormal", 300, 3, 16), ("random9", 400, 5, 16), ("poisson", 1023, 8, 32)]
 
 
+@pytest.mark.parametrize("peer", [0, 1])
 @pytest.mark.parametrize("wl,n,nranks,agg", CASES)
-def test_loopback_bitwise_vcycle(wl, n, nranks, agg):
+def test_loopback_bitwise_vcycle(wl, n, nranks, agg, peer):
+    """peer = 1: the ghost rows move by the fused legs' in-kernel stores into the
+    neighbouring slabs (bmg_comm_t.peer) instead of the exchange copies."""
     st = P.workload(wl, n, n)
     prm = bmg.bmg_params_default()
     prm.agglom_rows = agg
     single = bmg.Solver(st, prm)
     pitch = single.pitch
-    h = loopback(st, nranks, prm, pitch)
+    h = loopback(st, nranks, prm, pitch, peer)
     row0, nrows, ylo, yhi, K = bmg.bmg_local_rows(h)
     assert K >= 1
     f = single.grid(P.field_uniform(n, n, seed=51))

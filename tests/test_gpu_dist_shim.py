@@ -50,7 +50,7 @@ def _gpu():
     build_shim()
 
 
-def _rank_main(rank, P, wl, n, agg, path, out_dir, q):
+def _rank_main(rank, P, wl, n, agg, path, out_dir, q, peer=False):
     try:
         import ctypes
         import sys
@@ -69,7 +69,8 @@ def _rank_main(rank, P, wl, n, agg, path, out_dir, q):
         st = Pr.workload(wl, n, n)
         prm = bmg.bmg_params_default()
         prm.agglom_rows = agg
-        ds = D.DistSolver(st, P, rank, ctypes.c_void_p(comm), prm, pitch=bmg.default_pitch(n), nccl_lib=SHIM_LIB)
+        ds = D.DistSolver(st, P, rank, ctypes.c_void_p(comm), prm, pitch=bmg.default_pitch(n), nccl_lib=SHIM_LIB,
+                          peer=peer)
         f = Pr.field_uniform(n, n, seed=91)
         x0 = Pr.field_uniform(n, n, seed=92)
         fl, xl = ds.local(f), ds.local(x0)
@@ -164,15 +165,18 @@ def test_shim_itself(P):
 CASES = [("checker", 511, 2, 32), ("lognormal", 300, 3, 16), ("poisson", 1023, 4, 32), ("random9", 400, 2, 16)]
 
 
+@pytest.mark.parametrize("peer", [False, True])
 @pytest.mark.parametrize("wl,n,P,agg", CASES)
-def test_nccl_mode_multi_rank(orc, wl, n, P, agg):
+def test_nccl_mode_multi_rank(orc, wl, n, P, agg, peer):
+    """peer = True: the in-kernel ghost-row stores into CUDA-IPC-mapped neighbour arrays and
+    the system-scope signal/wait flags between processes (bmg_comm_t.peer)."""
     from paper_2502_05279_b200 import bmg, problems as Pr
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     with tempfile.TemporaryDirectory() as td:
         path = os.path.join(td, "shm")
-        procs = [ctx.Process(target=_rank_main, args=(r, P, wl, n, agg, path, td, q)) for r in range(P)]
+        procs = [ctx.Process(target=_rank_main, args=(r, P, wl, n, agg, path, td, q, peer)) for r in range(P)]
         for p in procs:
             p.start()
         res = [q.get(timeout=600) for _ in range(P)]
