@@ -26,6 +26,7 @@ from paper_2502_05279_b200 import bmg, dist as D, problems as P  # noqa: E402
 
 N = int(os.environ.get("N", "8191"))
 EXCH_US = float(os.environ.get("EXCH_US", "25"))  # assumed latency of one grouped NCCL exchange
+SIG_US = float(os.environ.get("SIG_US", "5"))  # assumed cost of one peer-mode signal + wait pair
 AGGLOM = os.environ.get("AGGLOM")  # params.agglom_rows (default: the library's)
 
 
@@ -44,7 +45,7 @@ def time_cycles(fn, ncyc=20):
 
 st = P.workload("poisson", N, N)
 f_np = P.rhs_const(N, N)
-out = {"n": N, "exch_us_assumed": EXCH_US}
+out = {"n": N, "exch_us_assumed": EXCH_US, "peer_sig_us_assumed": SIG_US}
 prm = bmg.bmg_params_default()
 if AGGLOM:
     prm.agglom_rows = int(AGGLOM)
@@ -66,9 +67,20 @@ for nr in (2, 4, 8):
     si.close()
     slabs = t_lb - t_in
     t_p = slabs / nr + t_in + (2 * K + 1) * EXCH_US / 1e3
+    # peer mode (bmg_comm_t.peer): the legs store their ghost rows into the neighbours'
+    # arrays themselves; left: the cycle-start level-0 exchange and the level-K all-gather
+    # (NCCL) and one signal/wait pair per leg (2K)
+    d = D.DistSolver(st, nr, 0, None, params=prm, loopback=True, peer=True)
+    f, x = d.local(f_np), d.local()
+    t_pe = time_cycles(lambda: d.vcycle(f, x, 1))
+    d.close()
+    slabs_pe = t_pe - t_in
+    t_pp = slabs_pe / nr + t_in + 2 * EXCH_US / 1e3 + 2 * K * SIG_US / 1e3
     out[f"p{nr}"] = {"kdist": K, "loopback_ms": t_lb, "inner_ms": t_in, "slabs_ms": slabs,
                      "slab_overhead_vs_single": slabs / (out["single_ms"] - t_in) if out["single_ms"] > t_in else None,
-                     "projected_ms": t_p, "projected_efficiency": out["single_ms"] / (nr * t_p)}
+                     "projected_ms": t_p, "projected_efficiency": out["single_ms"] / (nr * t_p),
+                     "peer_loopback_ms": t_pe, "peer_projected_ms": t_pp,
+                     "peer_projected_efficiency": out["single_ms"] / (nr * t_pp)}
 # weak scaling (BASELINE config 5): ~4096 rows x nx per GPU, 512-cell 1e6 checkerboard
 if os.environ.get("WEAK", "1") == "1":
     weak = {}
