@@ -215,6 +215,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="one kernel per method step (debug/comparison)")
     ap.add_argument("--dist", action="store_true", help="use the row-slab NCCL solver even on one GPU")
+    ap.add_argument("--peer", action="store_true",
+                    help="row slabs: ghost rows by in-kernel peer stores (bmg_comm_t.peer, CUDA IPC) instead of NCCL")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--relax", default="point", choices=sorted(RELAX),
                     help="relaxation: point GS (c6, default) or zebra line GS (c11)")
@@ -255,11 +257,11 @@ def main():
         from paper_2502_05279_b200 import dist as D
 
         comm = D.nccl_comm(world, rank)
-        solver = D.DistSolver(st, world, rank, comm, prm)
+        solver = D.DistSolver(st, world, rank, comm, prm, peer=args.peer)
         f = solver.local(P.rhs_const(nx, ny))
         x = solver.local()
-        parallelism = (f"{world} row slabs (NCCL ghost-row exchange, coarse levels all-gathered below "
-                       f"level {solver.kdist})")
+        parallelism = (f"{world} row slabs ({'in-kernel peer ghost-row stores' if args.peer else 'NCCL ghost-row exchange'}"
+                       f", coarse levels all-gathered below level {solver.kdist})")
         scaling = "strong"
     else:
         # a throwaway setup + cycle on a small grid first, so that the timed setup
