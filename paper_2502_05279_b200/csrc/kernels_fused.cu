@@ -266,6 +266,41 @@ struct FArgs {
     Push push;  // ghost rows also stored into the neighbours' arrays (peer mode)
 };
 
+// Peer mode (Push): the owned row w (columns c, c+1) also into the neighbours' ghost
+// rows when it lies within `halo` rows of the slab's edge; system fence so that the
+// leg's completion signal (dist.cu) orders these remote stores.  Out of line: the
+// single-GPU legs pay one uniform branch.
+__device__ __noinline__ void push_row(const Push &q, int w, long long off, int c, int nx, double ve, double vo)
+{
+    double *t[2] = {q.lo && w < q.ylo + q.halo ? q.lo : nullptr, q.hi && w >= q.yhi - q.halo ? q.hi : nullptr};
+    for (int k = 0; k < 2; k++) {
+        if (!t[k])
+            continue;
+        double *dst = t[k] + off;
+        if (c >= 1 && c + 1 <= nx)
+            *reinterpret_cast<double2 *>(dst) = make_double2(ve, vo);
+        else {
+            if (c >= 1 && c <= nx)
+                dst[0] = ve;
+            if (c + 1 >= 1 && c + 1 <= nx)
+                dst[1] = vo;
+        }
+        __threadfence_system();
+    }
+}
+
+__device__ __noinline__ void push_coarse(const Push &q, int J, long long off, double v)
+{
+    if (q.clo && J < q.cylo + q.halo) {
+        q.clo[off] = v;
+        __threadfence_system();
+    }
+    if (q.chi && J >= q.cyhi - q.halo) {
+        q.chi[off] = v;
+        __threadfence_system();
+    }
+}
+
 // TMA descriptors of one launch (kernel parameter, __grid_constant__):
 // u (rows of u_in), f, a (the operator's plane block, 3-D), c (the 8 weight
 // planes, 3-D), e (coarse correction, up leg).
@@ -519,7 +554,9 @@ __device__ __forceinline__ void split_row(double *smM, const double *smS, int ss
 }
 
 // ------------------------------------------------------------------ down kernel
-template <int KIND, int NS, int WD, int D, int PPT, int E>
+// PUSH: the peer mode's ghost-row stores (a separate instance: the single-GPU legs'
+// code is unchanged by them)
+template <int KIND, int NS, int WD, int D, int PPT, int E, bool PUSH = false>
 __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
     k_fused_down(FArgs a, const __grid_constant__ TMaps tmaps)
 {
@@ -654,27 +691,18 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
             const int h = m + p * NPG, sc = 2 * h, c = xl + sc;
             if (sc < H || sc >= H + TX)
                 continue;
+            double *dst = a.uout + (long long)w * P + c;
             const double ve = urow[h], vo = urow[HW + h];
-            auto put = [&](double *base) {
-                double *dst = base + (long long)w * P + c;
-                if (c >= 1 && c + 1 <= nx)
-                    *reinterpret_cast<double2 *>(dst) = make_double2(ve, vo);
-                else {
-                    if (c >= 1 && c <= nx)
-                        dst[0] = ve;
-                    if (c + 1 >= 1 && c + 1 <= nx)
-                        dst[1] = vo;
-                }
-            };
-            put(a.uout);
-            if (a.push.lo && w < a.push.ylo + a.push.halo) {
-                put(a.push.lo);  // the lower neighbour's upper ghost rows
-                __threadfence_system();
+            if (c >= 1 && c + 1 <= nx)
+                *reinterpret_cast<double2 *>(dst) = make_double2(ve, vo);
+            else {
+                if (c >= 1 && c <= nx)
+                    dst[0] = ve;
+                if (c + 1 >= 1 && c + 1 <= nx)
+                    dst[1] = vo;
             }
-            if (a.push.hi && w >= a.push.yhi - a.push.halo) {
-                put(a.push.hi);  // the upper neighbour's lower ghost rows
-                __threadfence_system();
-            }
+            if constexpr (PUSH)
+                push_row(a.push, w, (long long)w * P + c, c, nx, ve, vo);
         }
     };
     // restriction (fig:restrict_kernel) of coarse row J at the coarse points centred on columns 2h
@@ -712,14 +740,8 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
                 v += c1[(CI_LB - P0) * WC + ic] * rp[h];
             }
             a.fc[(long long)J * CP + I] = v;
-            if (a.push.clo && J < a.push.cylo + a.push.halo) {
-                a.push.clo[(long long)J * CP + I] = v;
-                __threadfence_system();
-            }
-            if (a.push.chi && J >= a.push.cyhi - a.push.halo) {
-                a.push.chi[(long long)J * CP + I] = v;
-                __threadfence_system();
-            }
+            if constexpr (PUSH)
+                push_coarse(a.push, J, (long long)J * CP + I, v);
             if (a.uc)
                 a.uc[(long long)J * CP + I] = 0.0;
         }
@@ -817,7 +839,7 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
 // REV (the symmetric cycle's adjoint post-smoother, c12): colours in reverse
 // order -- 5-point black before red, 9-point 3, 2, 1, 0 (odd rows first, odd
 // columns first) -- and the correction skips the points of that first pass.
-template <int KIND, int NS, int WD, int D, int PPT, int E, bool REV = false>
+template <int KIND, int NS, int WD, int D, int PPT, int E, bool REV = false, bool PUSH = false>
 __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
     k_fused_up(FArgs a, const __grid_constant__ TMaps tmaps)
 {
@@ -966,27 +988,18 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
             const int h = m + p * NPG, sc = 2 * h, c = xl + sc;
             if (sc < H || sc >= H + TX)
                 continue;
+            double *dst = a.uout + (long long)w * P + c;
             const double ve = urow[h], vo = urow[HW + h];
-            auto put = [&](double *base) {
-                double *dst = base + (long long)w * P + c;
-                if (c >= 1 && c + 1 <= nx)
-                    *reinterpret_cast<double2 *>(dst) = make_double2(ve, vo);
-                else {
-                    if (c >= 1 && c <= nx)
-                        dst[0] = ve;
-                    if (c + 1 >= 1 && c + 1 <= nx)
-                        dst[1] = vo;
-                }
-            };
-            put(a.uout);
-            if (a.push.lo && w < a.push.ylo + a.push.halo) {
-                put(a.push.lo);  // the lower neighbour's upper ghost rows
-                __threadfence_system();
+            if (c >= 1 && c + 1 <= nx)
+                *reinterpret_cast<double2 *>(dst) = make_double2(ve, vo);
+            else {
+                if (c >= 1 && c <= nx)
+                    dst[0] = ve;
+                if (c + 1 >= 1 && c + 1 <= nx)
+                    dst[1] = vo;
             }
-            if (a.push.hi && w >= a.push.yhi - a.push.halo) {
-                put(a.push.hi);  // the upper neighbour's lower ghost rows
-                __threadfence_system();
-            }
+            if constexpr (PUSH)
+                push_row(a.push, w, (long long)w * P + c, c, nx, ve, vo);
         }
     };
 
@@ -1198,13 +1211,18 @@ static void set_attrs(size_t optin)
 {
     using I = Inst<KIND, NS>;
     constexpr size_t sd = I::CD::SMEM, su = I::CU::SMEM;
-    if (sd <= optin)
+    if (sd <= optin) {
         cudaFuncSetAttribute(k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN, I::E_DN>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sd);
+        cudaFuncSetAttribute(k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN, I::E_DN, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sd);
+    }
     if (su <= optin) {
         cudaFuncSetAttribute(k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)su);
         cudaFuncSetAttribute(k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)su);
+        cudaFuncSetAttribute(k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP, false, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)su);
     }
     cudaGetLastError();  // an unsupported instance is simply not planned (plan_grid checks the size)
@@ -1373,7 +1391,12 @@ template <int KIND, int NS>
 static void launch_down(const FusedGeom &g, const FArgs &a, const TMaps &tm, cudaStream_t s)
 {
     using I = Inst<KIND, NS>;
-    k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN, I::E_DN><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a, tm);
+    if (a.push.halo)
+        k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN, I::E_DN, true>
+            <<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a, tm);
+    else
+        k_fused_down<KIND, NS, I::WD_DN, I::D_DN, I::PPT_DN, I::E_DN><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a,
+                                                                                                                   tm);
 }
 
 template <int KIND, int NS>
@@ -1383,6 +1406,9 @@ static void launch_up(const FusedGeom &g, const FArgs &a, const TMaps &tm, cudaS
     if (g.rev)
         k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP, true><<<g.nstrips * g.nchunks, g.threads, g.smem,
                                                                             s>>>(a, tm);
+    else if (a.push.halo)
+        k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP, false, true>
+            <<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a, tm);
     else
         k_fused_up<KIND, NS, I::WD_UP, I::D_UP, I::PPT_UP, I::E_UP><<<g.nstrips * g.nchunks, g.threads, g.smem, s>>>(a,
                                                                                                                    tm);
