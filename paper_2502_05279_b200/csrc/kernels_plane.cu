@@ -364,6 +364,28 @@ __global__ void kP_relax(OpP A, const double *__restrict__ f, double *__restrict
     u[p] = (f[p] - offP(a, u, p, A.g.px)) * rcp_pos(a.o);
 }
 
+// 9-point plane levels: a sweep in two launches.  Colours 0, 1 live on the even rows
+// and colour 1 depends only on colour 0 of its own row and on the (untouched) odd
+// rows, colours 2, 3 likewise on the odd rows, so one CTA per (row, plane) runs the
+// row's first colour, a barrier, its second colour -- in place, since no other CTA
+// touches that row -- and a sweep is two launches instead of four.  Same per-point
+// expression as kP_relax: the same iterate.
+__global__ void kP_relax9_rows(OpP A, const double *__restrict__ f, double *__restrict__ u, Batch bt, int odd)
+{
+    const int k = bt.k0 + 2 * blockIdx.z, j = 2 * blockIdx.x + (odd ? 1 : 2);
+    if (j > A.g.ny)
+        return;
+    const long long Y = A.g.px, base = (long long)k * A.g.ps + (long long)j * Y;
+    for (int c = 0; c < 2; c++) {  // i even, then i odd
+        for (int i = (c ? 1 : 2) + 2 * threadIdx.x; i <= A.g.nx; i += 2 * blockDim.x) {
+            const long long p = base + i;
+            const R9 a = rowP(A, p);
+            u[p] = (f[p] - offP(a, u, p, Y)) * rcp_pos(a.o);
+        }
+        __syncthreads();
+    }
+}
+
 void launchP_relax(const OpP &A, const double *f, double *u, Batch b, cudaStream_t s)
 {
     const int hx = (A.g.nx + 1) / 2;
@@ -372,9 +394,9 @@ void launchP_relax(const OpP &A, const double *f, double *u, Batch b, cudaStream
         for (int c = 0; c < 2; c++)
             kP_relax<5><<<grid, 128, 0, s>>>(A, f, u, b, c);
     } else {
-        dim3 grid((hx + 127) / 128, (A.g.ny + 1) / 2, b.nb);
-        for (int c = 0; c < 4; c++)
-            kP_relax<9><<<grid, 128, 0, s>>>(A, f, u, b, c);
+        const int nt = hx <= 32 ? 32 : hx <= 64 ? 64 : 128;
+        kP_relax9_rows<<<dim3(A.g.ny / 2, 1, b.nb), nt, 0, s>>>(A, f, u, b, 0);
+        kP_relax9_rows<<<dim3((A.g.ny + 1) / 2, 1, b.nb), nt, 0, s>>>(A, f, u, b, 1);
     }
 }
 
