@@ -58,6 +58,7 @@ struct Level3 {
     double *ci[26] = {};  // weights from level l+1 (its grid)
     std::vector<PLevel> pv;  // plane hierarchy (relax = planes, non-coarsest levels)
     double *pr = nullptr;    // plane level-0 residual scratch (3-D sized)
+    double *pt = nullptr;    // 5-point plane level 0: the one-pass sweep's second buffer (3-D sized)
     int ptail = 1 << 30;     // first plane level run by the plane tail (kernels_plane.cu)
     double *rc27 = nullptr;  // 27-point point relaxation: colour-major full rows (kernels3.cu)
     double *tmp = nullptr;   // 7-point point relaxation: the second buffer of the one-pass sweep (k3_rb7)
@@ -170,6 +171,8 @@ bmg_status_t plane_setup(bmg3_solver *h, Level3 &v, cudaStream_t s)
     const int M = (int)v.pv.size();
     if (M > 1)
         TRY(alloc(h, gsize(v.g), &v.pr, s));
+    if (M > 1 && v.pv[0].kind == 5)
+        TRY(alloc(h, gsize(v.g), &v.pt, s));
     for (int m = 0; m + 1 < M; m++) {
         PLevel &a = v.pv[m], &c = v.pv[m + 1];
         for (int q = 0; q < 8; q++)
@@ -230,6 +233,15 @@ void plane_vcycle(Level3 &v, int m, double *u, const double *f, Batch b, cudaStr
     }
     PLevel &c = v.pv[m + 1];
     double *r = m == 0 ? v.pr : a.r;
+    if (m == 0 && v.pt) {  // 5-point plane level: one-pass sweeps u -> pt, (correct pt,) pt -> u
+        launchP_rb5(A, f, u, v.pt, b, s);
+        launchP_residual(A, f, v.pt, r, b, s);
+        launchP_restrict(A, a.cip(c.g), r, c.f, c.u, b, s);
+        plane_vcycle(v, m + 1, c.u, c.f, b, s);
+        launchP_interp_add(a.g, a.cip(c.g), c.u, v.pt, b, s);
+        launchP_rb5(A, f, v.pt, u, b, s);
+        return;
+    }
     launchP_relax(A, f, u, b, s);
     launchP_residual(A, f, u, r, b, s);
     launchP_restrict(A, a.cip(c.g), r, c.f, c.u, b, s);

@@ -111,6 +111,8 @@ void launchP_interp(const OpP &A, double *const ci[8], const Grid3 &cg, int *err
 void launchP_rap(const OpP &A, const CIP &ci, double *const dst[5], cudaStream_t s);
 void launchP_assemble_chol(const OpP &A, double *L, int *err, cudaStream_t s);
 void launchP_relax(const OpP &A, const double *f, double *u, Batch b, cudaStream_t s);
+// 5-point plane levels: one red-black sweep uout = GS(uin) in one pass (uin != uout)
+void launchP_rb5(const OpP &A, const double *f, const double *uin, double *uout, Batch b, cudaStream_t s);
 void launchP_residual(const OpP &A, const double *f, const double *u, double *r, Batch b, cudaStream_t s);
 void launchP_restrict(const OpP &A, const CIP &ci, const double *r, double *fc, double *uc, Batch b,
                       cudaStream_t s);

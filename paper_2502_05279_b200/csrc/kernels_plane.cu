@@ -364,6 +364,68 @@ __global__ void kP_relax(OpP A, const double *__restrict__ f, double *__restrict
     u[p] = (f[p] - offP(a, u, p, A.g.px)) * rcp_pos(a.o);
 }
 
+// 5-point plane levels (the in-plane part of a 7-point level): a red-black sweep
+// uout = GS(uin) in ONE pass over the colour's planes -- the 2-D form of k3_rb7: a CTA
+// owns a strip of 256 points, 32 rows and one plane, marches up the rows (red of row j
+// on the strip plus a one-point ring from uin, a barrier, black of row j-1 from the
+// 4-row shared ring, row j-1 written out whole).  Same per-point expression as
+// kP_relax<5> (offP with the zero corner terms).
+constexpr int PRB_NT = 128, PRB_TX = 2 * PRB_NT, PRB_RC = 32;
+
+__device__ __forceinline__ double offP_v(const R9 &a, double sw, double s, double se, double w, double e, double nw,
+                                         double n, double ne)
+{
+    return a.sw * sw + a.s * s + a.se * se + a.w * w + a.e * e + a.nw * nw + a.n * n + a.ne * ne;
+}
+
+__global__ void __launch_bounds__(PRB_NT) kP_rb5(OpP A, const double *__restrict__ f, const double *__restrict__ uin,
+                                                 double *__restrict__ uout, Batch bt)
+{
+    __shared__ double red[4][PRB_TX + 2];
+    const int k = bt.k0 + 2 * blockIdx.z, nx = A.g.nx, ny = A.g.ny;
+    const long long Y = A.g.px, base = (long long)k * A.g.ps;
+    const int i0 = blockIdx.x * PRB_TX + 1, jb = blockIdx.y * PRB_RC + 1, je = min(jb + PRB_RC, ny + 1);
+    const int tid = threadIdx.x;
+    for (int j = jb - 1; j <= je; j++) {
+        double *rj = red[j & 3];
+        for (int t = tid; t <= PRB_NT; t += PRB_NT) {
+            const int i = i0 - 1 + 2 * t + ((i0 - 1 + j) & 1);
+            double v = 0.0;
+            if (j >= 1 && j <= ny && i >= 1 && i <= nx) {
+                const long long p = base + (long long)j * Y + i;
+                const R9 a = rowP(A, p);
+                v = (f[p] - offP_v(a, uin[p - Y - 1], uin[p - Y], uin[p - Y + 1], uin[p - 1], uin[p + 1],
+                                   uin[p + Y - 1], uin[p + Y], uin[p + Y + 1])) *
+                    rcp_pos(a.o);
+            }
+            if (i - (i0 - 1) < PRB_TX + 2)
+                rj[i - (i0 - 1)] = v;
+        }
+        __syncthreads();
+        const int jj = j - 1;
+        if (jj >= jb && jj < je) {
+            const int ia = i0 + 2 * tid;
+            const int ib = ia + (((ia + jj) & 1) ? 0 : 1), ir = ib == ia ? ia + 1 : ia;  // black, red of the pair
+            const double *rl = red[(jj - 1) & 3], *rm = red[jj & 3], *rh = red[j & 3];
+            const long long row = base + (long long)jj * Y;
+            if (ib <= nx) {
+                const long long p = row + ib;
+                const int x = ib - (i0 - 1);
+                const R9 a = rowP(A, p);
+                uout[p] = (f[p] - offP_v(a, 0.0, rl[x], 0.0, rm[x - 1], rm[x + 1], 0.0, rh[x], 0.0)) * rcp_pos(a.o);
+            }
+            if (ir <= nx)
+                uout[row + ir] = rm[ir - (i0 - 1)];
+        }
+    }
+}
+
+void launchP_rb5(const OpP &A, const double *f, const double *uin, double *uout, Batch b, cudaStream_t s)
+{
+    dim3 grid((A.g.nx + PRB_TX - 1) / PRB_TX, (A.g.ny + PRB_RC - 1) / PRB_RC, b.nb);
+    kP_rb5<<<grid, PRB_NT, 0, s>>>(A, f, uin, uout, b);
+}
+
 // 9-point plane levels: a sweep in two launches.  Colours 0, 1 live on the even rows
 // and colour 1 depends only on colour 0 of its own row and on the (untouched) odd
 // rows, colours 2, 3 likewise on the odd rows, so one CTA per (row, plane) runs the
