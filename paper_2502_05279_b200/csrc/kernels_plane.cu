@@ -603,6 +603,26 @@ namespace bmg3 {
 __device__ void pt_relax(const OpP &A, const double *f, double *u, long long base)
 {
     const int nx = A.g.nx, ny = A.g.ny, ncol = A.kind == 5 ? 2 : 4;
+    if (A.kind == 9) {
+        // a warp per row: colours 0, 1 of the even rows (the second only after the first
+        // within the row: __syncwarp), one barrier, colours 2, 3 of the odd rows -- two CTA
+        // barriers per sweep instead of four (same updates, same order per point)
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (int odd = 0; odd < 2; odd++) {
+            for (int j = (odd ? 1 : 2) + 2 * warp; j <= ny; j += 2 * nw) {
+                for (int c = 0; c < 2; c++) {
+                    for (int i = (c ? 1 : 2) + 2 * lane; i <= nx; i += 64) {
+                        const long long p = base + (long long)j * A.g.px + i;
+                        const R9 a = rowP(A, p);
+                        u[p] = (f[p] - offP(a, u, p, A.g.px)) * rcp_pos(a.o);
+                    }
+                    __syncwarp();
+                }
+            }
+            __syncthreads();
+        }
+        return;
+    }
     for (int c = 0; c < ncol; c++) {
         const int hx = (nx + 1) / 2;
         const int rows = A.kind == 5 ? ny : (ny + 1) / 2;
