@@ -448,7 +448,7 @@ template <int AM, int WD, int PPT>
 __device__ __forceinline__ void colour_pair9(double *sm, int s0, int sm1, int sp1, const Cols<PPT> &k, int bar,
                                              int nthreads)
 {
-    constexpr int HW = WD / 2, OI = 7;
+    constexpr int OI = 7;
     const int b0 = s0 * WD, bm = sm1 * WD, bp = sp1 * WD;
     double keep[PPT][6];  // u(r-1,2h), u(r-1,2h+1), u(r+1,2h), u(r+1,2h+1), W(2h+1), new u(2h)
 #pragma unroll
@@ -801,7 +801,10 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, false, PPT, E>::NT, 1)
                     split_row<NA, AM, WD, PPT, NPG, true>(sm, smS, tsd, tm, QSPLIT, NA, m);
             }
         } else if (grp < NSG) {
-            rg.wait(grp, t - 1);
+            // a 9-point stage's idle step (every other one) reads and writes nothing, so it
+            // arrives without waiting (the idle steps of its consumers follow it)
+            if (KIND == 5 || ((t + grp + 1) & 1))
+                rg.wait(grp, t - 1);
             if (KIND == 5) {
                 const int k = grp + 1, d = 2 * k, r = t - d;
                 if (r > lo && r < hi && r >= 1 && r <= ny)
@@ -1053,7 +1056,8 @@ __global__ void __launch_bounds__(Cfg<KIND, NS, WD, D, true, PPT, E>::NT, 1)
             rg.wait(R_CORR, t - 1);
             correct_task(t - 1, back<RM>(tm, 1), grp - G_CORR);
         } else if (grp < G_ST0 + NSG) {
-            rg.wait(grp - G_ST0, t - 1);
+            if (KIND == 5 || (((t + grp - G_ST0 + 1) & 1) == (REV ? 1 : 0)))  // idle 9-point steps: no wait
+                rg.wait(grp - G_ST0, t - 1);
             if (KIND == 5) {
                 const int k = grp - G_ST0 + 1, d = 2 * k + 1, r = t - d;
                 const int col = REV ? (k & 1) : ((k - 1) & 1);  // stage k's colour
