@@ -235,13 +235,16 @@ void launch_zero_col_block(int K, const Op &A, double *x, int col, cudaStream_t 
 
 // Small levels l0..L-1 of the cycle in one single-CTA launch (k_tail).  Lives in
 // device memory (filled once at setup); level 0's f/u are launch arguments.
+// row pitch of a level's shared-memory copy in k_tail_sm (compact)
+__host__ __device__ inline int tail_wp(int nx) { return nx + 2; }
+
 struct TailLevel {
     Op A;
     CIv ci;                // weights to level l+1 (unused on L-1)
     double *f, *u, *r;     // level arrays (l > 0); r: residual scratch
     // shared-memory copy (k_tail_sm): compact pitch nx+2; offsets in doubles of u, f, r,
-    // the plane block and the 8 weight planes (on level l+1's compact grid)
-    int so_u, so_f, so_r, so_pl, so_ci;
+    // the plane block, the 8 weight planes (on level l+1's compact grid) and 1/a_pp
+    int so_u, so_f, so_r, so_pl, so_ci, so_di;
 };
 struct TailPlan {
     int l0, L, nu1, nu2;

@@ -462,17 +462,23 @@ void launch_cg_direction(const Op &A, const double *sc, int inum, int iden, cons
 // ---------------------------------------------------------------- coarsest solve
 // u = A_L^{-1} f with the setup Cholesky factor: forward then backward
 // substitution (fig:vcycle_flowchart "Cholesky"), one CTA, the
-// right-hand side staged in shared memory (n <= 6144).
-// b: n doubles of shared memory; all threads of the CTA call this.
+// right-hand side staged in shared memory (n <= 6144).  The pivots' reciprocals
+// 1/L_kk are formed first, all at once, so the substitutions' dependent chain holds
+// multiplications instead of one FP64 division per unknown (a division is a ~40-
+// instruction sequence; the chain of 2n of them was ~3 us of the tail at n = 9).
+// b: 2n doubles of shared memory (b, then 1/L_kk); all threads of the CTA call this.
 __device__ __forceinline__ void coarse_solve_cta(const Op &A, const double *__restrict__ Lf,
                                                  const double *__restrict__ f, double *__restrict__ u, double *b)
 {
     int n = A.nx * A.ny;
-    for (int p = threadIdx.x; p < n; p += blockDim.x)
+    double *rd = b + n;
+    for (int p = threadIdx.x; p < n; p += blockDim.x) {
         b[p] = f[(p / A.nx + 1) * A.pitch + p % A.nx + 1];
+        rd[p] = 1.0 / Lf[(long long)p * n + p];
+    }
     __syncthreads();
     for (int k = 0; k < n; k++) {  // L y = b
-        double bk = b[k] / Lf[(long long)k * n + k];
+        double bk = b[k] * rd[k];
         __syncthreads();
         if (threadIdx.x == 0)
             b[k] = bk;
@@ -481,7 +487,7 @@ __device__ __forceinline__ void coarse_solve_cta(const Op &A, const double *__re
         __syncthreads();
     }
     for (int k = n - 1; k >= 0; k--) {  // L^T x = y
-        double bk = b[k] / Lf[(long long)k * n + k];
+        double bk = b[k] * rd[k];
         __syncthreads();
         if (threadIdx.x == 0)
             b[k] = bk;
@@ -493,23 +499,24 @@ __device__ __forceinline__ void coarse_solve_cta(const Op &A, const double *__re
         u[(p / A.nx + 1) * A.pitch + p % A.nx + 1] = b[p];
 }
 
-// The same two substitutions by ONE warp for n <= 32 unknowns (lane i holds b_i;
-// x_k is broadcast by a shuffle): the CTA version pays two __syncthreads per
+// The same two substitutions by ONE warp for n <= 32 unknowns (lane i holds b_i and
+// 1/L_ii; x_k is broadcast by a shuffle): the CTA version pays two __syncthreads per
 // unknown.  Identical operations in identical order, so bitwise the same result.
 __device__ __forceinline__ void coarse_solve_warp(const Op &A, const double *__restrict__ Lf,
                                                   const double *__restrict__ f, double *__restrict__ u)
 {
     const int n = A.nx * A.ny, i = threadIdx.x & 31;
     double b = i < n ? f[(i / A.nx + 1) * A.pitch + i % A.nx + 1] : 0.0;
+    const double rd = i < n ? 1.0 / Lf[(long long)i * n + i] : 0.0;
     for (int k = 0; k < n; k++) {  // L y = b
-        const double bk = __shfl_sync(0xffffffffu, b, k) / Lf[(long long)k * n + k];
+        const double bk = __shfl_sync(0xffffffffu, b, k) * __shfl_sync(0xffffffffu, rd, k);
         if (i == k)
             b = bk;
         else if (i > k && i < n)
             b -= Lf[(long long)i * n + k] * bk;
     }
     for (int k = n - 1; k >= 0; k--) {  // L^T x = y
-        const double bk = __shfl_sync(0xffffffffu, b, k) / Lf[(long long)k * n + k];
+        const double bk = __shfl_sync(0xffffffffu, b, k) * __shfl_sync(0xffffffffu, rd, k);
         if (i == k)
             b = bk;
         else if (i < k)
@@ -529,7 +536,16 @@ void launch_coarse_solve(const Op &A, const double *Lf, const double *f, double 
 {
     int n = A.nx * A.ny;
     int threads = n < 32 ? 32 : (n < 1024 ? ((n + 31) / 32) * 32 : 1024);
-    k_coarse_solve<<<1, threads, sizeof(double) * n, s>>>(A, Lf, f, u);
+    const size_t smem = 2 * sizeof(double) * n;  // b and 1/L_kk: > 48 KB beyond 3072 unknowns
+    if (smem > 48 * 1024) {
+        static std::once_flag once[64];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::call_once(once[dev & 63], []() {
+            cudaFuncSetAttribute(k_coarse_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 8 * 6144);
+        });
+    }
+    k_coarse_solve<<<1, threads, smem, s>>>(A, Lf, f, u);
 }
 
 // ---------------------------------------------------------------- tail kernel
@@ -655,18 +671,19 @@ bool tail_plan_smem(TailPlan &tp, int ncoarse, long long limit)
     };
     for (int l = tp.l0; l < tp.L; l++) {
         TailLevel &v = tp.lv[l];
-        const long long np = (long long)(v.A.ny + 2) * (v.A.nx + 2);
+        const long long np = (long long)(v.A.ny + 2) * tail_wp(v.A.nx);
         v.so_u = take(np);
         v.so_f = take(np);
         v.so_r = take(np);
         v.so_pl = take(np * (v.A.kind == 9 ? 5 : 3));
+        v.so_di = take(np);
         if (l + 1 < tp.L) {
             const TailLevel &c = tp.lv[l + 1];
-            v.so_ci = take(8LL * (c.A.ny + 2) * (c.A.nx + 2));
+            v.so_ci = take(8LL * (c.A.ny + 2) * tail_wp(c.A.nx));
         }
     }
     tp.so_chol = take((long long)ncoarse * ncoarse);
-    tp.so_b = take(ncoarse > 0 ? ncoarse : 1);
+    tp.so_b = take(ncoarse > 0 ? 2 * ncoarse : 1);
     tp.sm_doubles = (int)off;
     if (off > limit) {
         tp.sm_doubles = 0;
@@ -682,6 +699,10 @@ __device__ __forceinline__ void tail_cp8(double *dst, const double *src)
 }
 
 // copy rows 0..ny+1, cols 0..nx+1 of a pitched array into the compact shared copy
+// (cp.async 8 B per element, all in flight).  Measured (tools/tail_clock.py, 31^2
+// tail): the copy-in takes ~16 K cycles whatever the request shape -- 8-byte
+// elements, 16-byte chunks (24 K), or one 1-D bulk copy per row (16 K) -- so it is
+// the latency of the tail's first touch of these L2 lines, not the request count.
 __device__ __forceinline__ void tail_stage(double *dst, const double *src, long long pitch, int nx, int ny)
 {
     const int w = nx + 2, n = w * (ny + 2);
@@ -689,10 +710,79 @@ __device__ __forceinline__ void tail_stage(double *dst, const double *src, long 
         tail_cp8(dst + e, src + (long long)(e / w) * pitch + e % w);
 }
 
+// BMG_TAIL_CLOCK (tuning aid, tools/ only): thread 0 stamps clock64() after every phase
+// barrier of k_tail_sm into g_tclk (read back by bmg_debug_tail_clock).
+#ifdef BMG_TAIL_CLOCK
+__device__ long long g_tclk[256];
+__device__ int g_tclk_n;
+__shared__ long long s_tclk[128];
+__shared__ int s_tclk_n;
+#define TCLK()                                                \
+    do {                                                      \
+        if (threadIdx.x == 0 && s_tclk_n < 128)               \
+            s_tclk[s_tclk_n++] = clock64();                   \
+    } while (0)
+#else
+#define TCLK() \
+    do {       \
+    } while (0)
+#endif
+
+// Multicolour GS of the shared-memory tail: a 2-D thread map (lane -> column step of
+// 2 (one colour), warp -> row) instead of a divided linear index, and 1/a_pp read from
+// the level's reciprocal plane (formed once per launch by the same rcp_pos), so each
+// point's dependent chain is its loads and the 4 / 8 FMAs.  Same arithmetic, same order
+// as relax5_pt / relax9_pt: bitwise their iterate.
+template <int KIND>
+__device__ __forceinline__ void tail_relax_sm(const Op &A, const double *di, const double *f, double *u, int nsweeps,
+                                              bool rev)
+{
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny_t = blockDim.x >> 5;
+    const int P = (int)A.pitch;
+    for (int sw = 0; sw < nsweeps; sw++) {
+        for (int cc = 0; cc < (KIND == 5 ? 2 : 4); cc++) {
+            const int c = rev ? (KIND == 5 ? 1 : 3) - cc : cc;
+            if (KIND == 5) {
+                for (int j = 1 + ty; j <= A.ny; j += ny_t)
+                    for (int i = (((1 + j) & 1) == c ? 1 : 2) + 2 * tx; i <= A.nx; i += 64) {
+                        const int p = j * P + i;
+                        double acc = A.S[p] * u[p - P];
+                        acc += A.W[p] * u[p - 1];
+                        acc += A.W[p + 1] * u[p + 1];
+                        acc += A.S[p + P] * u[p + P];
+                        u[p] = (f[p] - acc) * di[p];
+                    }
+            } else {
+                for (int j = ((c >> 1) ? 1 : 2) + 2 * ty; j <= A.ny; j += 2 * ny_t)
+                    for (int i = ((c & 1) ? 1 : 2) + 2 * tx; i <= A.nx; i += 64) {
+                        const int p = j * P + i;
+                        double acc = A.SW[p] * u[p - P - 1];
+                        acc += A.S[p] * u[p - P];
+                        acc += A.NW[p - P + 1] * u[p - P + 1];
+                        acc += A.W[p] * u[p - 1];
+                        acc += A.W[p + 1] * u[p + 1];
+                        acc += A.NW[p] * u[p + P - 1];
+                        acc += A.S[p + P] * u[p + P];
+                        acc += A.SW[p + P + 1] * u[p + P + 1];
+                        u[p] = (f[p] - acc) * di[p];
+                    }
+            }
+            __syncthreads();
+            TCLK();
+        }
+    }
+}
+
 __global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail_sm(const TailPlan *__restrict__ tpg0, const double *f0,
                                                                  double *u0)
 {
     extern __shared__ __align__(16) double tsm[];
+#ifdef BMG_TAIL_CLOCK
+    if (threadIdx.x == 0) {
+        s_tclk_n = 0;
+        s_tclk[s_tclk_n++] = clock64();
+    }
+#endif
     // the plan itself in shared memory: every phase reads its level's views from it, and a
     // global (L2) read per phase would cost more than the phase's work
     __shared__ TailPlan tp_s;
@@ -702,15 +792,19 @@ __global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail_sm(const TailPlan 
         for (int e = threadIdx.x; e < (int)(sizeof(TailPlan) / sizeof(int)); e += blockDim.x)
             dst[e] = src[e];
         __syncthreads();
+    TCLK();
     }
     const TailPlan *tpg = &tp_s;
     const int l0 = tpg->l0, L = tpg->L, nt = blockDim.x;
     const int nu1 = tpg->nu1, nu2 = tpg->nu2, rev = tpg->cycle_sym, affine = tpg->affine;
     // copy in: operators and weights of every level, f and u of level l0, the factor
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny_t = nt >> 5;
+    TCLK();
     for (int l = l0; l < L; l++) {
         const TailLevel &v = tpg->lv[l];
         const Op A = v.A;
-        const long long np = (long long)(A.ny + 2) * (A.nx + 2);
+        const int wp = tail_wp(A.nx);
+        const long long np = (long long)(A.ny + 2) * wp;
         const double *pls[5] = {A.O, A.W, A.S, A.SW, A.NW};
         for (int k = 0; k < (A.kind == 9 ? 5 : 3); k++)
             tail_stage(tsm + v.so_pl + k * np, pls[k], A.pitch, A.nx, A.ny);
@@ -720,7 +814,8 @@ __global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail_sm(const TailPlan 
         }
         if (l + 1 < L) {
             const Op Ac = tpg->lv[l + 1].A;
-            const long long npc = (long long)(Ac.ny + 2) * (Ac.nx + 2);
+            const int wpc = tail_wp(Ac.nx);
+            const long long npc = (long long)(Ac.ny + 2) * wpc;
             for (int k = 0; k < 8; k++)
                 tail_stage(tsm + v.so_ci + k * npc, v.ci.w[k], v.ci.pitch, Ac.nx, Ac.ny);
         }
@@ -731,14 +826,27 @@ __global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail_sm(const TailPlan 
         for (int e = threadIdx.x; e < n * n; e += nt)
             tail_cp8(tsm + tpg->so_chol + e, tpg->chol + e);
     }
+    TCLK();
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+    TCLK();
+    // 1/a_pp of every tail level's interior points, once per launch (rcp_pos: the bits
+    // every other relaxation path multiplies by)
+    for (int l = l0; l < L; l++) {
+        const TailLevel &v = tpg->lv[l];
+        const int w = tail_wp(v.A.nx);
+        for (int j = 1 + ty; j <= v.A.ny; j += ny_t)
+            for (int i = 1 + tx; i <= v.A.nx; i += 32)
+                tsm[v.so_di + j * w + i] = rcp_pos(tsm[v.so_pl + j * w + i]);
+    }
+    __syncthreads();
+    TCLK();
     // Op / CIv views of the shared copies
     auto opv = [&](int l) {
         const TailLevel &v = tpg->lv[l];
         Op A = v.A;
-        const long long np = (long long)(A.ny + 2) * (A.nx + 2);
-        A.pitch = A.nx + 2;
+        A.pitch = tail_wp(A.nx);
+        const long long np = (long long)(A.ny + 2) * A.pitch;
         A.O = tsm + v.so_pl;
         A.W = tsm + v.so_pl + np;
         A.S = tsm + v.so_pl + 2 * np;
@@ -749,9 +857,9 @@ __global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail_sm(const TailPlan 
     auto civ = [&](int l) {
         const TailLevel &v = tpg->lv[l];
         const Op Ac = tpg->lv[l + 1].A;
-        const long long npc = (long long)(Ac.ny + 2) * (Ac.nx + 2);
         CIv c;
-        c.pitch = Ac.nx + 2;
+        c.pitch = tail_wp(Ac.nx);
+        const long long npc = (long long)(Ac.ny + 2) * c.pitch;
         c.roff = 0;
         c.nrows = Ac.ny + 2;
         for (int k = 0; k < 8; k++)
@@ -761,26 +869,27 @@ __global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail_sm(const TailPlan 
     auto U = [&](int l) { return tsm + tpg->lv[l].so_u; };
     auto F = [&](int l) { return tsm + tpg->lv[l].so_f; };
     auto R = [&](int l) { return tsm + tpg->lv[l].so_r; };
+    auto DI = [&](int l) { return tsm + tpg->lv[l].so_di; };
     for (int l = l0; l + 1 < L; l++) {
         const Op A = opv(l);
         const CIv ci = civ(l);
         double *u = U(l), *r = R(l);
         const double *f = F(l);
         if (A.kind == 5)
-            tail_relax<5>(A, f, u, nu1, false);
+            tail_relax_sm<5>(A, DI(l), f, u, nu1, false);
         else
-            tail_relax<9>(A, f, u, nu1, false);
-        const int wx = A.nx + 2, cnt = wx * (A.ny + 2);
-        for (int k = threadIdx.x; k < cnt; k += nt) {
-            const int j = k / wx, i = k % wx;
-            r[(long long)j * A.pitch + i] =
-                (i == 0 || j == 0 || i > A.nx || j > A.ny) ? 0.0 : residual_pt(A, f, u, i, j);
-        }
+            tail_relax_sm<9>(A, DI(l), f, u, nu1, false);
+        // residual, ring 0 (rows by warp, columns by lane: no index division)
+        for (int j = ty; j <= A.ny + 1; j += ny_t)
+            for (int i = tx; i <= A.nx + 1; i += 32)
+                r[j * A.pitch + i] = (i == 0 || j == 0 || i > A.nx || j > A.ny) ? 0.0 : residual_pt(A, f, u, i, j);
         __syncthreads();
-        const int cx = A.nx / 2 + 2, ccnt = cx * (A.ny / 2 + 2);
-        for (int k = threadIdx.x; k < ccnt; k += nt)
-            restrict_store(A, ci, r, F(l + 1), U(l + 1), k % cx, k / cx, nu1 > 0);
+    TCLK();
+        for (int J = ty; J <= A.ny / 2 + 1; J += ny_t)
+            for (int I = tx; I <= A.nx / 2 + 1; I += 32)
+                restrict_store(A, ci, r, F(l + 1), U(l + 1), I, J, nu1 > 0);
         __syncthreads();
+    TCLK();
     }
     {
         const Op Ac = opv(L - 1);
@@ -792,37 +901,55 @@ __global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail_sm(const TailPlan 
         }
     }
     __syncthreads();
+    TCLK();
     for (int l = L - 2; l >= l0; l--) {
         const Op A = opv(l);
         const CIv ci = civ(l);
         double *u = U(l);
         const double *e = U(l + 1);
-        const int cnt = A.nx * A.ny;
-        for (int k = threadIdx.x; k < cnt; k += nt) {
-            const int j = k / A.nx + 1, i = k % A.nx + 1;
-            double s = interp_pt(ci, e, i, j);
-            if (affine)
-                s += affine_pt(A, R(l), i, j);
-            u[(long long)j * A.pitch + i] += s;
-        }
+        for (int j = 1 + ty; j <= A.ny; j += ny_t)
+            for (int i = 1 + tx; i <= A.nx; i += 32) {
+                double s = interp_pt(ci, e, i, j);
+                if (affine)
+                    s += affine_pt(A, R(l), i, j);
+                u[j * A.pitch + i] += s;
+            }
         __syncthreads();
+    TCLK();
         if (A.kind == 5)
-            tail_relax<5>(A, F(l), u, nu2, rev);
+            tail_relax_sm<5>(A, DI(l), F(l), u, nu2, rev);
         else
-            tail_relax<9>(A, F(l), u, nu2, rev);
+            tail_relax_sm<9>(A, DI(l), F(l), u, nu2, rev);
     }
     // level l0's iterate back to its array
     {
         const TailLevel &v = tpg->lv[l0];
         double *ug = l0 == 0 ? u0 : v.u;
-        const int nx = v.A.nx, cnt = nx * v.A.ny;
+        const int nx = v.A.nx, wp = tail_wp(nx);
         const double *us = U(l0);
-        for (int k = threadIdx.x; k < cnt; k += nt) {
-            const int j = k / nx + 1, i = k % nx + 1;
-            ug[(long long)j * v.A.pitch + i] = us[j * (nx + 2) + i];
-        }
+        for (int j = 1 + ty; j <= v.A.ny; j += ny_t)
+            for (int i = 1 + tx; i <= nx; i += 32)
+                ug[(long long)j * v.A.pitch + i] = us[j * wp + i];
     }
+    TCLK();
+#ifdef BMG_TAIL_CLOCK
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < s_tclk_n; k++)
+            g_tclk[k] = s_tclk[k];
+        g_tclk_n = s_tclk_n;
+    }
+#endif
 }
+
+#ifdef BMG_TAIL_CLOCK
+extern "C" int bmg_debug_tail_clock(long long *out)
+{
+    int n = 0;
+    cudaMemcpyFromSymbol(&n, g_tclk_n, sizeof(int));
+    cudaMemcpyFromSymbol(out, g_tclk, sizeof(long long) * 256);
+    return n;
+}
+#endif
 
 void launch_tail(const TailPlan *tp_dev, int ncoarse, const double *f0, double *u0, cudaStream_t s, int sm_doubles)
 {
@@ -836,7 +963,16 @@ void launch_tail(const TailPlan *tp_dev, int ncoarse, const double *f0, double *
         k_tail_sm<<<1, BMG_TAIL_THREADS, sizeof(double) * sm_doubles, s>>>(tp_dev, f0, u0);
         return;
     }
-    k_tail<<<1, BMG_TAIL_THREADS, sizeof(double) * (ncoarse > 0 ? ncoarse : 1), s>>>(tp_dev, f0, u0);
+    const size_t smem = sizeof(double) * (ncoarse > 0 ? 2 * ncoarse : 1);  // coarse solve: b and 1/L_kk
+    if (smem > 48 * 1024) {
+        static std::once_flag once[64];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::call_once(once[dev & 63], []() {
+            cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 8 * 6144);
+        });
+    }
+    k_tail<<<1, BMG_TAIL_THREADS, smem, s>>>(tp_dev, f0, u0);
 }
 
 }  // namespace bmg
