@@ -347,6 +347,15 @@ __global__ void __launch_bounds__(RAP_TC *RAP_TR) k_rap_tiled(Op A, CIv ci, int 
     const int fx0 = 2 * I0 - 1, fy0 = 2 * Jt - 2;
     const int ylo = max(A.roff, 0), yhi = min(A.ny + 1, A.roff + A.nrows - 1);
     const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+    // cp.async with zero fill (source size 0 off the grid): every element of the tile in
+    // flight at once -- element-by-element loads into registers left one DRAM round trip
+    // per row chunk on each warp's critical path (ncu: 54 % long-scoreboard stalls)
+    const double *dummy = A.O;  // a valid global address for the zero-fill copies (nothing is read)
+    auto cp8 = [dummy](double *dst, const double *src, bool ok) {
+        const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(ok ? src : dummy), "r"(ok ? 8 : 0)
+                     : "memory");
+    };
     auto stage_plane = [&](const double *src, double (*dst)[RAP_FW]) {
         for (int r = warp; r < RAP_FH; r += nw) {
             const int gy = fy0 + r;
@@ -354,7 +363,8 @@ __global__ void __launch_bounds__(RAP_TC *RAP_TR) k_rap_tiled(Op A, CIv ci, int 
             const double *row = rin ? src + (long long)gy * A.pitch : nullptr;
             for (int c = lane; c < RAP_FW; c += 32) {
                 const int gx = fx0 + c;
-                dst[r][c] = (rin && gx <= A.nx + 1) ? row[gx] : 0.0;
+                const bool ok = rin && gx <= A.nx + 1;
+                cp8(&dst[r][c], ok ? row + gx : nullptr, ok);
             }
         }
     };
@@ -372,10 +382,12 @@ __global__ void __launch_bounds__(RAP_TC *RAP_TR) k_rap_tiled(Op A, CIv ci, int 
             const bool rin = cy >= cylo && cy <= cyhi;
             for (int c = lane; c < RAP_CW; c += 32) {
                 const int cx = I0 - 1 + c;
-                sm.ci[k][r][c] = (rin && cx <= ncx + 1) ? src[(long long)cy * ci.pitch + cx] : 0.0;
+                const bool ok = rin && cx <= ncx + 1;
+                cp8(&sm.ci[k][r][c], ok ? src + (long long)cy * ci.pitch + cx : nullptr, ok);
             }
         }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     const int tx = tid % RAP_TC, ty = tid / RAP_TC;
     const int I = I0 + tx, J = Jt + ty;
