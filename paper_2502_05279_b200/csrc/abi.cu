@@ -838,6 +838,52 @@ bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol,
     cudaStream_t s = (cudaStream_t)cuda_stream;
     if (iters_out)
         *iters_out = 0;
+    // history + state on the device (the graph loop's and the one-launch tail solve's)
+    auto solve_buffers = [&]() -> bmg_status_t {
+        if (h->solve_cap < maxiter + 1) {
+            CK(cudaStreamSynchronize(s));
+            for (auto &kv : h->sgraphs)  // their step nodes point at the old history
+                cudaGraphExecDestroy(kv.second);
+            h->sgraphs.clear();
+            if (h->solve_hist)
+                cudaFree(h->solve_hist);
+            h->solve_hist = nullptr;
+            h->solve_cap = 0;
+            const int cap = maxiter + 1 > 1024 ? maxiter + 1 : 1024;  // rarely reallocated (graphs go with it)
+            void *q;
+            CK(cudaMalloc(&q, sizeof(double) * (size_t)cap + sizeof(SolveState) + 64));
+            h->solve_hist = (double *)q;
+            h->solve_cap = cap;
+            h->solve_st = (SolveState *)(h->solve_hist + h->solve_cap + 1);
+            if (!h->solve_st_h)
+                CK(cudaMallocHost(&h->solve_st_h, sizeof(SolveState)));
+        }
+        return BMG_OK;
+    };
+    // the whole hierarchy in the shared-memory tail (small problems, config 1): norms, cycles
+    // and stopping test in ONE launch, the data staged once; bitwise the
+    // graph loop's iterate and history (tests/test_gpu_solve.py)
+    const char *tso = getenv("BMG_TAIL_SOLVE");  // 0: the graph loop (A/B, tests)
+    const bool tail_solve_off = tso && atoi(tso) == 0;
+    if (!h->dist && !h->timing && h->tail && h->tail_l0 == 0 && h->tail_sm > 0 && !tail_solve_off) {
+        TRY(solve_buffers());
+        *h->solve_st_h = SolveState{0.0, tol, 0, maxiter};
+        CK(cudaMemcpyAsync(h->solve_st, h->solve_st_h, sizeof(SolveState), cudaMemcpyHostToDevice, s));
+        launch_tail_solve(h->tail, rhs, x, h->solve_st, h->solve_hist, s, h->tail_sm);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h->solve_st_h, h->solve_st, sizeof(SolveState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const int k = h->solve_st_h->k;
+        const double fn0 = h->solve_st_h->fn;
+        std::vector<double> hv(k + 1);
+        CK(cudaMemcpy(hv.data(), h->solve_hist, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost));
+        if (hist_host)
+            for (int i = 0; i <= k; i++)
+                hist_host[i] = hv[i];
+        if (iters_out)
+            *iters_out = k;
+        return (fn0 == 0.0 || hv[k] <= tol * fn0) ? BMG_OK : fail(BMG_ENOTCONV, "maxiter reached");
+    }
     double fn;
     if (h->dist) {  // ||rhs|| = residual norm of x = 0
         std::string err;
@@ -881,24 +927,7 @@ bmg_status_t bmg_solve(bmg_solver_t h, const double *rhs, double *x, double tol,
                 hist_host[k] = rn;
         }
     } else if (rn > tol * fn && maxiter > 0) {  // device loop: one graph launch, one wait
-        if (h->solve_cap < maxiter + 1) {
-            CK(cudaStreamSynchronize(s));
-            for (auto &kv : h->sgraphs)  // their step nodes point at the old history
-                cudaGraphExecDestroy(kv.second);
-            h->sgraphs.clear();
-            if (h->solve_hist)
-                cudaFree(h->solve_hist);
-            h->solve_hist = nullptr;
-            h->solve_cap = 0;
-            const int cap = maxiter + 1 > 1024 ? maxiter + 1 : 1024;  // rarely reallocated (graphs go with it)
-            void *q;
-            CK(cudaMalloc(&q, sizeof(double) * (size_t)cap + sizeof(SolveState) + 64));
-            h->solve_hist = (double *)q;
-            h->solve_cap = cap;
-            h->solve_st = (SolveState *)(h->solve_hist + h->solve_cap + 1);
-            if (!h->solve_st_h)
-                CK(cudaMallocHost(&h->solve_st_h, sizeof(SolveState)));
-        }
+        TRY(solve_buffers());
         cudaGraphExec_t ex;
         TRY(get_solve_graph(h, rhs, x, &ex));
         *h->solve_st_h = SolveState{fn, tol, 0, maxiter};

@@ -253,6 +253,7 @@ struct TailPlan {
     const double *chol;    // coarsest Cholesky factor
     int sm_doubles;        // k_tail_sm: shared memory (0: the levels do not fit, k_tail runs)
     int so_chol, so_b;     // k_tail_sm: the Cholesky factor and the solve's scratch
+    int so_part;           // k_tail_solve: the norms' NORM_BLOCKS partials
     TailLevel lv[32];
 };
 // fills the so_* fields and sm_doubles (host); returns false if they exceed `limit` doubles
@@ -269,6 +270,11 @@ struct SolveState {
 // k = ++st->k; hist[k] = *norm; continue while *norm > tol*fn and k < maxiter
 void launch_solve_step(cudaGraphConditionalHandle hd, const double *norm, SolveState *st, double *hist,
                        cudaStream_t s);
+
+// bmg_solve in ONE launch when the whole hierarchy is the shared-memory tail (tail from
+// level 0): reads st->tol, st->maxiter; writes st->fn, st->k and hist[0..k]
+void launch_tail_solve(const TailPlan *tp_dev, const double *f0, double *u0, SolveState *st, double *hist,
+                       cudaStream_t s, int sm_doubles);
 
 // the block solve's state (K columns): continue while any ||r_c|| > tol ||rhs_c||
 struct SolveStateBlock {

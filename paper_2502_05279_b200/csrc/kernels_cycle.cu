@@ -684,6 +684,7 @@ bool tail_plan_smem(TailPlan &tp, int ncoarse, long long limit)
     }
     tp.so_chol = take((long long)ncoarse * ncoarse);
     tp.so_b = take(ncoarse > 0 ? 2 * ncoarse : 1);
+    tp.so_part = take(NORM_BLOCKS);
     tp.sm_doubles = (int)off;
     if (off > limit) {
         tp.sm_doubles = 0;
@@ -773,8 +774,82 @@ __device__ __forceinline__ void tail_relax_sm(const Op &A, const double *di, con
     }
 }
 
-__global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail_sm(const TailPlan *__restrict__ tpg0, const double *f0,
-                                                                 double *u0)
+// ||f|| (RESID = false) or ||f - A u|| over level l0's interior in the shared copies, in
+// EXACTLY the order of launch_norm / launch_resid_norm (k_norm_partial: NORM_BLOCKS
+// blocks of 256 threads, block b the rows ylo + b, ylo + b + NORM_BLOCKS, ..., thread t
+// the columns 1 + t, 1 + t + 256, ..., block_sum's tree; k_norm_final: 1024 threads,
+// thread k partial k, block_sum's tree), each virtual block's 8 virtual warps reduced by
+// one real warp with the same shuffles: bitwise the graph loop's norms.  part: NORM_BLOCKS
+// doubles of shared scratch.  All threads call this; all get the norm.
+template <bool RESID>
+__device__ __forceinline__ double tail_norm(const Op &A, const double *f, const double *u, double *part)
+{
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const long long P = A.pitch;
+    // virtual blocks without rows and virtual warps without columns sum to an exact 0.0,
+    // and adding 0.0 to a sum of squares changes no bit: only the others are evaluated
+    const int nb = min(NORM_BLOCKS, A.yhi - A.ylo), nvw = min(8, (A.nx + 31) / 32);
+    for (int b = w; b < nb; b += nw) {
+        double ws = 0.0;  // lane l of the block-level tree: virtual warp l's sum (l < 8)
+        for (int vw = 0; vw < nvw; vw++) {
+            const int t = vw * 32 + lane;  // virtual thread
+            double acc = 0.0;
+            for (int j = A.ylo + b; j < A.yhi; j += NORM_BLOCKS)
+                for (int i = 1 + t; i <= A.nx; i += 256) {
+                    const long long p = j * P + i;
+                    double v;
+                    if (RESID && A.kind == 5) {
+                        double sacc = __dmul_rn(A.S[p], u[p - P]);
+                        sacc = __fma_rn(A.W[p], u[p - 1], sacc);
+                        sacc = __fma_rn(A.W[p + 1], u[p + 1], sacc);
+                        sacc = __fma_rn(A.S[p + P], u[p + P], sacc);
+                        v = f[p] - __fma_rn(A.O[p], u[p], sacc);
+                    } else if (RESID) {
+                        Row9 a = load_row9(A, p);
+                        v = f[p] - (a.o * u[p] + offdiag(a, u, p, P));
+                    } else {
+                        v = f[p];
+                    }
+                    acc += v * v;
+                }
+            for (int o = 16; o > 0; o >>= 1)
+                acc += __shfl_down_sync(0xffffffffu, acc, o);
+            const double s = __shfl_sync(0xffffffffu, acc, 0);
+            if (lane == vw)
+                ws = s;
+        }
+        for (int o = 16; o > 0; o >>= 1)
+            ws += __shfl_down_sync(0xffffffffu, ws, o);
+        if (lane == 0)
+            part[b] = ws;
+    }
+    __syncthreads();
+    __shared__ double tn_result;
+    if (w == 0) {
+        double ws = 0.0;
+        for (int vw = 0; vw < (nb + 31) / 32; vw++) {
+            const int k = vw * 32 + lane;
+            double acc = 0.0;
+            if (k < nb)
+                acc += part[k];
+            for (int o = 16; o > 0; o >>= 1)
+                acc += __shfl_down_sync(0xffffffffu, acc, o);
+            const double s = __shfl_sync(0xffffffffu, acc, 0);
+            if (lane == vw)
+                ws = s;
+        }
+        for (int o = 16; o > 0; o >>= 1)
+            ws += __shfl_down_sync(0xffffffffu, ws, o);
+        if (lane == 0)
+            tn_result = sqrt(ws);
+    }
+    __syncthreads();
+    return tn_result;
+}
+
+template <bool SOLVE>
+__device__ __forceinline__ void tail_sm_body(const TailPlan *__restrict__ tpg0, const double *f0, double *u0,
+                                             SolveState *st, double *hist)
 {
     extern __shared__ __align__(16) double tsm[];
 #ifdef BMG_TAIL_CLOCK
@@ -870,56 +945,95 @@ __global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail_sm(const TailPlan 
     auto F = [&](int l) { return tsm + tpg->lv[l].so_f; };
     auto R = [&](int l) { return tsm + tpg->lv[l].so_r; };
     auto DI = [&](int l) { return tsm + tpg->lv[l].so_di; };
-    for (int l = l0; l + 1 < L; l++) {
-        const Op A = opv(l);
-        const CIv ci = civ(l);
-        double *u = U(l), *r = R(l);
-        const double *f = F(l);
-        if (A.kind == 5)
-            tail_relax_sm<5>(A, DI(l), f, u, nu1, false);
-        else
-            tail_relax_sm<9>(A, DI(l), f, u, nu1, false);
-        // residual, ring 0 (rows by warp, columns by lane: no index division)
-        for (int j = ty; j <= A.ny + 1; j += ny_t)
-            for (int i = tx; i <= A.nx + 1; i += 32)
-                r[j * A.pitch + i] = (i == 0 || j == 0 || i > A.nx || j > A.ny) ? 0.0 : residual_pt(A, f, u, i, j);
-        __syncthreads();
-    TCLK();
-        for (int J = ty; J <= A.ny / 2 + 1; J += ny_t)
-            for (int I = tx; I <= A.nx / 2 + 1; I += 32)
-                restrict_store(A, ci, r, F(l + 1), U(l + 1), I, J, nu1 > 0);
-        __syncthreads();
-    TCLK();
-    }
-    {
-        const Op Ac = opv(L - 1);
-        if (Ac.nx * Ac.ny <= 32) {
-            if (threadIdx.x < 32)
-                coarse_solve_warp(Ac, tsm + tpg->so_chol, F(L - 1), U(L - 1));
-        } else {
-            coarse_solve_cta(Ac, tsm + tpg->so_chol, F(L - 1), U(L - 1), tsm + tpg->so_b);
+    // one V-cycle over the shared copies (down legs, coarsest solve, up legs)
+    auto run_cycle = [&]() {
+        for (int l = l0; l + 1 < L; l++) {
+            const Op A = opv(l);
+            const CIv ci = civ(l);
+            double *u = U(l), *r = R(l);
+            const double *f = F(l);
+            if (A.kind == 5)
+                tail_relax_sm<5>(A, DI(l), f, u, nu1, false);
+            else
+                tail_relax_sm<9>(A, DI(l), f, u, nu1, false);
+            // residual, ring 0 (rows by warp, columns by lane: no index division)
+            for (int j = ty; j <= A.ny + 1; j += ny_t)
+                for (int i = tx; i <= A.nx + 1; i += 32)
+                    r[j * A.pitch + i] = (i == 0 || j == 0 || i > A.nx || j > A.ny) ? 0.0 : residual_pt(A, f, u, i, j);
+            __syncthreads();
+        TCLK();
+            for (int J = ty; J <= A.ny / 2 + 1; J += ny_t)
+                for (int I = tx; I <= A.nx / 2 + 1; I += 32)
+                    restrict_store(A, ci, r, F(l + 1), U(l + 1), I, J, nu1 > 0);
+            __syncthreads();
+        TCLK();
         }
-    }
-    __syncthreads();
-    TCLK();
-    for (int l = L - 2; l >= l0; l--) {
-        const Op A = opv(l);
-        const CIv ci = civ(l);
-        double *u = U(l);
-        const double *e = U(l + 1);
-        for (int j = 1 + ty; j <= A.ny; j += ny_t)
-            for (int i = 1 + tx; i <= A.nx; i += 32) {
-                double s = interp_pt(ci, e, i, j);
-                if (affine)
-                    s += affine_pt(A, R(l), i, j);
-                u[j * A.pitch + i] += s;
+        {
+            const Op Ac = opv(L - 1);
+            if (Ac.nx * Ac.ny <= 32) {
+                if (threadIdx.x < 32)
+                    coarse_solve_warp(Ac, tsm + tpg->so_chol, F(L - 1), U(L - 1));
+            } else {
+                coarse_solve_cta(Ac, tsm + tpg->so_chol, F(L - 1), U(L - 1), tsm + tpg->so_b);
             }
+        }
         __syncthreads();
-    TCLK();
-        if (A.kind == 5)
-            tail_relax_sm<5>(A, DI(l), F(l), u, nu2, rev);
-        else
-            tail_relax_sm<9>(A, DI(l), F(l), u, nu2, rev);
+        TCLK();
+        for (int l = L - 2; l >= l0; l--) {
+            const Op A = opv(l);
+            const CIv ci = civ(l);
+            double *u = U(l);
+            const double *e = U(l + 1);
+            for (int j = 1 + ty; j <= A.ny; j += ny_t)
+                for (int i = 1 + tx; i <= A.nx; i += 32) {
+                    double s = interp_pt(ci, e, i, j);
+                    if (affine)
+                        s += affine_pt(A, R(l), i, j);
+                    u[j * A.pitch + i] += s;
+                }
+            __syncthreads();
+        TCLK();
+            if (A.kind == 5)
+                tail_relax_sm<5>(A, DI(l), F(l), u, nu2, rev);
+            else
+                tail_relax_sm<9>(A, DI(l), F(l), u, nu2, rev);
+        }
+    };
+    if (!SOLVE) {
+        run_cycle();
+    } else {
+        // bmg_solve with the whole hierarchy in this CTA (tail from level 0): ||rhs||, then
+        // cycles until ||r_k|| <= tol ||rhs|| or maxiter -- the host loop's test on the same
+        // doubles; the norms replicate launch_norm / launch_resid_norm's fixed reduction
+        // tree (tail_norm), so iterations, history and iterate are bitwise the graph loop's
+        const Op A0 = opv(l0);
+        const double fn = tail_norm<false>(A0, F(l0), U(l0), tsm + tpg->so_part);
+        double rn = 0.0;
+        int k = 0;
+        if (fn == 0.0) {  // b = 0 -> x = 0
+            for (int j = 1 + ty; j <= A0.ny; j += ny_t)
+                for (int i = 1 + tx; i <= A0.nx; i += 32)
+                    U(l0)[j * A0.pitch + i] = 0.0;
+            __syncthreads();
+        } else {
+            rn = tail_norm<true>(A0, F(l0), U(l0), tsm + tpg->so_part);
+            const double tol = st->tol;
+            const int maxiter = st->maxiter;
+            if (threadIdx.x == 0)
+                hist[0] = rn;
+            while (rn > tol * fn && k < maxiter) {
+                run_cycle();
+                k++;
+                rn = tail_norm<true>(A0, F(l0), U(l0), tsm + tpg->so_part);
+                if (threadIdx.x == 0)
+                    hist[k] = rn;
+            }
+        }
+        if (threadIdx.x == 0) {
+            st->fn = fn;
+            st->k = k;
+            hist[k] = rn;
+        }
     }
     // level l0's iterate back to its array
     {
@@ -941,6 +1055,20 @@ __global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail_sm(const TailPlan 
 #endif
 }
 
+
+__global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail_sm(const TailPlan *__restrict__ tpg0, const double *f0,
+                                                                 double *u0)
+{
+    tail_sm_body<false>(tpg0, f0, u0, nullptr, nullptr);
+}
+
+__global__ void __launch_bounds__(BMG_TAIL_THREADS, 1) k_tail_solve(const TailPlan *__restrict__ tpg0,
+                                                                    const double *f0, double *u0, SolveState *st,
+                                                                    double *hist)
+{
+    tail_sm_body<true>(tpg0, f0, u0, st, hist);
+}
+
 #ifdef BMG_TAIL_CLOCK
 extern "C" int bmg_debug_tail_clock(long long *out)
 {
@@ -950,6 +1078,18 @@ extern "C" int bmg_debug_tail_clock(long long *out)
     return n;
 }
 #endif
+
+void launch_tail_solve(const TailPlan *tp_dev, const double *f0, double *u0, SolveState *st, double *hist,
+                       cudaStream_t s, int sm_doubles)
+{
+    static std::once_flag once[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::call_once(once[dev & 63], []() {
+        cudaFuncSetAttribute(k_tail_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
+    });
+    k_tail_solve<<<1, BMG_TAIL_THREADS, sizeof(double) * sm_doubles, s>>>(tp_dev, f0, u0, st, hist);
+}
 
 void launch_tail(const TailPlan *tp_dev, int ncoarse, const double *f0, double *u0, cudaStream_t s, int sm_doubles)
 {

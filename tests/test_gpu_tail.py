@@ -60,3 +60,41 @@ def test_tail_sm_bitwise(wl, nx, ny, nu1, nu2, sym, affine):
     assert np.array_equal(t, _cycle(wl, nx, ny, 1, nu1, nu2, sym, affine, tail_sm=False))
     ps = _cycle(wl, nx, ny, 0, nu1, nu2, sym, affine)
     assert np.abs(t - ps).max() <= 1e-12 * np.abs(ps).max()
+
+
+def _solve(wl, nx, ny, tol, maxiter, one_launch, rhs_zero=False):
+    old = os.environ.get("BMG_TAIL_SOLVE")
+    os.environ["BMG_TAIL_SOLVE"] = "1" if one_launch else "0"
+    try:
+        s = bmg.Solver(P.workload(wl, nx, ny))
+        f = s.grid(np.zeros((ny + 2, nx + 2)) if rhs_zero else P.rhs_const(nx, ny))
+        x = s.grid(P.field_uniform(nx, ny, seed=3))
+        it, hist, rc = s.solve(f, x, tol, maxiter)
+        torch.cuda.synchronize()
+        out = (it, np.asarray(hist).copy(), rc, x.cpu().numpy())
+        s.close()
+        return out
+    finally:
+        if old is None:
+            del os.environ["BMG_TAIL_SOLVE"]
+        else:
+            os.environ["BMG_TAIL_SOLVE"] = old
+
+
+@pytest.mark.parametrize("wl,nx,ny,tol,maxiter", [("poisson", 31, 31, 1e-10, 100), ("aniso", 31, 31, 1e-8, 100),
+                                                  ("checker", 30, 17, 1e-10, 100), ("random9", 25, 32, 1e-9, 100),
+                                                  ("lognormal", 3, 40, 1e-10, 100), ("poisson", 31, 31, 1e-12, 3),
+                                                  ("poisson", 31, 31, 1e-8, 0)])
+def test_tail_solve_one_launch_bitwise_graph_loop(wl, nx, ny, tol, maxiter):
+    """bmg_solve with the whole hierarchy in the tail runs as ONE k_tail_solve launch
+    (norms in launch_resid_norm's reduction order): iterations, status, history and the
+    iterate bitwise the graph loop's (BMG_TAIL_SOLVE=0), incl. maxiter reached / 0."""
+    a = _solve(wl, nx, ny, tol, maxiter, True)
+    b = _solve(wl, nx, ny, tol, maxiter, False)
+    assert a[0] == b[0] and a[2] == b[2]
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[3], b[3])
+
+
+def test_tail_solve_zero_rhs():
+    it, hist, rc, x = _solve("poisson", 31, 31, 1e-10, 100, True, rhs_zero=True)
+    assert rc == 0 and it == 0 and hist[0] == 0.0 and np.all(x[1:-1, 1:32] == 0.0)
