@@ -266,8 +266,11 @@ def main():
     else:
         # a throwaway setup + cycle on a small grid first, so that the timed setup
         # (solve.setup_ms) does not include the one-time lazy loading of the kernels
-        warm = bmg.Solver(P.workload(wl, 255, 255), prm)
-        wf = warm.grid(P.rhs_const(255, 255))
+        # (1023^2: its level 0 plans the fused legs, whose first planning sets every fused
+        # instance's attributes -- ~0.1 s of module loading measured inside a timed setup)
+        wn = min(1023, nx, ny)
+        warm = bmg.Solver(P.workload(wl, wn, wn), prm)
+        wf = warm.grid(P.rhs_const(wn, wn))
         warm.vcycle(wf, warm.grid(), 1)
         torch.cuda.synchronize()
         warm.close()

@@ -109,8 +109,17 @@ if os.environ.get("WEAK", "1") == "1":
         si.close()
         slabs = t_lb - t_in
         t_p = slabs / nr + t_in + (2 * K + 1) * EXCH_US / 1e3
+        # peer mode, as for strong scaling above
+        d = D.DistSolver(stw, nr, 0, None, params=prm, loopback=True, peer=True)
+        a, b = d.local(fw), d.local()
+        t_pe = time_cycles(lambda: d.vcycle(a, b, 1), ncyc=10)
+        d.close()
+        del d, a, b
+        torch.cuda.empty_cache()
+        t_pp = (t_pe - t_in) / nr + t_in + 2 * EXCH_US / 1e3 + 2 * K * SIG_US / 1e3
         weak[f"p{nr}"] = {"global": [gx, gy], "kdist": K, "loopback_ms": t_lb, "inner_ms": t_in,
                           "slabs_per_gpu_ms": slabs / nr, "projected_ms": t_p,
-                          "projected_weak_efficiency": t1 / t_p}
+                          "projected_weak_efficiency": t1 / t_p, "peer_loopback_ms": t_pe,
+                          "peer_projected_ms": t_pp, "peer_projected_weak_efficiency": t1 / t_pp}
     out["weak_config5"] = weak
 print(json.dumps(out))
