@@ -95,6 +95,9 @@ struct bmg3_solver {
     int L = 0;
     std::vector<Level3> lv;
     std::vector<void *> allocs;
+    char *chunk = nullptr;  // bump allocator (alloc): current chunk, the bytes left in it,
+    size_t chunk_left = 0;  // the size of the next chunk (64 MB, doubling up to 1 GB)
+    size_t chunk_next = (size_t)64 << 20;
     double *chol = nullptr;
     int nco = 0;
     int *d_err = nullptr;
@@ -106,11 +109,26 @@ struct bmg3_solver {
 
 namespace {
 
+// Level arrays come from a bump allocator over large chunks (64 MB doubling up to 1 GB, or
+// one per larger array; 256-byte aligned pieces): the plane hierarchies alone ask for ~16
+// arrays per plane level and 3-D level, and a cudaMalloc each cost ~0.5 s of a 255^3
+// setup.  Every piece is zeroed, as before.
 bmg_status_t alloc(bmg3_solver *h, size_t ndouble, double **p, cudaStream_t s)
 {
-    void *q = nullptr;
-    CK(cudaMalloc(&q, ndouble * sizeof(double)));
-    h->allocs.push_back(q);
+    const size_t bytes = (ndouble * sizeof(double) + 255) / 256 * 256;
+    if (bytes > h->chunk_left) {
+        const size_t cb = bytes > h->chunk_next ? bytes : h->chunk_next;
+        if (h->chunk_next < ((size_t)1 << 30))
+            h->chunk_next *= 2;
+        void *q = nullptr;
+        CK(cudaMalloc(&q, cb));
+        h->allocs.push_back(q);
+        h->chunk = (char *)q;
+        h->chunk_left = cb;
+    }
+    void *q = h->chunk;
+    h->chunk += bytes;
+    h->chunk_left -= bytes;
     CK(cudaMemsetAsync(q, 0, ndouble * sizeof(double), s));
     *p = (double *)q;
     return BMG_OK;
