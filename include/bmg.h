@@ -133,6 +133,24 @@ bmg_status_t bmg_vcycle_host(bmg_solver_t h, const double *rhs_host, double *x_h
                              void *cuda_stream);
 
 /*
+ * bmg_vcycle_host for a batch of nprob INDEPENDENT problems on the same
+ * operator (fig:vcycle_flowchart P:108-162 applied to each): for each i,
+ * x_host[i] <- V^ncycles(x_host[i]) with right-hand side rhs_host[i].
+ * rhs_host, x_host: arrays of nprob HOST pointers (pinned for the copies to
+ * overlap; pageable works, serialised), each a grid function with the setup
+ * pitch; x_host[i] is read and overwritten, rhs_host[i] only read.  The
+ * arrays must not alias each other.  Pipelined over two device staging slots:
+ * problem i's host->device copies and problem i-1's device->host copy run on
+ * the handle's own copy streams while cuda_stream runs the cycles in between,
+ * so a batch is bound by the PCIe rate rather than copy + cycle + copy in
+ * series.  Results are bitwise those of bmg_vcycle_host per problem.  Returns
+ * after every copy completed (synchronises cuda_stream).  BMG_EINVAL: NULL
+ * arrays, nprob < 0, ncycles < 0, or a distributed handle.
+ */
+bmg_status_t bmg_vcycle_host_batch(bmg_solver_t h, int nprob, const double *const *rhs_host,
+                                   double *const *x_host, int ncycles, void *cuda_stream);
+
+/*
  * Solve loop: hist[0] = ||rhs - A x0||_2; repeat V-cycles
  * until ||r_k||_2 <= tol*||rhs||_2 or maxiter cycles.  ||rhs|| = 0 sets
  * x = 0 (interior) and returns 0 iterations.  iters_out (host, may be NULL)

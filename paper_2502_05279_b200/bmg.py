@@ -21,7 +21,7 @@ BMG_OK, BMG_EINVAL, BMG_ENOMEM, BMG_ECUDA, BMG_ENCCL, BMG_ENOTSPD, BMG_ENOTCONV 
 
 # Every symbol include/bmg.h declares (checked by tests/test_abi.py).
 EXPORTS = (
-    "bmg_params_default", "bmg_setup", "bmg_vcycle", "bmg_vcycle_host", "bmg_solve", "bmg_pcg", "bmg_residual_norm",
+    "bmg_params_default", "bmg_setup", "bmg_vcycle", "bmg_vcycle_host", "bmg_vcycle_host_batch", "bmg_solve", "bmg_pcg", "bmg_residual_norm",
     "bmg_num_levels", "bmg_level_shape", "bmg_level_pitch", "bmg_export_level", "bmg_relax", "bmg_residual",
     "bmg_restrict", "bmg_interp_add", "bmg_smooth_restrict", "bmg_correct_smooth", "bmg_cycle_kernel_count", "bmg_timing",
     "bmg_timing_read", "bmg_profile_legs", "bmg_setup_time", "bmg_destroy", "bmg_strerror",
@@ -78,6 +78,7 @@ def lib():
                               ctypes.POINTER(vp)]),
             "bmg_vcycle": (i, [vp, vp, vp, i, vp]),
             "bmg_vcycle_host": (i, [vp, vp, vp, i, vp]),
+            "bmg_vcycle_host_batch": (i, [vp, i, vp, vp, i, vp]),
             "bmg_solve": (i, [vp, vp, vp, d, i, ip, dp, vp]),
             "bmg_pcg": (i, [vp, vp, vp, d, i, ip, dp, vp]),
             "bmg_vcycle_block": (i, [vp, i, vp, vp, i, vp]),
@@ -156,6 +157,15 @@ def bmg_setup(planes, kind: int, nx: int, ny: int, pitch: int, params: bmg_param
 
 def bmg_vcycle(h, rhs, x, ncycles: int = 1, stream=None):
     _check(lib().bmg_vcycle(h, _ptr(rhs), _ptr(x), ncycles, _stream(stream)), "bmg_vcycle")
+
+
+def bmg_vcycle_host_batch(h, rhs_hosts, x_hosts, ncycles: int = 1, stream=None):
+    """bmg_vcycle_host_batch: lists of host tensors/arrays (pinned for overlap), one problem each."""
+    n = len(rhs_hosts)
+    assert len(x_hosts) == n
+    ra = (ctypes.c_void_p * max(n, 1))(*[_ptr(a).value for a in rhs_hosts])
+    xa = (ctypes.c_void_p * max(n, 1))(*[_ptr(a).value for a in x_hosts])
+    _check(lib().bmg_vcycle_host_batch(h, n, ra, xa, ncycles, _stream(stream)), "bmg_vcycle_host_batch")
 
 
 def bmg_vcycle_host(h, rhs_host, x_host, ncycles: int = 1, stream=None):

@@ -144,6 +144,13 @@ bmg_status_t bmg_destroy(bmg_solver_t h)
             cudaEventDestroy(e);
     if (h->cap)
         cudaStreamDestroy(h->cap);
+    for (cudaEvent_t e : h->hb_ev)
+        if (e)
+            cudaEventDestroy(e);
+    if (h->hb_in)
+        cudaStreamDestroy(h->hb_in);
+    if (h->hb_out)
+        cudaStreamDestroy(h->hb_out);
     delete h;
     return BMG_OK;
 }
@@ -805,6 +812,58 @@ bmg_status_t bmg_vcycle_host(bmg_solver_t h, const double *rhs_host, double *x_h
     CK(cudaMemcpyAsync(h->stage_x, x_host, bytes, cudaMemcpyHostToDevice, s));
     TRY(bmg_vcycle(h, h->stage_f, h->stage_x, ncycles, cuda_stream));
     CK(cudaMemcpyAsync(x_host, h->stage_x, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return BMG_OK;
+}
+
+// nprob independent problems with host data, pipelined over two device staging slots:
+// problem i's host->device copies (stream hb_in) and problem i-1's device->host copy
+// (stream hb_out) overlap the cycles of the problem in between (cuda_stream), so the
+// batch runs at the PCIe rate instead of copy + compute + copy in series.
+bmg_status_t bmg_vcycle_host_batch(bmg_solver_t h, int nprob, const double *const *rhs_host,
+                                   double *const *x_host, int ncycles, void *cuda_stream)
+{
+    join_pcg(h, (cudaStream_t)cuda_stream);
+    if (!h || nprob < 0 || (nprob > 0 && (!rhs_host || !x_host)) || ncycles < 0 || h->dist)
+        return fail(BMG_EINVAL, "bad arguments to bmg_vcycle_host_batch (not for distributed handles)");
+    for (int i = 0; i < nprob; i++)
+        if (!rhs_host[i] || !x_host[i])
+            return fail(BMG_EINVAL, "bmg_vcycle_host_batch: NULL host array");
+    Level &v = h->lv[0];
+    const size_t bytes = (size_t)(v.ny + 2) * v.pitch * sizeof(double);
+    if (!h->stage_f) {
+        TRY(dalloc(h, &h->stage_f, bytes / sizeof(double)));
+        TRY(dalloc(h, &h->stage_x, bytes / sizeof(double)));
+    }
+    if (!h->stage_f2) {
+        TRY(dalloc(h, &h->stage_f2, bytes / sizeof(double)));
+        TRY(dalloc(h, &h->stage_x2, bytes / sizeof(double)));
+        CK(cudaStreamCreateWithFlags(&h->hb_in, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&h->hb_out, cudaStreamNonBlocking));
+        for (cudaEvent_t &e : h->hb_ev)
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    double *fs[2] = {h->stage_f, h->stage_f2}, *xs[2] = {h->stage_x, h->stage_x2};
+    cudaEvent_t *in_done = h->hb_ev, *cyc_done = h->hb_ev + 2, *out_done = h->hb_ev + 4;
+    // the slots are free of earlier work on cuda_stream before the first copy into them
+    CK(cudaEventRecord(cyc_done[0], s));
+    CK(cudaStreamWaitEvent(h->hb_in, cyc_done[0], 0));
+    for (int i = 0; i < nprob; i++) {
+        const int k = i & 1;
+        if (i >= 2)  // slot k's previous result has left (its D2H waited for its cycle)
+            CK(cudaStreamWaitEvent(h->hb_in, out_done[k], 0));
+        CK(cudaMemcpyAsync(fs[k], rhs_host[i], bytes, cudaMemcpyHostToDevice, h->hb_in));
+        CK(cudaMemcpyAsync(xs[k], x_host[i], bytes, cudaMemcpyHostToDevice, h->hb_in));
+        CK(cudaEventRecord(in_done[k], h->hb_in));
+        CK(cudaStreamWaitEvent(s, in_done[k], 0));
+        TRY(bmg_vcycle(h, fs[k], xs[k], ncycles, cuda_stream));
+        CK(cudaEventRecord(cyc_done[k], s));
+        CK(cudaStreamWaitEvent(h->hb_out, cyc_done[k], 0));
+        CK(cudaMemcpyAsync(x_host[i], xs[k], bytes, cudaMemcpyDeviceToHost, h->hb_out));
+        CK(cudaEventRecord(out_done[k], h->hb_out));
+    }
+    CK(cudaStreamSynchronize(h->hb_out));
     CK(cudaStreamSynchronize(s));
     return BMG_OK;
 }

@@ -102,6 +102,9 @@ struct bmg_solver {
     double *partials = nullptr, *d_norm = nullptr, *h_norm = nullptr;  // h_norm: a pinned slot (pinned_slot)
     cudaEvent_t setup_ev[2] = {nullptr, nullptr};  // around the S0-S3 kernels (bmg_setup_time)
     double *stage_f = nullptr, *stage_x = nullptr;                     // bmg_vcycle_host staging
+    double *stage_f2 = nullptr, *stage_x2 = nullptr;                   // bmg_vcycle_host_batch: 2nd slot
+    cudaStream_t hb_in = nullptr, hb_out = nullptr;                    // its copy streams
+    cudaEvent_t hb_ev[6] = {};                                         // in/compute/out done per slot
     cudaStream_t cap = nullptr;                                        // capture stream
     std::map<std::pair<const void *, const void *>, GraphRec> graphs, tgraphs;  // plain / timed
     cudaEvent_t cev[2] = {nullptr, nullptr};  // placeholders captured into timed graphs

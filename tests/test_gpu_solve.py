@@ -60,3 +60,22 @@ def test_device_loop_reuse_and_limits():
     it3, h3, rc3 = s.solve(f, x, 1e-8, 2000)  # a larger history than the first allocation
     assert rc3 == 0 and it3 == it0 and np.array_equal(h3, h0)
     s.close()
+
+
+def test_vcycle_host_batch_bitwise_per_problem():
+    """bmg_vcycle_host_batch (include/bmg.h): each problem's result is bitwise that of
+    bmg_vcycle_host on the same host arrays, with copies overlapping across problems
+    (pinned) -- 5 problems, two staging slots reused, distinct rhs and starts."""
+    n = 255
+    s = bmg.Solver(P.workload("checker", n, n))
+    rhs = [P.field_uniform(n, n, seed=10 + i) for i in range(5)]
+    x0 = [P.field_uniform(n, n, seed=20 + i) for i in range(5)]
+    fh = [s.grid(a).cpu().pin_memory() for a in rhs]
+    xb = [s.grid(a).cpu().pin_memory() for a in x0]
+    bmg.bmg_vcycle_host_batch(s.h, fh, xb, 2)
+    for i in range(5):
+        xr = s.grid(x0[i]).cpu().pin_memory()
+        bmg.bmg_vcycle_host(s.h, fh[i], xr, 2)
+        assert torch.equal(xb[i], xr), i
+    bmg.bmg_vcycle_host_batch(s.h, [], [], 1)  # empty batch: a no-op
+    s.close()
