@@ -1260,25 +1260,22 @@ static void plan_grid(FusedGeom &g, int nx, int ny, int warm)
     const int slots = dv.sms * occ;
     g.nstrips = nx / g.TX + 1;
     double best = 1e300;
-    for (int w = 1; w <= 32; w++)
-        // the rounded chunk count, and the one rounded down: rounding up can overshoot the
-        // w-wave slot count by a few CTAs and cost a whole extra wave (1023^2: 5 strips x 30
-        // chunks = 150 CTAs on 148 slots)
-        for (int down = 0; down < 2; down++) {
-            int nch = std::max(1, (int)((double)w * slots / g.nstrips + (down ? 0.0 : 0.5)));
-            nch = std::min(nch, std::max(1, (ny + 1) / 8));
-            int chunk = (ny + 1 + nch - 1) / nch;
-            nch = (ny + 1 + chunk - 1) / chunk;
-            long long units = (long long)g.nstrips * nch;
-            long long waves = (units + slots - 1) / slots;
-            double cost = (double)waves * (chunk + warm + 8);
-            if (cost < best) {
-                best = cost;
-                g.nchunks = nch;
-                g.chunk = chunk;
-                g.ok = true;
-            }
+    // every chunk count (at most (ny+1)/8): the cost model is cheap, and rounding a per-wave
+    // count can overshoot the slots by a few CTAs and cost a whole extra wave (1023^2: 5
+    // strips x 30 chunks = 150 CTAs on 148 slots)
+    for (int nc = 1; nc <= std::max(1, (ny + 1) / 8); nc++) {
+        const int chunk = (ny + 1 + nc - 1) / nc;
+        const int nch = (ny + 1 + chunk - 1) / chunk;
+        const long long units = (long long)g.nstrips * nch;
+        const long long waves = (units + slots - 1) / slots;
+        const double cost = (double)waves * (chunk + warm + 8);
+        if (cost < best) {
+            best = cost;
+            g.nchunks = nch;
+            g.chunk = chunk;
+            g.ok = true;
         }
+    }
 }
 
 bmg_status_t fused_plan_level(FusedPlan &fp, int l, int nx, int ny, long long pitch, int kind, int nu1, int nu2,
