@@ -1268,7 +1268,10 @@ static void plan_grid(FusedGeom &g, int nx, int ny, int warm)
         const int nch = (ny + 1 + chunk - 1) / chunk;
         const long long units = (long long)g.nstrips * nch;
         const long long waves = (units + slots - 1) / slots;
-        const double cost = (double)waves * (chunk + warm + 8);
+#ifndef BMG_PLAN_K
+#define BMG_PLAN_K 0  // per-CTA fixed cost in row steps beyond the warm-up (swept 0/8/16/32: 0 best at 8191^2, others within 0.1 %)
+#endif
+        const double cost = (double)waves * (chunk + warm + BMG_PLAN_K);
         if (cost < best) {
             best = cost;
             g.nchunks = nch;
