@@ -7,6 +7,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <climits>
 #include <mutex>
 #include <cstdlib>
 #include <utility>
@@ -603,7 +604,7 @@ __global__ void __launch_bounds__(32 * RB_TY) k3_rb7(Op3 A, const double *__rest
 // only compute (k3_rb7 re-read halo and next-plane data through L1/L2, 1.42x the
 // arrays from DRAM; the cp.async variant was issue-bound, tools/archive/k3_rb7s.cu.txt).
 namespace rbt {
-constexpr int TX = 64, TY = 6, KC = 32, NT = 32 * TY;
+constexpr int TX = 64, TY = 6, NT = 32 * TY;  // z-chunk (planes per CTA): planned per launch
 constexpr int UX = TX + 6, UY = TY + 4;  // u_in box: origin (i0-3, j0-2) (TMA needs a 16-B aligned x start)
 constexpr int RX = TX + 2, RY = TY + 2;  // f, O, B, red: origin (i0-1, j0-1)
 constexpr int WX = TX + 4;               // W box: 68 wide (16-B multiple), origin (i0-1, j0-1)
@@ -647,7 +648,7 @@ __device__ __forceinline__ void mb_wait(unsigned long long *bar, unsigned parity
 
 template <bool RCP>
 __global__ void __launch_bounds__(rbt::NT, 2) k3_rb7t(Op3 A, double *__restrict__ uout,
-                                                      const __grid_constant__ Maps7 M)
+                                                      const __grid_constant__ Maps7 M, int KC)
 {
     using namespace rbt;
     extern __shared__ __align__(1024) double sm[];
@@ -788,13 +789,34 @@ bool launch3_rb7t(const Op3 &A, const double *f, const double *uin, double *uout
         !map3(&M.w, A.a[12], A.g, WX, RY) || !map3(&M.s, A.a[10], A.g, RX, SY) || !map3(&M.b, A.a[4], A.g, RX, RY))
         return false;
     const size_t smem = sizeof(double) * TOTAL + 16;
+    // z-chunk: the fewest waves x (planes + 2 warm-up) over 2 CTAs per SM (the 2-D planner's
+    // model, DESIGN §5.2/§5.8): at 255^3 172 column tiles x 5 chunks of 51 planes = 3 waves
+    // (a fixed 32 planes gave 8 chunks = 4.65 waves; measured 1.865 -> 1.831 ms per cycle)
+    int sms = 148;
+    {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+            sms = v;
+    }
+    const long long cols = (long long)((A.g.nx + TX - 1) / TX) * ((A.g.ny + TY - 1) / TY), slots = 2LL * sms;
+    int KC = A.g.nz, best_cost = INT_MAX;
+    for (int nzc = 1; nzc <= A.g.nz; nzc++) {
+        const int kc = (A.g.nz + nzc - 1) / nzc;
+        const long long waves = (cols * ((A.g.nz + kc - 1) / kc) + slots - 1) / slots;
+        const long long cost = waves * (kc + 2);
+        if (cost < best_cost) {
+            best_cost = (int)cost;
+            KC = kc;
+        }
+    }
     dim3 grid((A.g.nx + TX - 1) / TX, (A.g.ny + TY - 1) / TY, (A.g.nz + KC - 1) / KC);
     if (ro) {
         cudaFuncSetAttribute(k3_rb7t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k3_rb7t<true><<<grid, dim3(32, TY), smem, s>>>(A, uout, M);
+        k3_rb7t<true><<<grid, dim3(32, TY), smem, s>>>(A, uout, M, KC);
     } else {
         cudaFuncSetAttribute(k3_rb7t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k3_rb7t<false><<<grid, dim3(32, TY), smem, s>>>(A, uout, M);
+        k3_rb7t<false><<<grid, dim3(32, TY), smem, s>>>(A, uout, M, KC);
     }
     return true;
 }
